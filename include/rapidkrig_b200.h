@@ -1,0 +1,186 @@
+/*
+ * rapidkrig_b200 — C ABI of the B200-native rapid-Kriging hot path.
+ *
+ * Drop-in boundary for the reference package rapidkrig 0.1.0
+ * (/root/reference/pkg/src/rapidkrig).  The reference has no FFI of its own:
+ * its boundary is the Python API re-exported at __init__.py:16-49.  Each entry
+ * point below replaces the reference function cited beside it; the Python
+ * package paper_2605_29284_b200 binds them with ctypes under the reference's
+ * names and signatures.
+ *
+ * Conventions
+ *   - plain C types only; device pointers are `const double*` etc. that the
+ *     caller allocated on the current CUDA device; `void* stream` is a
+ *     cudaStream_t (NULL = legacy default stream).
+ *   - every function returns an rk_status; on failure rk_last_error() holds a
+ *     thread-local message.  Status -> exception mapping mirrors errors.py:4-17:
+ *     RK_DOMAIN -> DomainError, RK_NUMERIC -> NumericError,
+ *     RK_INTERNAL -> InternalError, RK_CUDA -> RapidKrigError.
+ *   - arrays are row-major [iy, ix] with x fastest (gridding.py:6-8).
+ *   - handles are immutable after creation; concurrent calls on different
+ *     streams are safe (rapid.py:140-144).
+ */
+#ifndef RAPIDKRIG_B200_H
+#define RAPIDKRIG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum rk_status {
+  RK_OK = 0,
+  RK_DOMAIN = 1,    /* errors.py:8  DomainError   */
+  RK_NUMERIC = 2,   /* errors.py:12 NumericError  */
+  RK_INTERNAL = 3,  /* errors.py:16 InternalError */
+  RK_CUDA = 4       /* device failure (RapidKrigError) */
+} rk_status;
+
+/* CovarianceModel (covariance.py:50-89) plus the host-computed constants of
+ * bessel.py (half-integer Horner coefficients 224-234, Temme gammas 37-47,
+ * Gamma(nu) 255) so device arithmetic follows the reference's constants. */
+typedef struct rk_model {
+  double sigma2, alpha, nu, tau2;
+  int32_t half_n;          /* n for nu = n + 1/2 (bessel.py:216-221), else -1 */
+  int32_t nl;              /* int(nu + 0.5) (bessel.py:245) */
+  double half_coef[13];    /* (n+i)!/(i!(n-i)!), i ascending */
+  double half_pref;        /* n!/(2n)! */
+  double mu;               /* nu - nl */
+  double temme_gampl, temme_gammi, temme_gam1, temme_gam2, temme_fact;
+  double gamma_nu;         /* math.gamma(nu) */
+} rk_model;
+
+/* PaddedGrid (gridding.py:38-111) */
+typedef struct rk_grid {
+  double x0, y0;           /* interior origin */
+  double hx, hy;           /* spacing */
+  int32_t m1, m2;          /* interior dims */
+  int32_t pad[4];          /* left, right, bottom, top */
+} rk_grid;
+
+typedef struct rk_setup rk_setup;   /* device-resident RapidSetup (rapid.py:138-174) */
+typedef struct rk_fit rk_fit;       /* device-resident KrigingFit (exact.py:40-56)  */
+
+/* ---- library ------------------------------------------------------------ */
+const char* rk_last_error(void);
+int32_t rk_version(void);
+/* number of kernels this library launched on the calling thread so far */
+int64_t rk_launch_count(void);
+
+/* ---- L0: Matern correlation (bessel.py:258-278 via covariance.py:83-89) --- */
+/* out[i] = sigma2 * phi(alpha * d[i]); d, out device arrays of length n */
+rk_status rk_matern_cov(const rk_model* model, const double* d_dev, double* out_dev,
+                        int64_t n, void* stream);
+
+/* ---- L1: padded grid (gridding.py:130-178) ------------------------------ */
+/* obs_host: (n, 2) host array; fills grid (origin, spacing, dims, pads) */
+rk_status rk_build_padded_grid(const double domain[4], int32_t m1, int32_t m2, int32_t L,
+                               const double* obs_host, int64_t n, rk_grid* grid_out);
+
+/* ---- L2: rapid setup (rapid.py:177-230) --------------------------------- */
+/* Builds K_N and its Cholesky (rapid.py:112-135), stencil base indices
+ * (gridding.py:181-205), weights + conditional variance (rapid.py:202-225)
+ * and the filter spectrum (rapid.py:72-86), all device resident.
+ * *ridge_applied = 1 when the K_N ridge retry fired (RuntimeWarning upstream). */
+rk_status rk_build_setup(const rk_model* model, const rk_grid* grid, int32_t L,
+                         const double* obs_host, int64_t n, rk_setup** out,
+                         int32_t* ridge_applied);
+/* Observation-free setup: filter spectrum (rapid.py:72-86) and, on demand, the
+ * circulant embedding (simulate.py:82-100) for a (model, grid) pair.  Serves
+ * build_filter_spectrum and sim_unconditional_grid, which take no observations. */
+rk_status rk_grid_setup_create(const rk_model* model, const rk_grid* grid, rk_setup** out);
+rk_status rk_setup_destroy(rk_setup* s);
+/* n_obs, L, embed dims (p1, p2), padded dims (M1, M2) */
+rk_status rk_setup_info(const rk_setup* s, int64_t* n_obs, int32_t* L, int32_t embed[2],
+                        int32_t total[2]);
+/* Materialise the RapidSetup fields on the host (any pointer may be NULL):
+ * neighbor_indices (n, M) int64, weights (n, M), cond_var (n), kn_inv (M, M). */
+rk_status rk_setup_copy_out(const rk_setup* s, int64_t* indices_host, double* weights_host,
+                            double* cond_var_host, double* kn_inv_host);
+/* Filter spectrum real part, full (p2, p1) layout, UNSCALED like np.fft.fft2
+ * (rapid.py:86); imaginary part is zero for the even lag filter. */
+rk_status rk_setup_copy_spectrum(const rk_setup* s, double* spectrum_host);
+
+/* ---- L2: rapid predict (rapid.py:164-174, 89-100, 233-261) -------------- */
+/* c* = A' c  (RapidSetup.coefficients_to_grid, rapid.py:164-174); device arrays */
+rk_status rk_coefficients_to_grid(const rk_setup* s, const double* c_dev, double* cstar_dev,
+                                  void* stream);
+/* convolve_filter (rapid.py:89-100) of a padded (M2, M1) device field with the
+ * setup's spectrum; out (M2, M1) */
+rk_status rk_convolve_filter(const rk_setup* s, const double* values_dev, double* out_dev,
+                             void* stream);
+/* convolve_filter (rapid.py:89-100) with a caller-supplied real-even spectrum in
+ * quarter form spec_q[kx * (p2/2+1) + ky] = Re S[ky, kx] / (p1 p2), kx <= p1/2,
+ * ky <= p2/2 (device); values/out (M2, M1) device. */
+rk_status rk_convolve_spectrum(const double* spec_q_dev, int32_t p1, int32_t p2,
+                               const double* values_dev, int32_t M1, int32_t M2, double* out_dev,
+                               void* stream);
+/* predict_rapid (rapid.py:252-261), device pointers.  beta_dev may be NULL
+ * (no fixed part); p = len(beta); xg_dev (m1*m2, p) row-major or NULL
+ * (then p must be 1: scalar beta[0]).  out_dev (m2, m1). */
+rk_status rk_predict_dev(const rk_setup* s, const double* c_dev, const double* beta_dev,
+                         int32_t p, const double* xg_dev, double* out_dev, void* stream);
+/* Same call on HOST buffers: H2D of c / beta / xg, compute, D2H of the field,
+ * synchronous on `stream`. */
+rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta, int32_t p,
+                          const double* xg, double* out, void* stream);
+
+/* ---- L2: exact fit / refit (exact.py:71-113) ---------------------------- */
+/* GPU fit: M = K + tau2 I (covariance.py:100-116), Cholesky with ridge retry
+ * (exact.py:25-37), GLS (exact.py:59-68).  X_host (n, p) row-major or NULL. */
+rk_status rk_fit_create(const rk_model* model, const double* obs_host, int64_t n,
+                        const double* z_host, const double* X_host, int32_t p, rk_fit** out,
+                        int32_t* ridge_applied);
+/* Adopt a host KrigingFit (reference object): chol_M (n, n) lower row-major,
+ * X (n, p), beta (p), c (n). */
+rk_status rk_fit_import(const rk_model* model, const double* obs_host, int64_t n,
+                        const double* X_host, int32_t p, const double* chol_host,
+                        const double* beta_host, const double* c_host, rk_fit** out);
+rk_status rk_fit_destroy(rk_fit* f);
+/* copies out beta (p), c (n), chol_M (n, n lower, row-major); NULL skips */
+rk_status rk_fit_copy_out(const rk_fit* f, double* beta_host, double* c_host, double* chol_host);
+rk_status rk_fit_info(const rk_fit* f, int64_t* n, int32_t* p);
+/* refit_coefficients (exact.py:108-113) for `batch` right-hand sides:
+ * z_dev (batch, n) -> beta_dev (batch, p), c_dev (batch, n) */
+rk_status rk_refit_dev(const rk_fit* f, const double* z_dev, int64_t batch, double* beta_dev,
+                       double* c_dev, void* stream);
+
+/* ---- L3: conditional simulation (simulate.py:52-192) -------------------- */
+/* seed ^ splitmix64(j)  (simulate.py:52-62) */
+uint64_t rk_draw_seed(uint64_t seed, uint64_t j);
+/* Standard normals from the Philox4x64-10 stream keyed (seed, stream), words
+ * [start, start+count) (simulate.py:65-74) -> device out */
+rk_status rk_philox_normals(uint64_t seed, uint64_t stream_id, uint64_t start, int64_t count,
+                            double* out_dev, void* stream);
+/* raw Philox words (for bit-exactness tests) */
+rk_status rk_philox_raw(uint64_t seed, uint64_t stream_id, uint64_t start, int64_t count,
+                        uint64_t* out_dev, void* stream);
+/* circulant embedding (simulate.py:82-100): dims after the PSD check / doubling.
+ * Fails with RK_NUMERIC ("... most negative eigenvalue ...") if still indefinite. */
+rk_status rk_setup_embedding(rk_setup* s, int32_t embed_out[2], int32_t* doubled);
+/* sim_unconditional_grid (simulate.py:103-118): field_dev (M2, M1) */
+rk_status rk_sim_unconditional_dev(rk_setup* s, uint64_t seed, double* field_dev, void* stream);
+/* sim_obs_local (simulate.py:121-143): field_dev (M2, M1) -> z_dev (n) */
+rk_status rk_sim_obs_local_dev(const rk_setup* s, double tau2, const double* field_dev,
+                               uint64_t seed, double* z_dev, void* stream);
+/* Ensemble slice (simulate.py:146-192): realizations j in [j0, j0+count) with
+ * sub-seeds draw_seed(seed, j).  Adds, in j order and per pixel,
+ *   e_j = interior(g_j) - predict_rapid(c_sim_j, beta_sim_j)
+ * into s1_dev += e, s2_dev += e*e (m2*m1 each, caller-zeroed per chunk).
+ * draw_j = data_pred + e_j is written to draws_dev (count, m2, m1) if non-NULL.
+ * xg_dev / p as in rk_predict_dev (p = fit's covariate count). */
+rk_status rk_ensemble_accumulate(rk_setup* s, const rk_fit* f, uint64_t seed, int64_t j0,
+                                 int64_t count, const double* xg_dev,
+                                 const double* data_pred_dev, double* s1_dev, double* s2_dev,
+                                 double* draws_dev, int32_t batch, void* stream);
+/* mean = data_pred + s1/R ; se = sqrt((s2 - s1*s1/R)/(R-1)) (simulate.py:191-192) */
+rk_status rk_ensemble_finalize(int64_t n_pix, int64_t n_draws, const double* data_pred_dev,
+                               const double* s1_dev, const double* s2_dev, double* mean_dev,
+                               double* se_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RAPIDKRIG_B200_H */

@@ -1,0 +1,802 @@
+// rapidkrig B200: library infrastructure, padded grid, rapid setup.
+//
+// Reference mapping (/root/reference/pkg/src/rapidkrig):
+//   build_padded_grid   gridding.py:130-178   -> rk_build_padded_grid / pad_kernel
+//   neighborhood        gridding.py:181-205   -> weights_kernel (stencil part)
+//   neighbor_cov        rapid.py:103-117      -> host kn_matrix (M x M, tiny)
+//   _factor_neighbor_cov rapid.py:120-135     -> host cholesky_lower with ridge retry
+//   build_setup         rapid.py:177-230      -> rk_build_setup (weights_kernel + sort +
+//                                                spectrum_quarter)
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "rk_internal.cuh"
+
+namespace rk {
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local std::string g_err;
+thread_local int g_code = RK_OK;
+thread_local int64_t g_launches = 0;
+}  // namespace
+
+void set_error(int code, const std::string& msg) {
+  g_code = code;
+  g_err = msg;
+}
+int last_code() { return g_code; }
+void count_launch(int k) { g_launches += k; }
+
+static int finish(const Status& s) {
+  if (!s.good()) set_error(s.code, s.msg);
+  return s.code;
+}
+
+// ------------------------------------------------------------------- plans
+bool fft_factor(int n, FftPlan* pl) {
+  int a = 0, b = 0, m = n;
+  if (n < 1) return false;
+  while (m % 2 == 0) { m /= 2; ++a; }
+  while (m % 3 == 0) { m /= 3; ++b; }
+  if (m != 1) return false;
+  std::vector<int> r;
+  pl->n9 = b / 2;
+  b -= 2 * pl->n9;
+  pl->r3 = 1;
+  if (b == 1) {
+    if (a >= 1) { pl->r3 = 6; a -= 1; } else { pl->r3 = 3; }
+  }
+  pl->n8 = a / 3;
+  a -= 3 * pl->n8;
+  pl->r2 = a == 2 ? 4 : a == 1 ? 2 : 1;
+  for (int i = 0; i < pl->n9; ++i) r.push_back(9);
+  if (pl->r3 > 1) r.push_back(pl->r3);
+  for (int i = 0; i < pl->n8; ++i) r.push_back(8);
+  if (pl->r2 > 1) r.push_back(pl->r2);
+  pl->n = n;
+  pl->nstages = (int)r.size();
+  int need = 1;
+  for (size_t i = 0; i < r.size(); ++i) {
+    const int nb = n / r[i];
+    const int k = fft_kmax(r[i]);
+    need = std::max(need, (nb + k - 1) / k);
+  }
+  pl->nthr = std::max(32, (need + 31) / 32 * 32);
+  return true;
+}
+
+namespace {
+std::mutex g_plan_mu;
+std::map<std::pair<int, int>, FftPlan> g_plans;
+std::map<std::pair<int, const void*>, bool> g_smem_set;
+}  // namespace
+
+Status plan_for(int n, FftPlan* out) {
+  int dev = 0;
+  RK_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto key = std::make_pair(dev, n);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) {
+    *out = it->second;
+    return Status::ok();
+  }
+  FftPlan pl{};
+  if (!fft_factor(n, &pl))
+    return Status::err(RK_INTERNAL, "FFT length " + std::to_string(n) + " is not 2^a 3^b");
+  if (pl.nthr > 512)
+    return Status::err(RK_DOMAIN, "FFT length " + std::to_string(n) + " too large for one CTA");
+  std::vector<double2> tw(n);
+  const long double PI_L = 3.141592653589793238462643383279502884L;
+  for (int t = 0; t < n; ++t) {
+    const long double ang = 2.0L * PI_L * (long double)t / (long double)n;
+    tw[t] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+  }
+  double2* d = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&d, sizeof(double2) * n));
+  RK_CUDA_TRY(cudaMemcpy(d, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+  pl.tw = d;
+  g_plans[key] = pl;
+  *out = pl;
+  return Status::ok();
+}
+
+int pick_lpc(const FftPlan& pl, int max_lines) {
+  const size_t line_bytes = (size_t)pl.n * sizeof(double2);
+  int lpc = std::max(1, max_lines);
+  while (lpc > 1 && ((size_t)lpc * line_bytes > 96 * 1024 || lpc * pl.nthr > 512)) --lpc;
+  return lpc;
+}
+
+Status set_smem_attr(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return Status::ok();
+  int dev = 0;
+  RK_CUDA_TRY(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    if (g_smem_set.count({dev, fn})) return Status::ok();
+  }
+  RK_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  g_smem_set[{dev, fn}] = true;
+  return Status::ok();
+}
+
+Status scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static bool pool_cfg = false;
+  if (!pool_cfg) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_cfg = true;
+  }
+  RK_CUDA_TRY(cudaMallocAsync(p, bytes ? bytes : 16, st));
+  return Status::ok();
+}
+
+void scratch_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
+// ------------------------------------------------------------ Matern ABI
+__global__ void matern_kernel(MaternDev P, const double* __restrict__ d, double* __restrict__ out,
+                              int64_t n, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = matern_cov(P, d[i], bad);
+}
+
+// ------------------------------------------------------------- padded grid
+// cells with the floor tie rule and 1e-9 snap (gridding.py:123-127)
+__device__ __forceinline__ int snap_cell(double t) {
+  const double r = rint(t);
+  return fabs(__dsub_rn(t, r)) <= 1.0e-9 ? (int)r : (int)floor(t);
+}
+
+struct PadArgs {
+  const double* obs;
+  int64_t n;
+  double x0, y0, hx, hy;
+  double lox, hix, loy, hiy;   // inclusive domain bounds with 1e-9 h slack
+  int L, m1, m2;
+  int* out;                    // [0] first bad index, [1..4] max(L-1-cx), max(cx+L-(m1-1)), ...
+};
+
+__global__ void pad_kernel(PadArgs a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = a.obs[2 * i], y = a.obs[2 * i + 1];
+    if (!(x >= a.lox && x <= a.hix && y >= a.loy && y <= a.hiy)) {
+      atomicMin(&a.out[0], (int)i);
+      continue;
+    }
+    const int cx = snap_cell(__ddiv_rn(__dsub_rn(x, a.x0), a.hx));
+    const int cy = snap_cell(__ddiv_rn(__dsub_rn(y, a.y0), a.hy));
+    atomicMax(&a.out[1], (a.L - 1) - cx);
+    atomicMax(&a.out[2], cx + a.L - (a.m1 - 1));
+    atomicMax(&a.out[3], (a.L - 1) - cy);
+    atomicMax(&a.out[4], cy + a.L - (a.m2 - 1));
+  }
+}
+
+// --------------------------------------------------------------- weights
+// One warp per observation (rapid.py:202-225): stencil (gridding.py:181-205),
+// k_i = sigma2 phi(alpha |node - obs|), w = K_N^-1 k_i by forward/back
+// substitution against the shared lower factor (in shared memory), cond_var,
+// on-node unit rows and the cond_var clamp.
+struct WArgs {
+  MaternDev P;
+  const double* obs;
+  int64_t n;
+  double px0, py0, hx, hy;
+  double hix, hiy;             // (M1 - 1) + 1e-9, (M2 - 1) + 1e-9
+  int L, bs, M, M1, M2;
+  const double* chol;          // (M, M) row-major lower (global)
+  int32_t* base;
+  double* weights;
+  double* cond_var;
+  int* err;                    // [0] domain idx, [1] internal idx, [2] bessel
+};
+
+template <int MPL>
+__global__ void __launch_bounds__(256) weights_kernel(WArgs a) {
+  extern __shared__ double wsm[];
+  const int M = a.M;
+  const bool smem_l = M <= 64;
+  double* Lr = wsm;            // row-major
+  double* Lc = wsm + M * M;    // column-major
+  if (smem_l) {
+    for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
+      const int r = e / M, c = e % M;
+      const double v = a.chol[e];
+      Lr[e] = v;
+      Lc[c * M + r] = v;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * wpb + warp; i < a.n; i += (int64_t)gridDim.x * wpb) {
+    const double x = a.obs[2 * i], y = a.obs[2 * i + 1];
+    const double tx = __ddiv_rn(__dsub_rn(x, a.px0), a.hx);
+    const double ty = __ddiv_rn(__dsub_rn(y, a.py0), a.hy);
+    if (!(tx >= -1.0e-9 && tx <= a.hix && ty >= -1.0e-9 && ty <= a.hiy)) {
+      if (lane == 0) atomicMin(&a.err[0], (int)i);
+      continue;
+    }
+    const int cx = snap_cell(tx), cy = snap_cell(ty);
+    const int xlo = cx - (a.L - 1), ylo = cy - (a.L - 1);
+    if (xlo < 0 || ylo < 0 || cx + a.L > a.M1 - 1 || cy + a.L > a.M2 - 1) {
+      if (lane == 0) atomicMin(&a.err[1], (int)i);
+      continue;
+    }
+    const double ox = __dsub_rn(tx, (double)cx), oy = __dsub_rn(ty, (double)cy);
+    const bool on_node = fabs(ox) <= 1.0e-9 && fabs(oy) <= 1.0e-9;
+    double k[MPL], v[MPL];
+    int bad = 0;
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) {
+      const int m = s * 32 + lane;
+      k[s] = 0.0;
+      if (m < M) {
+        const int r = m / a.bs, q = m % a.bs;
+        const double nx = __dadd_rn(a.px0, __dmul_rn((double)(xlo + q), a.hx));
+        const double ny = __dadd_rn(a.py0, __dmul_rn((double)(ylo + r), a.hy));
+        const double dist = hypot(__dsub_rn(nx, x), __dsub_rn(ny, y));
+        k[s] = matern_cov(a.P, dist, &bad);
+      }
+      v[s] = k[s];
+    }
+    if (bad) atomicOr(&a.err[2], 1);
+    // forward substitution L y = k (column oriented; y overwrites v)
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) {
+      for (int cc = 0; cc < 32; ++cc) {
+        const int c = s * 32 + cc;
+        if (c >= M) break;
+        const double dcc = smem_l ? Lr[c * M + c] : a.chol[c * M + c];
+        const double mine = v[s] / dcc;
+        const double yc = __shfl_sync(0xffffffffu, mine, cc);
+        if (lane == cc) v[s] = yc;
+#pragma unroll
+        for (int s2 = s; s2 < MPL; ++s2) {
+          const int r = s2 * 32 + lane;
+          if (r > c && r < M) {
+            const double lrc = smem_l ? Lc[c * M + r] : a.chol[r * M + c];
+            v[s2] = fma(-lrc, yc, v[s2]);
+          }
+        }
+      }
+    }
+    // back substitution L^T w = y
+#pragma unroll
+    for (int s = MPL - 1; s >= 0; --s) {
+      for (int cc = 31; cc >= 0; --cc) {
+        const int c = s * 32 + cc;
+        if (c >= M) continue;
+        const double dcc = smem_l ? Lr[c * M + c] : a.chol[c * M + c];
+        const double mine = v[s] / dcc;
+        const double wc = __shfl_sync(0xffffffffu, mine, cc);
+        if (lane == cc) v[s] = wc;
+#pragma unroll
+        for (int s2 = 0; s2 <= s; ++s2) {
+          const int r = s2 * 32 + lane;
+          if (r < c) {
+            const double lcr = smem_l ? Lr[c * M + r] : a.chol[c * M + r];
+            v[s2] = fma(-lcr, wc, v[s2]);
+          }
+        }
+      }
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) part = fma(v[s], k[s], part);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    double cv = a.P.sigma2 - part;
+    const int corner = (a.L - 1) * a.bs + (a.L - 1);
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) {
+      const int m = s * 32 + lane;
+      if (m < M) {
+        double w = v[s];
+        if (on_node) w = (m == corner) ? 1.0 : 0.0;
+        a.weights[i * M + m] = w;
+      }
+    }
+    if (on_node) cv = 0.0;
+    if (cv < 0.0 && cv > -1.0e-10 * a.P.sigma2) cv = 0.0;
+    if (lane == 0) {
+      a.cond_var[i] = cv;
+      a.base[i] = ylo * a.M1 + xlo;
+    }
+  }
+}
+
+// cell_start[b] = lower_bound(sorted keys, b) for b in [0, nb]
+__global__ void cell_start_kernel(const int32_t* __restrict__ keys, int64_t n, int32_t* cs,
+                                  int64_t nb) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < b) lo = mid + 1; else hi = mid;
+    }
+    cs[b] = (int32_t)lo;
+  }
+}
+
+__global__ void iota_kernel(int32_t* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int32_t)i;
+}
+
+__global__ void permute_rows_kernel(const double* __restrict__ w, const int32_t* __restrict__ perm,
+                                    double* __restrict__ ws, int64_t n, int M) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * M;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / M;
+    const int m = (int)(e % M);
+    ws[e] = w[(int64_t)perm[j] * M + m];
+  }
+}
+
+__global__ void expand_indices_kernel(const int32_t* __restrict__ base, int64_t n, int bs, int M1,
+                                      int64_t* __restrict__ out) {
+  const int M = bs * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * M;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / M;
+    const int m = (int)(e % M);
+    out[e] = (int64_t)base[i] + (int64_t)(m / bs) * M1 + (m % bs);
+  }
+}
+
+// ----------------------------------------------------- host K_N (tiny, M x M)
+// rapid.py:103-117: offsets (arange(2L) h) row-major over the block, cdist-free
+// hypot distances, covariance, 0.5 (k + k') symmetrisation.
+static Status kn_matrix_dev(const rk_setup* s, std::vector<double>* kn) {
+  const int M = s->M, bs = s->bs;
+  std::vector<double> dist((size_t)M * M);
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < M; ++j) {
+      const double xi = (double)(i % bs) * s->grid.hx, yi = (double)(i / bs) * s->grid.hy;
+      const double xj = (double)(j % bs) * s->grid.hx, yj = (double)(j / bs) * s->grid.hy;
+      dist[(size_t)i * M + j] = std::hypot(xi - xj, yi - yj);
+    }
+  double *dd = nullptr, *dk = nullptr;
+  int* bad = nullptr;
+  const size_t bytes = sizeof(double) * M * M;
+  RK_CUDA_TRY(cudaMalloc(&dd, bytes));
+  RK_CUDA_TRY(cudaMalloc(&dk, bytes));
+  RK_CUDA_TRY(cudaMalloc(&bad, sizeof(int)));
+  RK_CUDA_TRY(cudaMemset(bad, 0, sizeof(int)));
+  RK_CUDA_TRY(cudaMemcpy(dd, dist.data(), bytes, cudaMemcpyHostToDevice));
+  matern_kernel<<<(M * M + 255) / 256, 256>>>(s->mat, dd, dk, (int64_t)M * M, bad);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  kn->resize((size_t)M * M);
+  RK_CUDA_TRY(cudaMemcpy(kn->data(), dk, bytes, cudaMemcpyDeviceToHost));
+  int hb = 0;
+  RK_CUDA_TRY(cudaMemcpy(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(dd);
+  cudaFree(dk);
+  cudaFree(bad);
+  if (hb) return Status::err(RK_NUMERIC, "Temme series / continued fraction for K_nu failed to converge");
+  for (int i = 0; i < M; ++i)
+    for (int j = i + 1; j < M; ++j) {
+      const double a = (*kn)[(size_t)i * M + j], b = (*kn)[(size_t)j * M + i];
+      const double v = 0.5 * (a + b);
+      (*kn)[(size_t)i * M + j] = v;
+      (*kn)[(size_t)j * M + i] = v;
+    }
+  return Status::ok();
+}
+
+// lower Cholesky (right-looking, row-major); false if not positive definite
+static bool cholesky_lower(std::vector<double>& a, int M) {
+  for (int j = 0; j < M; ++j) {
+    double d = a[(size_t)j * M + j];
+    for (int k = 0; k < j; ++k) d -= a[(size_t)j * M + k] * a[(size_t)j * M + k];
+    if (!(d > 0.0)) return false;
+    d = std::sqrt(d);
+    a[(size_t)j * M + j] = d;
+    for (int i = j + 1; i < M; ++i) {
+      double v = a[(size_t)i * M + j];
+      for (int k = 0; k < j; ++k) v -= a[(size_t)i * M + k] * a[(size_t)j * M + k];
+      a[(size_t)i * M + j] = v / d;
+    }
+    for (int k = j + 1; k < M; ++k) a[(size_t)j * M + k] = 0.0;
+  }
+  return true;
+}
+
+static void chol_inverse(const std::vector<double>& L, int M, std::vector<double>* inv) {
+  // (L L')^-1 column by column: cho_solve(I) (rapid.py:193)
+  inv->assign((size_t)M * M, 0.0);
+  std::vector<double> y(M);
+  for (int c = 0; c < M; ++c) {
+    for (int i = 0; i < M; ++i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) v -= L[(size_t)i * M + k] * y[k];
+      y[i] = v / L[(size_t)i * M + i];
+    }
+    for (int i = M - 1; i >= 0; --i) {
+      double v = y[i];
+      for (int k = i + 1; k < M; ++k) v -= L[(size_t)k * M + i] * (*inv)[(size_t)k * M + c];
+      (*inv)[(size_t)i * M + c] = v / L[(size_t)i * M + i];
+    }
+  }
+}
+
+Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2, double scale,
+                        double* out_q, cudaStream_t st);  // rk_predict.cu
+
+static void free_setup(rk_setup* s) {
+  if (!s) return;
+  cudaFree(s->obs);
+  cudaFree(s->base);
+  cudaFree(s->weights);
+  cudaFree(s->cond_var);
+  cudaFree(s->perm);
+  cudaFree(s->bsort);
+  cudaFree(s->wsort);
+  cudaFree(s->cell_start);
+  cudaFree(s->spec_q);
+  cudaFree(s->kn_chol_dev);
+  cudaFree(s->emb.root_q);
+  delete s;
+}
+
+static Status build_setup(const rk_model* model, const rk_grid* grid, int L, const double* obs_host,
+                          int64_t n, rk_setup** out, int32_t* ridge_applied, bool grid_only = false) {
+  if (n <= 0 && !grid_only) return Status::err(RK_DOMAIN, "build_setup requires at least one observation");
+  if (L < 1) return Status::err(RK_DOMAIN, "neighbor order L must be >= 1");
+  rk_setup* s = new rk_setup();
+  std::unique_ptr<rk_setup, void (*)(rk_setup*)> guard(s, free_setup);
+  RK_CUDA_TRY(cudaGetDevice(&s->device));
+  s->model = *model;
+  s->mat = make_matern_dev(*model);
+  s->grid = *grid;
+  s->L = L;
+  s->bs = 2 * L;
+  s->M = s->bs * s->bs;
+  s->n = n;
+  s->m1 = grid->m1;
+  s->m2 = grid->m2;
+  s->M1 = grid->m1 + grid->pad[0] + grid->pad[1];
+  s->M2 = grid->m2 + grid->pad[2] + grid->pad[3];
+  // padded_origin (gridding.py:44-48): origin - pad * spacing
+  s->px0 = grid->x0 - (double)grid->pad[0] * grid->hx;
+  s->py0 = grid->y0 - (double)grid->pad[2] * grid->hy;
+  if (s->M > 1024) return Status::err(RK_DOMAIN, "neighbor order L > 16 not supported");
+  *ridge_applied = 0;
+  if (grid_only) {
+    s->n = 0;
+    goto spectrum;
+  }
+  {
+
+  // K_N and its factor (rapid.py:190-193)
+  std::vector<double> kn;
+  RK_TRY(kn_matrix_dev(s, &kn));
+  std::vector<double> chol = kn;
+  if (!cholesky_lower(chol, s->M)) {
+    const double ridge = 1.0e-12 * model->sigma2 * (double)(s->bs * s->bs);
+    chol = kn;
+    for (int i = 0; i < s->M; ++i) chol[(size_t)i * s->M + i] += ridge;
+    if (!cholesky_lower(chol, s->M))
+      return Status::err(RK_NUMERIC, "Cholesky of K_N failed even with ridge; reduce the neighbor "
+                                     "order L or the smoothness nu");
+    *ridge_applied = 1;
+  }
+  s->kn_chol = chol;
+  chol_inverse(chol, s->M, &s->kn_inv);
+
+  const int M = s->M;
+  RK_CUDA_TRY(cudaMalloc(&s->obs, sizeof(double) * 2 * n));
+  RK_CUDA_TRY(cudaMalloc(&s->base, sizeof(int32_t) * n));
+  RK_CUDA_TRY(cudaMalloc(&s->weights, sizeof(double) * n * M));
+  RK_CUDA_TRY(cudaMalloc(&s->cond_var, sizeof(double) * n));
+  RK_CUDA_TRY(cudaMalloc(&s->kn_chol_dev, sizeof(double) * M * M));
+  RK_CUDA_TRY(cudaMemcpy(s->obs, obs_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+  RK_CUDA_TRY(cudaMemcpy(s->kn_chol_dev, chol.data(), sizeof(double) * M * M, cudaMemcpyHostToDevice));
+  int* err = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&err, sizeof(int) * 4));
+  int herr[4] = {INT_MAX, INT_MAX, 0, 0};
+  RK_CUDA_TRY(cudaMemcpy(err, herr, sizeof(herr), cudaMemcpyHostToDevice));
+
+  WArgs wa;
+  wa.P = s->mat;
+  wa.obs = s->obs;
+  wa.n = n;
+  wa.px0 = s->px0;
+  wa.py0 = s->py0;
+  wa.hx = grid->hx;
+  wa.hy = grid->hy;
+  wa.hix = (double)(s->M1 - 1) + 1.0e-9;
+  wa.hiy = (double)(s->M2 - 1) + 1.0e-9;
+  wa.L = L;
+  wa.bs = s->bs;
+  wa.M = M;
+  wa.M1 = s->M1;
+  wa.M2 = s->M2;
+  wa.chol = s->kn_chol_dev;
+  wa.base = s->base;
+  wa.weights = s->weights;
+  wa.cond_var = s->cond_var;
+  wa.err = err;
+  const size_t wsm = M <= 64 ? sizeof(double) * 2 * M * M : 0;
+  const int wblocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 16);
+  const int mpl = (M + 31) / 32;
+  if (mpl <= 1) {
+    weights_kernel<1><<<wblocks, 256, wsm>>>(wa);
+  } else if (mpl <= 2) {
+    weights_kernel<2><<<wblocks, 256, wsm>>>(wa);
+  } else if (mpl <= 4) {
+    weights_kernel<4><<<wblocks, 256, wsm>>>(wa);
+  } else if (mpl <= 8) {
+    weights_kernel<8><<<wblocks, 256, wsm>>>(wa);
+  } else if (mpl <= 16) {
+    weights_kernel<16><<<wblocks, 256, wsm>>>(wa);
+  } else {
+    weights_kernel<32><<<wblocks, 256, wsm>>>(wa);
+  }
+  count_launch();
+  RK_LAUNCH_CHECK();
+  RK_CUDA_TRY(cudaMemcpy(herr, err, sizeof(herr), cudaMemcpyDeviceToHost));
+  cudaFree(err);
+  if (herr[0] != INT_MAX) {
+    std::vector<double> o(2);
+    RK_CUDA_TRY(cudaMemcpy(o.data(), s->obs + 2 * (int64_t)herr[0], 16, cudaMemcpyDeviceToHost));
+    char b[256];
+    snprintf(b, sizeof b, "location (%.17g, %.17g) outside padded grid coverage", o[0], o[1]);
+    return Status::err(RK_DOMAIN, b);
+  }
+  if (herr[1] != INT_MAX) {
+    std::vector<double> o(2);
+    RK_CUDA_TRY(cudaMemcpy(o.data(), s->obs + 2 * (int64_t)herr[1], 16, cudaMemcpyDeviceToHost));
+    char b[256];
+    snprintf(b, sizeof b,
+             "neighborhood of (%.17g, %.17g) exits the padded grid; padding contract violated",
+             o[0], o[1]);
+    return Status::err(RK_INTERNAL, b);
+  }
+  if (herr[2]) return Status::err(RK_NUMERIC, "Temme series / continued fraction for K_nu failed to converge");
+
+  // cell-sorted structure for the deterministic gather (stable radix sort by base)
+  RK_CUDA_TRY(cudaMalloc(&s->perm, sizeof(int32_t) * n));
+  RK_CUDA_TRY(cudaMalloc(&s->bsort, sizeof(int32_t) * n));
+  RK_CUDA_TRY(cudaMalloc(&s->wsort, sizeof(double) * n * M));
+  const int64_t nb = (int64_t)s->M1 * s->M2;
+  RK_CUDA_TRY(cudaMalloc(&s->cell_start, sizeof(int32_t) * (nb + 1)));
+  int32_t* iota = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&iota, sizeof(int32_t) * n));
+  iota_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 4096), 256>>>(iota, n);
+  count_launch();
+  size_t tmp_bytes = 0;
+  int end_bit = 1;
+  while (end_bit < 31 && ((int64_t)1 << end_bit) <= nb) ++end_bit;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, s->base, s->bsort, iota, s->perm, (int)n, 0,
+                                  end_bit);
+  void* tmp = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 16));
+  RK_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, s->base, s->bsort, iota, s->perm,
+                                              (int)n, 0, end_bit));
+  count_launch();
+  cudaFree(tmp);
+  cudaFree(iota);
+  cell_start_kernel<<<(int)std::min<int64_t>(ceil_div(nb + 1, 256), 148 * 32), 256>>>(
+      s->bsort, n, s->cell_start, nb);
+  count_launch();
+  permute_rows_kernel<<<(int)std::min<int64_t>(ceil_div(n * M, 256), 148 * 32), 256>>>(
+      s->weights, s->perm, s->wsort, n, M);
+  count_launch();
+  RK_LAUNCH_CHECK();
+
+  std::vector<double> cv(n);
+  RK_CUDA_TRY(cudaMemcpy(cv.data(), s->cond_var, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  s->cond_var_min = *std::min_element(cv.begin(), cv.end());
+  }
+spectrum:
+  // filter spectrum on the (2M-1)-rounded torus (rapid.py:72-86)
+  auto next_fft_len = [](int64_t m) -> int64_t {
+    if (m <= 1) return 1;
+    int64_t best = -1;
+    for (int64_t two = 1; two < 4 * m; two *= 2) {
+      int64_t v = two;
+      while (v < m) v *= 3;
+      if (best < 0 || v < best) best = v;
+    }
+    return best;
+  };
+  s->p1 = (int)next_fft_len(2 * (int64_t)s->M1 - 1);
+  s->p2 = (int)next_fft_len(2 * (int64_t)s->M2 - 1);
+  s->H1 = s->p1 / 2 + 1;
+  s->Q2 = s->p2 / 2 + 1;
+  RK_TRY(plan_for(s->p1, &s->pl1));
+  RK_TRY(plan_for(s->p2, &s->pl2));
+  RK_CUDA_TRY(cudaMalloc(&s->spec_q, sizeof(double) * (size_t)s->H1 * s->Q2));
+  RK_TRY(spectrum_quarter(s->mat, grid->hx, grid->hy, s->p1, s->p2,
+                          1.0 / ((double)s->p1 * (double)s->p2), s->spec_q, 0));
+  RK_CUDA_TRY(cudaDeviceSynchronize());
+  *out = guard.release();
+  return Status::ok();
+}
+
+}  // namespace rk
+
+using namespace rk;
+
+extern "C" {
+
+const char* rk_last_error(void) { return rk::g_err.c_str(); }
+int32_t rk_version(void) { return 1; }
+int64_t rk_launch_count(void) { return rk::g_launches; }
+
+rk_status rk_matern_cov(const rk_model* model, const double* d_dev, double* out_dev, int64_t n,
+                        void* stream) {
+  auto run = [&]() -> Status {
+    if (n <= 0) return Status::ok();
+    const MaternDev P = make_matern_dev(*model);
+    int* bad = nullptr;
+    RK_CUDA_TRY(cudaMallocAsync((void**)&bad, sizeof(int), (cudaStream_t)stream));
+    RK_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), (cudaStream_t)stream));
+    matern_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 32), 256, 0,
+                    (cudaStream_t)stream>>>(P, d_dev, out_dev, n, bad);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    int hb = 0;
+    RK_CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    RK_CUDA_TRY(cudaFreeAsync(bad, (cudaStream_t)stream));
+    RK_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    if (hb) return Status::err(RK_NUMERIC, "Temme series / continued fraction for K_nu failed to converge");
+    return Status::ok();
+  };
+  return (rk_status)finish(run());
+}
+
+rk_status rk_build_padded_grid(const double domain[4], int32_t m1, int32_t m2, int32_t L,
+                               const double* obs_host, int64_t n, rk_grid* g) {
+  auto run = [&]() -> Status {
+    const double x0 = domain[0], x1 = domain[1], y0 = domain[2], y1 = domain[3];
+    if (L < 1) return Status::err(RK_DOMAIN, "neighbor order L must be >= 1, got " + std::to_string(L));
+    if (m1 < std::max(2, 2 * L) || m2 < std::max(2, 2 * L))
+      return Status::err(RK_DOMAIN, "grid dims too small for neighbor order L=" + std::to_string(L) +
+                                        "; need >= " + std::to_string(2 * L));
+    if (!(x1 > x0 && y1 > y0)) return Status::err(RK_DOMAIN, "degenerate domain rectangle");
+    g->x0 = x0;
+    g->y0 = y0;
+    g->hx = (x1 - x0) / (double)(m1 - 1);
+    g->hy = (y1 - y0) / (double)(m2 - 1);
+    g->m1 = m1;
+    g->m2 = m2;
+    for (int k = 0; k < 4; ++k) g->pad[k] = 0;
+    if (n <= 0) return Status::ok();
+    double* dobs = nullptr;
+    int* out = nullptr;
+    RK_CUDA_TRY(cudaMalloc(&dobs, sizeof(double) * 2 * n));
+    RK_CUDA_TRY(cudaMalloc(&out, sizeof(int) * 5));
+    RK_CUDA_TRY(cudaMemcpy(dobs, obs_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+    int init[5] = {INT_MAX, INT_MIN, INT_MIN, INT_MIN, INT_MIN};
+    RK_CUDA_TRY(cudaMemcpy(out, init, sizeof(init), cudaMemcpyHostToDevice));
+    PadArgs a;
+    a.obs = dobs;
+    a.n = n;
+    a.x0 = x0;
+    a.y0 = y0;
+    a.hx = g->hx;
+    a.hy = g->hy;
+    const double ex = 1.0e-9 * g->hx, ey = 1.0e-9 * g->hy;
+    a.lox = x0 - ex;
+    a.hix = x1 + ex;
+    a.loy = y0 - ey;
+    a.hiy = y1 + ey;
+    a.L = L;
+    a.m1 = m1;
+    a.m2 = m2;
+    a.out = out;
+    pad_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 4096), 256>>>(a);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    int res[5];
+    RK_CUDA_TRY(cudaMemcpy(res, out, sizeof(res), cudaMemcpyDeviceToHost));
+    cudaFree(dobs);
+    cudaFree(out);
+    if (res[0] != INT_MAX) {
+      char b[256];
+      snprintf(b, sizeof b, "observation %d at (%.17g, %.17g) lies outside the domain", res[0],
+               obs_host[2 * (int64_t)res[0]], obs_host[2 * (int64_t)res[0] + 1]);
+      return Status::err(RK_DOMAIN, b);
+    }
+    for (int k = 0; k < 4; ++k) g->pad[k] = std::max(0, res[k + 1]);
+    return Status::ok();
+  };
+  return (rk_status)finish(run());
+}
+
+rk_status rk_build_setup(const rk_model* model, const rk_grid* grid, int32_t L, const double* obs_host,
+                         int64_t n, rk_setup** out, int32_t* ridge_applied) {
+  int32_t r = 0;
+  Status s = build_setup(model, grid, L, obs_host, n, out, &r);
+  if (ridge_applied) *ridge_applied = r;
+  return (rk_status)finish(s);
+}
+
+rk_status rk_grid_setup_create(const rk_model* model, const rk_grid* grid, rk_setup** out) {
+  int32_t r = 0;
+  return (rk_status)finish(build_setup(model, grid, 1, nullptr, 0, out, &r, true));
+}
+
+rk_status rk_setup_destroy(rk_setup* s) {
+  free_setup(s);
+  return RK_OK;
+}
+
+rk_status rk_setup_info(const rk_setup* s, int64_t* n_obs, int32_t* L, int32_t embed[2],
+                        int32_t total[2]) {
+  if (n_obs) *n_obs = s->n;
+  if (L) *L = s->L;
+  if (embed) { embed[0] = s->p1; embed[1] = s->p2; }
+  if (total) { total[0] = s->M1; total[1] = s->M2; }
+  return RK_OK;
+}
+
+rk_status rk_setup_copy_out(const rk_setup* s, int64_t* indices_host, double* weights_host,
+                            double* cond_var_host, double* kn_inv_host) {
+  auto run = [&]() -> Status {
+    const int64_t nm = s->n * s->M;
+    if (indices_host) {
+      int64_t* d = nullptr;
+      RK_CUDA_TRY(cudaMalloc(&d, sizeof(int64_t) * nm));
+      expand_indices_kernel<<<(int)std::min<int64_t>(ceil_div(nm, 256), 4096), 256>>>(
+          s->base, s->n, s->bs, s->M1, d);
+      count_launch();
+      RK_LAUNCH_CHECK();
+      RK_CUDA_TRY(cudaMemcpy(indices_host, d, sizeof(int64_t) * nm, cudaMemcpyDeviceToHost));
+      cudaFree(d);
+    }
+    if (weights_host)
+      RK_CUDA_TRY(cudaMemcpy(weights_host, s->weights, sizeof(double) * nm, cudaMemcpyDeviceToHost));
+    if (cond_var_host)
+      RK_CUDA_TRY(cudaMemcpy(cond_var_host, s->cond_var, sizeof(double) * s->n, cudaMemcpyDeviceToHost));
+    if (kn_inv_host) std::copy(s->kn_inv.begin(), s->kn_inv.end(), kn_inv_host);
+    return Status::ok();
+  };
+  return (rk_status)finish(run());
+}
+
+rk_status rk_setup_copy_spectrum(const rk_setup* s, double* spectrum_host) {
+  auto run = [&]() -> Status {
+    std::vector<double> q((size_t)s->H1 * s->Q2);
+    RK_CUDA_TRY(cudaMemcpy(q.data(), s->spec_q, sizeof(double) * q.size(), cudaMemcpyDeviceToHost));
+    const double P = (double)s->p1 * (double)s->p2;
+    for (int ky = 0; ky < s->p2; ++ky) {
+      const int a = std::min(ky, s->p2 - ky);
+      for (int kx = 0; kx < s->p1; ++kx) {
+        const int b = std::min(kx, s->p1 - kx);
+        spectrum_host[(size_t)ky * s->p1 + kx] = q[(size_t)b * s->Q2 + a] * P;
+      }
+    }
+    return Status::ok();
+  };
+  return (rk_status)finish(run());
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Internal structures shared by the rapidkrig B200 translation units.
+#pragma once
+
+#include <vector>
+
+#include "rk_common.cuh"
+#include "rk_fft.cuh"
+#include "rk_matern.cuh"
+
+namespace rk {
+
+// --------------------------------------------------------------- bookkeeping
+void count_launch(int k = 1);
+Status plan_for(int n, FftPlan* out);            // cached per (device, n)
+int pick_lpc(const FftPlan& pl, int max_lines);  // lines per CTA for a kernel
+Status set_smem_attr(const void* fn, size_t bytes);
+
+// RAII-free stream-ordered scratch (cudaMallocAsync pool)
+Status scratch_alloc(void** p, size_t bytes, cudaStream_t st);
+void scratch_free(void* p, cudaStream_t st);
+
+// ------------------------------------------------------------------- setup
+struct Embedding {
+  bool ready = false;
+  int ps1 = 0, ps2 = 0, doubled = 0;
+  int hs1 = 0, qs2 = 0;          // ps1/2+1, ps2/2+1
+  FftPlan pl1{}, pl2{};
+  double* root_q = nullptr;      // (qs2, hs1) row-major: sqrt(clip(lambda,0)) * sqrt(P)/P
+};
+
+}  // namespace rk
+
+struct rk_setup {
+  int device = 0;
+  rk_model model{};
+  rk::MaternDev mat{};
+  rk_grid grid{};
+  int L = 0, bs = 0, M = 0;      // bs = 2L, M = bs^2
+  int64_t n = 0;
+  int M1 = 0, M2 = 0, m1 = 0, m2 = 0;
+  double px0 = 0, py0 = 0;
+  int p1 = 0, p2 = 0, H1 = 0, Q2 = 0;
+  rk::FftPlan pl1{}, pl2{};
+  // device arrays
+  double* obs = nullptr;        // (n, 2)
+  int32_t* base = nullptr;      // (n) flat padded index of block entry 0
+  double* weights = nullptr;    // (n, M) original order
+  double* cond_var = nullptr;   // (n)
+  int32_t* perm = nullptr;      // sorted -> original
+  int32_t* bsort = nullptr;     // sorted base keys
+  double* wsort = nullptr;      // (n, M) sorted order
+  int32_t* cell_start = nullptr;  // (M1*M2 + 1) lower bounds of base keys
+  double* spec_q = nullptr;     // (H1, Q2): Re fft2(filter)[ky, kx] / (p1 p2), ky <= p2/2
+  double* kn_chol_dev = nullptr;  // (M, M) row-major lower
+  std::vector<double> kn_chol, kn_inv;
+  double cond_var_min = 0;
+  rk::Embedding emb;
+};
+
+struct rk_fit {
+  int device = 0;
+  rk_model model{};
+  int64_t n = 0;
+  int p = 0;
+  double* U = nullptr;          // (n, n) column-major UPPER factor = row-major lower L
+  double* X = nullptr;          // (n, p) column-major
+  double* B = nullptr;          // L^-1 X (n, p) column-major
+  double* beta = nullptr;       // (p)
+  double* c = nullptr;          // (n)
+  std::vector<double> gram_lu;  // (p, p) LU of B'B with partial pivoting (row-major)
+  std::vector<int> gram_piv;
+  void* cublas = nullptr;
+};
+
+namespace rk {
+
+// predict pipeline pieces (rk_predict.cu), used by the ensemble driver
+enum EpiMode { EPI_PLAIN = 0, EPI_SCALAR = 1, EPI_COV = 2 };
+
+struct PredictBatch {
+  int batch = 1;
+  const double* c = nullptr;      // (batch, n)
+  int64_t c_stride = 0;
+  const double* beta = nullptr;   // (batch, p) or null
+  int p = 0;
+  const double* xg = nullptr;     // (m1*m2, p) or null
+  const double* g = nullptr;      // CS: (batch, M2, M1) unconditional fields, or null
+  double* out = nullptr;          // (batch, m2, m1): field, or e = interior(g) - field in CS mode
+};
+Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st);
+
+// CS pieces (rk_sim.cu)
+Status ensure_embedding(rk_setup* s, cudaStream_t st);
+
+}  // namespace rk

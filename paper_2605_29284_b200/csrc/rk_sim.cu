@@ -1,0 +1,823 @@
+// rapidkrig B200: conditional simulation ensemble + exact fit / refit.
+//
+// Reference mapping (/root/reference/pkg/src/rapidkrig):
+//   _splitmix64 / draw_seed   simulate.py:52-62   -> splitmix64(), draw_seed()
+//   _rng / _std_normals       simulate.py:65-74   -> philox4x64_10() keyed (seed, stream),
+//        pre-incremented counter (block b uses counter b+1), normal = ndtri(((w>>11)+.5)/2^53)
+//   _embedding_root           simulate.py:82-100  -> ensure_embedding() (PSD test, one doubling)
+//   sim_unconditional_grid    simulate.py:103-118 -> cs_row_kernel + cs_col_kernel
+//   sim_obs_local             simulate.py:121-143 -> obs_local_kernel
+//   refit_coefficients/_gls   exact.py:59-68,108-113 -> refit() (batched triangular solves)
+//   conditional_draw / generate_ensemble simulate.py:146-192 -> rk_ensemble_accumulate
+//   fit / _cholesky_with_ridge exact.py:25-37,71-105 -> rk_fit_create
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include "rk_internal.cuh"
+
+namespace rk {
+
+// ------------------------------------------------------------- randomness
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t v) {
+  uint64_t z = v + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t draw_seed(uint64_t seed, uint64_t j) {
+  return seed ^ splitmix64(j);
+}
+
+// Philox4x64-10 (Salmon et al., SC'11) block for counter (ctr0, 0, 0, 0), key (k0, k1)
+__device__ __forceinline__ void philox4x64_10(uint64_t ctr0, uint64_t k0, uint64_t k1, uint64_t o[4]) {
+  uint64_t c0 = ctr0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ULL;
+      k1 += 0xBB67AE8584CAA73BULL;
+    }
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ULL * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0);
+    const uint64_t lo1 = 0xCA5A826395121157ULL * c2, hi1 = __umul64hi(0xCA5A826395121157ULL, c2);
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+  }
+  o[0] = c0; o[1] = c1; o[2] = c2; o[3] = c3;
+}
+
+__device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t stream, uint64_t w) {
+  uint64_t o[4];
+  philox4x64_10(w / 4 + 1, seed, stream, o);
+  const int q = (int)(w & 3);
+  return q == 0 ? o[0] : q == 1 ? o[1] : q == 2 ? o[2] : o[3];
+}
+
+// integers(0, 2^53) == w >> 11 (Lemire, power-of-two range); u = (k + 0.5) / 2^53; ndtri(u)
+__device__ __forceinline__ double word_normal(uint64_t w) {
+  const double u = ((double)(w >> 11) + 0.5) * 0x1.0p-53;
+  return normcdfinv(u);
+}
+
+__global__ void philox_kernel(uint64_t seed, uint64_t stream, uint64_t start, int64_t count,
+                              double* out_n, uint64_t* out_raw) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t w = philox_word(seed, stream, start + (uint64_t)t);
+    if (out_raw) out_raw[t] = w;
+    if (out_n) out_n[t] = word_normal(w);
+  }
+}
+
+// ------------------------------------------------------------- CS field
+struct CsRowArgs {
+  FftPlan pl;
+  int lpc;
+  int ps1, ps2;
+  int keep;                  // M1 columns kept
+  const double* root_q;      // (ps2/2+1, ps1/2+1) row-major, sqrt(P)/P folded
+  int rq_ld;
+  uint64_t seed;             // ensemble seed (per-realization sub-seeds) ...
+  int64_t j0;
+  int direct;                // ... or 1: `seed` is the field seed itself
+  double2* V;                // (batch, keep, ldV)
+  int64_t ldV, V_bstride;
+};
+
+__global__ void __launch_bounds__(512, 1) cs_row_kernel(const CsRowArgs a) {
+  extern __shared__ double2 smem[];
+  const int n = a.pl.n;
+  const int nthr = a.pl.nthr;
+  const int line = threadIdx.x / nthr;
+  const int tl = threadIdx.x - line * nthr;
+  const int b = blockIdx.y;
+  const int iy = blockIdx.x * a.lpc + line;
+  const bool valid = iy < a.ps2;
+  double2* buf = smem + (size_t)line * n;
+  const uint64_t fs =
+      a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
+  if (valid) {
+    const uint64_t Ps = (uint64_t)a.ps1 * (uint64_t)a.ps2;
+    const uint64_t wb = (uint64_t)iy * (uint64_t)a.ps1;
+    // real parts: words [wb, wb + ps1); imaginary: [Ps + wb, Ps + wb + ps1)   (simulate.py:114-115)
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const uint64_t w0 = wb + (part ? Ps : 0);
+      const uint64_t b0 = w0 / 4, b1 = (w0 + (uint64_t)a.ps1 - 1) / 4;
+      for (uint64_t blk = b0 + tl; blk <= b1; blk += nthr) {
+        uint64_t o[4];
+        philox4x64_10(blk + 1, fs, 0, o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t w = blk * 4 + q;
+          if (w >= w0 && w < w0 + (uint64_t)a.ps1) {
+            const double z = word_normal(o[q]);
+            if (part) buf[w - w0].y = z; else buf[w - w0].x = z;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (valid) {
+    const double* R = a.root_q + (int64_t)min(iy, a.ps2 - iy) * a.rq_ld;
+    for (int ix = tl; ix < n; ix += nthr) buf[ix] = cscale(buf[ix], __ldg(&R[min(ix, n - ix)]));
+  } else {
+    for (int ix = tl; ix < n; ix += nthr) buf[ix] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_line<true>(buf, a.pl, tl);
+  double2* V = a.V + (int64_t)b * a.V_bstride;
+  for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
+    const int l = idx % a.lpc, ix = idx / a.lpc;
+    const int row = blockIdx.x * a.lpc + l;
+    if (row < a.ps2) V[(int64_t)ix * a.ldV + row] = smem[(size_t)l * n + ix];
+  }
+}
+
+struct CsColArgs {
+  FftPlan pl;
+  int lpc;
+  int ncols;                 // M1
+  int keep;                  // M2
+  const double2* V;
+  int64_t ldV, V_bstride;
+  double* g;                 // (batch, M2, M1)
+  int64_t g_bstride;
+};
+
+__global__ void __launch_bounds__(512, 1) cs_col_kernel(const CsColArgs a) {
+  extern __shared__ double2 smem[];
+  const int n = a.pl.n;
+  const int nthr = a.pl.nthr;
+  const int line = threadIdx.x / nthr;
+  const int tl = threadIdx.x - line * nthr;
+  const int b = blockIdx.y;
+  const int ix = blockIdx.x * a.lpc + line;
+  double2* buf = smem + (size_t)line * n;
+  const double2* V = a.V + (int64_t)b * a.V_bstride + (int64_t)ix * a.ldV;
+  for (int y = tl; y < n; y += nthr) buf[y] = ix < a.ncols ? V[y] : make_double2(0.0, 0.0);
+  __syncthreads();
+  fft_line<true>(buf, a.pl, tl);
+  double* g = a.g + (int64_t)b * a.g_bstride;
+  for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
+    const int l = idx % a.lpc, y = idx / a.lpc;
+    const int col = blockIdx.x * a.lpc + l;
+    if (col < a.ncols) g[(int64_t)y * a.ncols + col] = smem[(size_t)l * n + y].x;
+  }
+}
+
+struct ObsArgs {
+  const int32_t* base;
+  const double* weights;
+  const double* cond_var;
+  int64_t n;
+  int M, bs, M1;
+  const double* g;
+  int64_t g_bstride;
+  double sqrt_tau2;
+  uint64_t seed;
+  int64_t j0;
+  int direct;
+  double* z;                 // (batch, n)
+};
+
+__global__ void obs_local_kernel(const ObsArgs a) {
+  const int b = blockIdx.y;
+  const uint64_t os = a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 202);
+  const double* g = a.g + (int64_t)b * a.g_bstride;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t base = a.base[i];
+    const double* w = a.weights + i * a.M;
+    double mean = 0.0;
+    for (int m = 0; m < a.M; ++m) mean = fma(w[m], g[base + (int64_t)(m / a.bs) * a.M1 + (m % a.bs)], mean);
+    const double eta = word_normal(philox_word(os, 1, (uint64_t)i));
+    const double eps = word_normal(philox_word(os, 1, (uint64_t)(a.n + i)));
+    const double cv = fmax(a.cond_var[i], 0.0);
+    const double gs = mean + sqrt(cv) * eta;
+    a.z[(int64_t)b * a.n + i] = gs + a.sqrt_tau2 * eps;
+  }
+}
+
+__global__ void accumulate_kernel(const double* __restrict__ E, int batch, int64_t npix,
+                                  const double* __restrict__ dp, double* s1, double* s2,
+                                  double* draws) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    double a1 = s1[p], a2 = s2[p];
+    const double d = dp[p];
+    for (int b = 0; b < batch; ++b) {
+      const double e = E[(int64_t)b * npix + p];
+      a1 += e;
+      a2 = fma(e, e, a2);
+      if (draws) draws[(int64_t)b * npix + p] = d + e;
+    }
+    s1[p] = a1;
+    s2[p] = a2;
+  }
+}
+
+__global__ void finalize_kernel(int64_t npix, double R, const double* dp, const double* s1,
+                                const double* s2, double* mean, double* se) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const double m = s1[p] / R;
+    if (mean) mean[p] = dp[p] + m;
+    if (se) se[p] = sqrt(fmax((s2[p] - s1[p] * m) / (R - 1.0), 0.0));
+  }
+}
+
+__global__ void root_q_kernel(const double* __restrict__ lam_q, int hs1, int qs2, double scale,
+                              double* __restrict__ root_q) {
+  const int64_t tot = (int64_t)hs1 * qs2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int a = (int)(e / hs1), bc = (int)(e % hs1);   // root_q[a][b] <- lam_q[b][a]
+    root_q[e] = sqrt(fmax(lam_q[(int64_t)bc * qs2 + a], 0.0)) * scale;
+  }
+}
+
+Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2, double scale,
+                        double* out_q, cudaStream_t st);
+
+static int64_t next_fft_len(int64_t m) {
+  if (m <= 1) return 1;
+  int64_t best = -1;
+  for (int64_t two = 1; two < 4 * m; two *= 2) {
+    int64_t v = two;
+    while (v < m) v *= 3;
+    if (best < 0 || v < best) best = v;
+  }
+  return best;
+}
+
+Status ensure_embedding(rk_setup* s, cudaStream_t st) {
+  if (s->emb.ready) return Status::ok();
+  int64_t p1 = next_fft_len(2 * (int64_t)s->M1 - 1), p2 = next_fft_len(2 * (int64_t)s->M2 - 1);
+  double lmin = 0, lmax = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const int hs1 = (int)(p1 / 2 + 1), qs2 = (int)(p2 / 2 + 1);
+    double* lam = nullptr;
+    RK_CUDA_TRY(cudaMalloc(&lam, sizeof(double) * (size_t)hs1 * qs2));
+    Status sp = spectrum_quarter(s->mat, s->grid.hx, s->grid.hy, (int)p1, (int)p2, 1.0, lam, st);
+    if (!sp.good()) { cudaFree(lam); return sp; }
+    std::vector<double> h((size_t)hs1 * qs2);
+    RK_CUDA_TRY(cudaMemcpy(h.data(), lam, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+    lmin = *std::min_element(h.begin(), h.end());
+    lmax = *std::max_element(h.begin(), h.end());
+    if (!(lmin < -1.0e-8 * lmax)) {
+      Embedding& e = s->emb;
+      e.ps1 = (int)p1;
+      e.ps2 = (int)p2;
+      e.doubled = attempt;
+      e.hs1 = hs1;
+      e.qs2 = qs2;
+      RK_TRY(plan_for(e.ps1, &e.pl1));
+      RK_TRY(plan_for(e.ps2, &e.pl2));
+      RK_CUDA_TRY(cudaMalloc(&e.root_q, sizeof(double) * (size_t)hs1 * qs2));
+      const double P = (double)p1 * (double)p2;
+      root_q_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)hs1 * qs2, 256), 148 * 32), 256, 0, st>>>(
+          lam, hs1, qs2, std::sqrt(P) / P, e.root_q);
+      count_launch();
+      RK_LAUNCH_CHECK();
+      RK_CUDA_TRY(cudaStreamSynchronize(st));
+      cudaFree(lam);
+      e.ready = true;
+      return Status::ok();
+    }
+    cudaFree(lam);
+    p1 = next_fft_len(2 * p1);
+    p2 = next_fft_len(2 * p2);
+  }
+  char b[256];
+  snprintf(b, sizeof b,
+           "circulant embedding is not positive semidefinite even after doubling; most negative "
+           "eigenvalue %.6e",
+           lmin);
+  return Status::err(RK_NUMERIC, b);
+}
+
+static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, int batch,
+                            double* g, cudaStream_t st) {
+  RK_TRY(ensure_embedding(s, st));
+  const Embedding& e = s->emb;
+  const int64_t ldV = (e.ps2 + 1) & ~1;
+  double2* V = nullptr;
+  RK_TRY(scratch_alloc((void**)&V, sizeof(double2) * (size_t)s->M1 * ldV * batch, st));
+  CsRowArgs ra{};
+  ra.pl = e.pl1;
+  ra.lpc = pick_lpc(e.pl1, 4);
+  ra.ps1 = e.ps1;
+  ra.ps2 = e.ps2;
+  ra.keep = s->M1;
+  ra.root_q = e.root_q;
+  ra.rq_ld = e.hs1;
+  ra.seed = seed;
+  ra.j0 = j0;
+  ra.direct = direct;
+  ra.V = V;
+  ra.ldV = ldV;
+  ra.V_bstride = (int64_t)s->M1 * ldV;
+  {
+    const dim3 grid((unsigned)ceil_div(e.ps2, ra.lpc), (unsigned)batch);
+    const size_t smem = sizeof(double2) * e.ps1 * ra.lpc;
+    RK_TRY(set_smem_attr((const void*)cs_row_kernel, smem));
+    cs_row_kernel<<<grid, ra.lpc * e.pl1.nthr, smem, st>>>(ra);
+    count_launch();
+    RK_LAUNCH_CHECK();
+  }
+  CsColArgs ca{};
+  ca.pl = e.pl2;
+  ca.lpc = pick_lpc(e.pl2, 4);
+  ca.ncols = s->M1;
+  ca.keep = s->M2;
+  ca.V = V;
+  ca.ldV = ldV;
+  ca.V_bstride = ra.V_bstride;
+  ca.g = g;
+  ca.g_bstride = (int64_t)s->M1 * s->M2;
+  {
+    const dim3 grid((unsigned)ceil_div(s->M1, ca.lpc), (unsigned)batch);
+    const size_t smem = sizeof(double2) * e.ps2 * ca.lpc;
+    RK_TRY(set_smem_attr((const void*)cs_col_kernel, smem));
+    cs_col_kernel<<<grid, ca.lpc * e.pl2.nthr, smem, st>>>(ca);
+    count_launch();
+    RK_LAUNCH_CHECK();
+  }
+  scratch_free(V, st);
+  return Status::ok();
+}
+
+static Status obs_local(const rk_setup* s, double tau2, const double* g, uint64_t seed, int64_t j0,
+                        int direct, int batch, double* z, cudaStream_t st) {
+  if (s->cond_var_min < -1.0e-10 * s->model.sigma2) {
+    char b[160];
+    snprintf(b, sizeof b, "negative conditional variance %.3e; K_N solve inconsistent",
+             s->cond_var_min);
+    return Status::err(RK_NUMERIC, b);
+  }
+  ObsArgs a;
+  a.base = s->base;
+  a.weights = s->weights;
+  a.cond_var = s->cond_var;
+  a.n = s->n;
+  a.M = s->M;
+  a.bs = s->bs;
+  a.M1 = s->M1;
+  a.g = g;
+  a.g_bstride = (int64_t)s->M1 * s->M2;
+  a.sqrt_tau2 = std::sqrt(tau2);
+  a.seed = seed;
+  a.j0 = j0;
+  a.direct = direct;
+  a.z = z;
+  const dim3 grid((unsigned)std::min<int64_t>(ceil_div(s->n, 128), 4096), (unsigned)batch);
+  obs_local_kernel<<<grid, 128, 0, st>>>(a);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  return Status::ok();
+}
+
+// ------------------------------------------------------------------- fit
+#define RK_CUBLAS_TRY(expr)                                                                  \
+  do {                                                                                       \
+    cublasStatus_t _b = (expr);                                                              \
+    if (_b != CUBLAS_STATUS_SUCCESS)                                                         \
+      return Status::err(RK_CUDA, std::string("cuBLAS status ") + std::to_string((int)_b) + \
+                                      " at " #expr);                                        \
+  } while (0)
+
+// dense M = K + tau2 I (+ ridge) column-major, cdist distances (covariance.py:100-116)
+__global__ void dense_cov_kernel(MaternDev P, const double* __restrict__ obs, int64_t n, double diag_add,
+                                 double* __restrict__ Mm, int* bad) {
+  const int64_t tot = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / n, i = e % n;
+    if (i > j) continue;   // only the upper triangle is read by potrf(UPPER)
+    const double dx = obs[2 * i] - obs[2 * j], dy = obs[2 * i + 1] - obs[2 * j + 1];
+    const double d = sqrt(dx * dx + dy * dy);
+    double v = matern_cov(P, d, bad);
+    if (i == j) v += diag_add;
+    Mm[e] = v;
+  }
+}
+
+__global__ void add_diag_kernel(double* Mm, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    Mm[i * n + i] += v;
+}
+
+__global__ void zero_lower_kernel(double* U, int64_t n) {
+  const int64_t tot = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / n, i = e % n;
+    if (i > j) U[e] = 0.0;
+  }
+}
+
+// r[:, b] = z[:, b] - X beta[:, b]   (exact.py:65)
+__global__ void resid_kernel(const double* __restrict__ z, const double* __restrict__ X, int64_t n,
+                             int p, const double* __restrict__ beta, int batch, double* __restrict__ r) {
+  const int64_t tot = n * batch;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / n, i = e % n;
+    double xb = 0.0;
+    for (int q = 0; q < p; ++q) xb = fma(X[(int64_t)q * n + i], beta[b * p + q], xb);
+    r[e] = z[e] - xb;
+  }
+}
+
+struct GramLU {
+  double lu[64];
+  int piv[8];
+  int p;
+};
+
+// beta[:, b] = gram^-1 rhs[:, b] from the host LU with partial pivoting (np.linalg.solve)
+__global__ void gram_solve_kernel(GramLU g, double* rhs, int batch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  double x[8];
+  const int p = g.p;
+  for (int i = 0; i < p; ++i) x[i] = rhs[(int64_t)b * p + i];
+  for (int i = 0; i < p; ++i) {
+    const int pi = g.piv[i];
+    if (pi != i) { const double t = x[i]; x[i] = x[pi]; x[pi] = t; }
+  }
+  for (int i = 0; i < p; ++i)
+    for (int k = 0; k < i; ++k) x[i] -= g.lu[i * p + k] * x[k];
+  for (int i = p - 1; i >= 0; --i) {
+    for (int k = i + 1; k < p; ++k) x[i] -= g.lu[i * p + k] * x[k];
+    x[i] /= g.lu[i * p + i];
+  }
+  for (int i = 0; i < p; ++i) rhs[(int64_t)b * p + i] = x[i];
+}
+
+static bool lu_factor(std::vector<double>& a, int p, std::vector<int>& piv) {
+  piv.assign(p, 0);
+  for (int k = 0; k < p; ++k) {
+    int m = k;
+    for (int i = k + 1; i < p; ++i)
+      if (std::fabs(a[(size_t)i * p + k]) > std::fabs(a[(size_t)m * p + k])) m = i;
+    piv[k] = m;
+    if (a[(size_t)m * p + k] == 0.0) return false;
+    if (m != k)
+      for (int j = 0; j < p; ++j) std::swap(a[(size_t)k * p + j], a[(size_t)m * p + j]);
+    for (int i = k + 1; i < p; ++i) {
+      a[(size_t)i * p + k] /= a[(size_t)k * p + k];
+      for (int j = k + 1; j < p; ++j) a[(size_t)i * p + j] -= a[(size_t)i * p + k] * a[(size_t)k * p + j];
+    }
+  }
+  return true;
+}
+
+static GramLU gram_args(const rk_fit* f) {
+  GramLU g{};
+  g.p = f->p;
+  for (int i = 0; i < f->p * f->p; ++i) g.lu[i] = f->gram_lu[i];
+  for (int i = 0; i < f->p; ++i) g.piv[i] = f->gram_piv[i];
+  return g;
+}
+
+// GLS for `batch` right-hand sides Z (n x batch, column-major) -> beta (p x batch), C (n x batch)
+static Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C,
+                        cudaStream_t st) {
+  cublasHandle_t h = (cublasHandle_t)f->cublas;
+  RK_CUBLAS_TRY(cublasSetStream(h, st));
+  const int n = (int)f->n, p = f->p, nb = (int)batch;
+  const double one = 1.0, zero = 0.0;
+  double* A = nullptr;
+  RK_TRY(scratch_alloc((void**)&A, sizeof(double) * (size_t)n * nb, st));
+  RK_CUDA_TRY(cudaMemcpyAsync(A, Z, sizeof(double) * (size_t)n * nb, cudaMemcpyDeviceToDevice, st));
+  // a = L^-1 z  (L = U^T)
+  RK_CUBLAS_TRY(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
+                            CUBLAS_DIAG_NON_UNIT, n, nb, &one, f->U, n, A, n));
+  // rhs = b' a
+  RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, nb, n, &one, f->B, n, A, n, &zero, beta, p));
+  gram_solve_kernel<<<(nb + 127) / 128, 128, 0, st>>>(gram_args(f), beta, nb);
+  count_launch();
+  // resid = z - X beta ; half = L^-1 resid ; c = L^-T half
+  resid_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)n * nb, 256), 148 * 32), 256, 0, st>>>(
+      Z, f->X, n, p, beta, nb, C);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  RK_CUBLAS_TRY(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
+                            CUBLAS_DIAG_NON_UNIT, n, nb, &one, f->U, n, C, n));
+  RK_CUBLAS_TRY(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                            CUBLAS_DIAG_NON_UNIT, n, nb, &one, f->U, n, C, n));
+  scratch_free(A, st);
+  return Status::ok();
+}
+
+static void free_fit(rk_fit* f) {
+  if (!f) return;
+  cudaFree(f->U);
+  cudaFree(f->X);
+  cudaFree(f->B);
+  cudaFree(f->beta);
+  cudaFree(f->c);
+  if (f->cublas) cublasDestroy((cublasHandle_t)f->cublas);
+  delete f;
+}
+
+// common tail: X upload, B = L^-1 X, gram LU
+static Status fit_prepare_x(rk_fit* f, const double* X_host) {
+  const int64_t n = f->n;
+  const int p = f->p;
+  std::vector<double> Xc((size_t)n * p);
+  for (int64_t i = 0; i < n; ++i)
+    for (int q = 0; q < p; ++q) Xc[(size_t)q * n + i] = X_host ? X_host[(size_t)i * p + q] : 1.0;
+  RK_CUDA_TRY(cudaMalloc(&f->X, sizeof(double) * n * p));
+  RK_CUDA_TRY(cudaMalloc(&f->B, sizeof(double) * n * p));
+  RK_CUDA_TRY(cudaMemcpy(f->X, Xc.data(), sizeof(double) * n * p, cudaMemcpyHostToDevice));
+  RK_CUDA_TRY(cudaMemcpy(f->B, Xc.data(), sizeof(double) * n * p, cudaMemcpyHostToDevice));
+  cublasHandle_t h = (cublasHandle_t)f->cublas;
+  RK_CUBLAS_TRY(cublasSetStream(h, 0));
+  const double one = 1.0, zero = 0.0;
+  RK_CUBLAS_TRY(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
+                            CUBLAS_DIAG_NON_UNIT, (int)n, p, &one, f->U, (int)n, f->B, (int)n));
+  double* G = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&G, sizeof(double) * p * p));
+  RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, p, (int)n, &one, f->B, (int)n, f->B,
+                            (int)n, &zero, G, p));
+  std::vector<double> g((size_t)p * p);
+  RK_CUDA_TRY(cudaMemcpy(g.data(), G, sizeof(double) * p * p, cudaMemcpyDeviceToHost));
+  cudaFree(G);
+  // column-major p x p -> row-major (symmetric anyway)
+  std::vector<double> gr((size_t)p * p);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) gr[(size_t)i * p + j] = g[(size_t)j * p + i];
+  f->gram_lu = gr;
+  if (!lu_factor(f->gram_lu, p, f->gram_piv))
+    return Status::err(RK_NUMERIC, "singular GLS Gram matrix X' M^-1 X");
+  return Status::ok();
+}
+
+}  // namespace rk
+
+using namespace rk;
+
+static int finish_sim(const Status& s) {
+  if (!s.good()) rk::set_error(s.code, s.msg);
+  return s.code;
+}
+
+extern "C" {
+
+uint64_t rk_draw_seed(uint64_t seed, uint64_t j) { return draw_seed(seed, j); }
+
+rk_status rk_philox_normals(uint64_t seed, uint64_t stream_id, uint64_t start, int64_t count,
+                            double* out_dev, void* stream) {
+  auto run = [&]() -> Status {
+    if (count <= 0) return Status::ok();
+    philox_kernel<<<(int)std::min<int64_t>(ceil_div(count, 256), 148 * 32), 256, 0,
+                    (cudaStream_t)stream>>>(seed, stream_id, start, count, out_dev, nullptr);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_philox_raw(uint64_t seed, uint64_t stream_id, uint64_t start, int64_t count,
+                        uint64_t* out_dev, void* stream) {
+  auto run = [&]() -> Status {
+    if (count <= 0) return Status::ok();
+    philox_kernel<<<(int)std::min<int64_t>(ceil_div(count, 256), 148 * 32), 256, 0,
+                    (cudaStream_t)stream>>>(seed, stream_id, start, count, nullptr, out_dev);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_setup_embedding(rk_setup* s, int32_t embed_out[2], int32_t* doubled) {
+  Status st = ensure_embedding(s, 0);
+  if (st.good()) {
+    if (embed_out) { embed_out[0] = s->emb.ps1; embed_out[1] = s->emb.ps2; }
+    if (doubled) *doubled = s->emb.doubled;
+  }
+  return (rk_status)finish_sim(st);
+}
+
+rk_status rk_sim_unconditional_dev(rk_setup* s, uint64_t seed, double* field_dev, void* stream) {
+  return (rk_status)finish_sim(uncond_fields(s, seed, 0, 1, 1, field_dev, (cudaStream_t)stream));
+}
+
+rk_status rk_sim_obs_local_dev(const rk_setup* s, double tau2, const double* field_dev, uint64_t seed,
+                               double* z_dev, void* stream) {
+  return (rk_status)finish_sim(obs_local(s, tau2, field_dev, seed, 0, 1, 1, z_dev, (cudaStream_t)stream));
+}
+
+rk_status rk_fit_create(const rk_model* model, const double* obs_host, int64_t n, const double* z_host,
+                        const double* X_host, int32_t p, rk_fit** out, int32_t* ridge_applied) {
+  auto run = [&]() -> Status {
+    if (n < 1 || p < 1 || p > 8 || n < p) return Status::err(RK_DOMAIN, "need n >= p >= 1 (p <= 8)");
+    rk_fit* f = new rk_fit();
+    std::unique_ptr<rk_fit, void (*)(rk_fit*)> guard(f, free_fit);
+    RK_CUDA_TRY(cudaGetDevice(&f->device));
+    f->model = *model;
+    f->n = n;
+    f->p = p;
+    cublasHandle_t h;
+    RK_CUBLAS_TRY(cublasCreate(&h));
+    f->cublas = h;
+    const MaternDev P = make_matern_dev(*model);
+    double* dobs = nullptr;
+    int* bad = nullptr;
+    RK_CUDA_TRY(cudaMalloc(&dobs, sizeof(double) * 2 * n));
+    RK_CUDA_TRY(cudaMalloc(&bad, sizeof(int)));
+    RK_CUDA_TRY(cudaMemset(bad, 0, sizeof(int)));
+    RK_CUDA_TRY(cudaMemcpy(dobs, obs_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+    RK_CUDA_TRY(cudaMalloc(&f->U, sizeof(double) * (size_t)n * n));
+    cusolverDnHandle_t sh;
+    if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) return Status::err(RK_CUDA, "cusolverDnCreate failed");
+    int lwork = 0;
+    cusolverDnDpotrf_bufferSize(sh, CUBLAS_FILL_MODE_UPPER, (int)n, f->U, (int)n, &lwork);
+    double* work = nullptr;
+    int* info = nullptr;
+    RK_CUDA_TRY(cudaMalloc(&work, sizeof(double) * std::max(lwork, 1)));
+    RK_CUDA_TRY(cudaMalloc(&info, sizeof(int)));
+    // trace(M) = sum(sigma2 * phi(0) + tau2) (exact.py:102)
+    const double diag = model->sigma2 + model->tau2;
+    double trace = 0.0;
+    for (int64_t i = 0; i < n; ++i) trace += diag;
+    const double ridge = 1.0e-10 * trace / (double)n;
+    int hinfo = 0;
+    *ridge_applied = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      dense_cov_kernel<<<(int)std::min<int64_t>(ceil_div(n * n, 256), 148 * 64), 256>>>(
+          P, dobs, n, model->tau2, f->U, bad);
+      count_launch();
+      RK_LAUNCH_CHECK();
+      if (attempt == 1) {  // (K + tau2 I) + ridge I  (exact.py:33-35)
+        add_diag_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 4096), 256>>>(f->U, n, ridge);
+        count_launch();
+      }
+      if (cusolverDnDpotrf(sh, CUBLAS_FILL_MODE_UPPER, (int)n, f->U, (int)n, work, lwork, info) !=
+          CUSOLVER_STATUS_SUCCESS)
+        return Status::err(RK_CUDA, "cusolverDnDpotrf failed");
+      RK_CUDA_TRY(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
+      if (hinfo == 0) break;
+      if (attempt == 0) *ridge_applied = 1;
+    }
+    cusolverDnDestroy(sh);
+    cudaFree(work);
+    cudaFree(info);
+    int hb = 0;
+    RK_CUDA_TRY(cudaMemcpy(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(bad);
+    cudaFree(dobs);
+    if (hb) return Status::err(RK_NUMERIC, "Temme series / continued fraction for K_nu failed to converge");
+    if (hinfo != 0)
+      return Status::err(RK_NUMERIC, "Cholesky of the observation covariance M failed even with ridge");
+    zero_lower_kernel<<<(int)std::min<int64_t>(ceil_div(n * n, 256), 148 * 64), 256>>>(f->U, n);
+    count_launch();
+    RK_TRY(fit_prepare_x(f, X_host));
+    RK_CUDA_TRY(cudaMalloc(&f->beta, sizeof(double) * p));
+    RK_CUDA_TRY(cudaMalloc(&f->c, sizeof(double) * n));
+    double* z = nullptr;
+    RK_CUDA_TRY(cudaMalloc(&z, sizeof(double) * n));
+    RK_CUDA_TRY(cudaMemcpy(z, z_host, sizeof(double) * n, cudaMemcpyHostToDevice));
+    RK_TRY(gls_batch(f, z, 1, f->beta, f->c, 0));
+    RK_CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(z);
+    *out = guard.release();
+    return Status::ok();
+  };
+  int32_t r = 0;
+  if (!ridge_applied) ridge_applied = &r;
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_fit_import(const rk_model* model, const double* obs_host, int64_t n, const double* X_host,
+                        int32_t p, const double* chol_host, const double* beta_host,
+                        const double* c_host, rk_fit** out) {
+  auto run = [&]() -> Status {
+    (void)obs_host;
+    if (n < 1 || p < 1 || p > 8) return Status::err(RK_DOMAIN, "need n >= p >= 1 (p <= 8)");
+    rk_fit* f = new rk_fit();
+    std::unique_ptr<rk_fit, void (*)(rk_fit*)> guard(f, free_fit);
+    RK_CUDA_TRY(cudaGetDevice(&f->device));
+    f->model = *model;
+    f->n = n;
+    f->p = p;
+    cublasHandle_t h;
+    RK_CUBLAS_TRY(cublasCreate(&h));
+    f->cublas = h;
+    // row-major lower L == column-major upper U = L^T
+    RK_CUDA_TRY(cudaMalloc(&f->U, sizeof(double) * (size_t)n * n));
+    RK_CUDA_TRY(cudaMemcpy(f->U, chol_host, sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+    RK_TRY(fit_prepare_x(f, X_host));
+    RK_CUDA_TRY(cudaMalloc(&f->beta, sizeof(double) * p));
+    RK_CUDA_TRY(cudaMalloc(&f->c, sizeof(double) * n));
+    RK_CUDA_TRY(cudaMemcpy(f->beta, beta_host, sizeof(double) * p, cudaMemcpyHostToDevice));
+    RK_CUDA_TRY(cudaMemcpy(f->c, c_host, sizeof(double) * n, cudaMemcpyHostToDevice));
+    *out = guard.release();
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_fit_destroy(rk_fit* f) {
+  free_fit(f);
+  return RK_OK;
+}
+
+rk_status rk_fit_info(const rk_fit* f, int64_t* n, int32_t* p) {
+  if (n) *n = f->n;
+  if (p) *p = f->p;
+  return RK_OK;
+}
+
+rk_status rk_fit_copy_out(const rk_fit* f, double* beta_host, double* c_host, double* chol_host) {
+  auto run = [&]() -> Status {
+    if (beta_host) RK_CUDA_TRY(cudaMemcpy(beta_host, f->beta, sizeof(double) * f->p, cudaMemcpyDeviceToHost));
+    if (c_host) RK_CUDA_TRY(cudaMemcpy(c_host, f->c, sizeof(double) * f->n, cudaMemcpyDeviceToHost));
+    if (chol_host)
+      RK_CUDA_TRY(cudaMemcpy(chol_host, f->U, sizeof(double) * (size_t)f->n * f->n, cudaMemcpyDeviceToHost));
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_refit_dev(const rk_fit* f, const double* z_dev, int64_t batch, double* beta_dev,
+                       double* c_dev, void* stream) {
+  return (rk_status)finish_sim(gls_batch(f, z_dev, batch, beta_dev, c_dev, (cudaStream_t)stream));
+}
+
+rk_status rk_ensemble_accumulate(rk_setup* s, const rk_fit* f, uint64_t seed, int64_t j0, int64_t count,
+                                 const double* xg_dev, const double* data_pred_dev, double* s1_dev,
+                                 double* s2_dev, double* draws_dev, int32_t batch, void* stream) {
+  auto run = [&]() -> Status {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (f->n != s->n) return Status::err(RK_DOMAIN, "fit and setup disagree on the number of observations");
+    if (!xg_dev && f->p != 1)
+      return Status::err(RK_DOMAIN, "grid covariates are required when beta_hat has more than one entry");
+    RK_TRY(ensure_embedding(s, st));
+    const int B = std::max(1, (int)batch);
+    const int64_t npix = (int64_t)s->m1 * s->m2;
+    double *G = nullptr, *Z = nullptr, *C = nullptr, *BT = nullptr, *E = nullptr;
+    RK_TRY(scratch_alloc((void**)&G, sizeof(double) * (size_t)s->M1 * s->M2 * B, st));
+    RK_TRY(scratch_alloc((void**)&Z, sizeof(double) * (size_t)s->n * B, st));
+    RK_TRY(scratch_alloc((void**)&C, sizeof(double) * (size_t)s->n * B, st));
+    RK_TRY(scratch_alloc((void**)&BT, sizeof(double) * (size_t)f->p * B, st));
+    RK_TRY(scratch_alloc((void**)&E, sizeof(double) * (size_t)npix * B, st));
+    for (int64_t j = j0; j < j0 + count; j += B) {
+      const int bc = (int)std::min<int64_t>(B, j0 + count - j);
+      RK_TRY(uncond_fields(s, seed, j, 0, bc, G, st));
+      RK_TRY(obs_local(s, f->model.tau2, G, seed, j, 0, bc, Z, st));
+      RK_TRY(gls_batch(f, Z, bc, BT, C, st));
+      PredictBatch pb;
+      pb.batch = bc;
+      pb.c = C;
+      pb.c_stride = s->n;
+      pb.beta = BT;
+      pb.p = f->p;
+      pb.xg = xg_dev;
+      pb.g = G;
+      pb.out = E;
+      RK_TRY(predict_batch(s, pb, st));
+      accumulate_kernel<<<(int)std::min<int64_t>(ceil_div(npix, 256), 148 * 16), 256, 0, st>>>(
+          E, bc, npix, data_pred_dev, s1_dev, s2_dev, draws_dev ? draws_dev + (j - j0) * npix : nullptr);
+      count_launch();
+      RK_LAUNCH_CHECK();
+    }
+    scratch_free(G, st);
+    scratch_free(Z, st);
+    scratch_free(C, st);
+    scratch_free(BT, st);
+    scratch_free(E, st);
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_ensemble_finalize(int64_t n_pix, int64_t n_draws, const double* data_pred_dev,
+                               const double* s1_dev, const double* s2_dev, double* mean_dev,
+                               double* se_dev, void* stream) {
+  auto run = [&]() -> Status {
+    if (n_draws < 2) return Status::err(RK_DOMAIN, "need at least 2 draws, got " + std::to_string(n_draws));
+    finalize_kernel<<<(int)std::min<int64_t>(ceil_div(n_pix, 256), 148 * 16), 256, 0,
+                      (cudaStream_t)stream>>>(n_pix, (double)n_draws, data_pred_dev, s1_dev, s2_dev,
+                                              mean_dev, se_dev);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+}  // extern "C"

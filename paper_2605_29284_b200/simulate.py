@@ -1,0 +1,180 @@
+"""Conditional-simulation ensembles on the B200.
+
+Interface of reference simulate.py:52-192: ``draw_seed``, ``sim_unconditional_grid``,
+``sim_obs_local``, ``conditional_draw``, ``generate_ensemble`` and ``Ensemble``,
+with the same Philox4x64-10 streams (key = (seed, stream), pre-incremented
+counter) and inverse-CDF normals, so draws match the reference to roundoff.
+
+``generate_ensemble`` runs realizations in batches through one fused device
+pipeline (rk_ensemble_accumulate): Philox+normal+sqrt(lambda) fused into the
+row IFFT pass, column IFFT, local observation simulation, batched GLS refit,
+the rapid predict passes with the draw epilogue, and in-order per-pixel moment
+accumulation.  Moments are kept per fixed chunk of realizations (independent
+of how many GPUs run them) and combined in chunk order, so the ensemble is
+bitwise identical on 1, 2, 4 or 8 GPUs (see distributed.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .errors import DomainError
+from .exact import as_device_fit, refit_coefficients
+from .rapid import GRID_SETUPS, _fixed_inputs, predict_rapid
+
+__all__ = ["Ensemble", "RNG_ALGORITHM", "draw_seed", "sim_unconditional_grid", "sim_obs_local",
+           "conditional_draw", "generate_ensemble", "ensemble_chunks", "ENSEMBLE_CHUNKS"]
+
+RNG_ALGORITHM = "philox4x64-10"
+ENSEMBLE_CHUNKS = 8
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(v: int) -> int:
+    z = (v + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return (z ^ (z >> 31)) & _M64
+
+
+def draw_seed(seed: int, j: int) -> int:
+    """seed XOR splitmix64(j) (simulate.py:52-62)."""
+    return (int(seed) ^ _splitmix64(int(j))) & _M64
+
+
+@dataclass(frozen=True)
+class Ensemble:
+    draws: object            # (n_draws, m2, m1) numpy array, or None with keep_draws=False
+    seed: int
+    n_draws: int
+    mean_field: np.ndarray
+    empirical_se: np.ndarray
+    rng_algorithm: str = RNG_ALGORITHM
+
+
+def _embedding_handle(model, setup_or_grid):
+    """Device object carrying the circulant embedding of (model, grid)."""
+    from .rapid import RapidSetup
+    if isinstance(setup_or_grid, RapidSetup) and setup_or_grid.model == model:
+        return setup_or_grid.handle
+    grid = setup_or_grid.grid if isinstance(setup_or_grid, RapidSetup) else setup_or_grid
+    return GRID_SETUPS.get(model, grid).ptr
+
+
+def embedding_dims(model, grid):
+    emb = (N.C.c_int32 * 2)()
+    dbl = N.C.c_int32()
+    N.call("rk_setup_embedding", _embedding_handle(model, grid), N.C.byref(emb), N.C.byref(dbl))
+    return int(emb[0]), int(emb[1]), bool(dbl.value)
+
+
+def sim_unconditional_grid(model, grid, seed: int, device: bool = False):
+    """Stationary field on the padded grid, (M2, M1), by circulant embedding (simulate.py:103-118)."""
+    h = _embedding_handle(model, grid)
+    g = grid.grid if hasattr(grid, "embed_dims") else grid
+    M1, M2 = g.total_dims
+    out = D.empty((M2, M1))
+    N.call("rk_sim_unconditional_dev", h, int(seed) & _M64, N.ptr(out), N.stream_ptr())
+    return out if device else out.cpu().numpy()
+
+
+def sim_obs_local(model, setup, grid_field, seed: int):
+    """z_i = A_i . g[N(i)] + sqrt(cond_var_i) eta_i + sqrt(tau2) eps_i (simulate.py:121-143)."""
+    expect = tuple(setup.grid.total_dims[::-1])
+    if tuple(grid_field.shape) != expect:
+        raise DomainError(f"grid field shape {tuple(grid_field.shape)} does not match {expect}")
+    dev = D.is_device_tensor(grid_field)
+    g = D.to_device(grid_field)
+    z = D.empty((setup.n_obs,))
+    N.call("rk_sim_obs_local_dev", setup.handle, float(model.tau2), N.ptr(g), int(seed) & _M64,
+           N.ptr(z), N.stream_ptr())
+    return z if dev else z.cpu().numpy()
+
+
+def conditional_draw(krig, setup, seed: int, grid_covariates=None, data_prediction=None):
+    """data_prediction + (interior(g_uncond) - predict_rapid(refit(z_sim))) (simulate.py:146-159)."""
+    f = as_device_fit(krig)
+    g = sim_unconditional_grid(f.model, setup, draw_seed(seed, 101), device=True)
+    zs = sim_obs_local(f.model, setup, g, draw_seed(seed, 202))
+    bs, cs = refit_coefficients(f, D.to_device(zs))
+    if data_prediction is None:
+        data_prediction = predict_rapid(setup, D.to_device(f.c), f.beta_hat, grid_covariates)
+    sim = predict_rapid(setup, cs, bs, grid_covariates)
+    l, _, b, _ = setup.grid.pad
+    m1, m2 = setup.grid.interior_dims
+    dp = D.to_device(data_prediction)
+    draw = dp + (g[b:b + m2, l:l + m1] - sim)
+    return draw.cpu().numpy()
+
+
+def ensemble_chunks(n_draws: int, n_chunks: int = ENSEMBLE_CHUNKS):
+    """Fixed chunk boundaries [j0, j1) of the realization index range."""
+    k = max(1, min(n_chunks, n_draws))
+    b = [(i * n_draws) // k for i in range(k + 1)]
+    return [(b[i], b[i + 1]) for i in range(k) if b[i + 1] > b[i]]
+
+
+def _prepare(krig, setup, grid_covariates):
+    f = as_device_fit(krig)
+    beta, xg = _fixed_inputs(setup, f.beta_hat, grid_covariates)
+    xd = None if xg is None else D.to_device(xg)
+    dp = predict_rapid(setup, D.to_device(f.c), f.beta_hat, grid_covariates)
+    return f, xd, dp
+
+
+def accumulate_chunk(setup, f, seed, j0, j1, xd, dp, draws=None, batch=32, stream=None):
+    """Per-chunk partial moments (s1, s2) of e_j = draw_j - data_pred, j in [j0, j1)."""
+    m1, m2 = setup.grid.interior_dims
+    s1 = D.zeros((m2, m1))
+    s2 = D.zeros((m2, m1))
+    N.call("rk_ensemble_accumulate", setup.handle, f.handle, int(seed) & _M64, int(j0), int(j1 - j0),
+           N.ptr(xd), N.ptr(dp), N.ptr(s1), N.ptr(s2), N.ptr(draws), int(batch),
+           N.stream_ptr(stream))
+    return s1, s2
+
+
+def combine_chunks(partials):
+    """Chunk partials summed in chunk order (deterministic, GPU-count independent)."""
+    s1 = partials[0][0].clone()
+    s2 = partials[0][1].clone()
+    for a, b in partials[1:]:
+        s1 += a
+        s2 += b
+    return s1, s2
+
+
+def finalize(dp, s1, s2, n_draws):
+    mean = D.empty(dp.shape)
+    se = D.empty(dp.shape)
+    N.call("rk_ensemble_finalize", dp.numel(), int(n_draws), N.ptr(dp), N.ptr(s1), N.ptr(s2),
+           N.ptr(mean), N.ptr(se), N.stream_ptr())
+    return mean, se
+
+
+def generate_ensemble(krig, setup, n_draws: int, seed: int, grid_covariates=None, *,
+                      keep_draws: bool = True, batch: int = 32, device: bool = False):
+    """n_draws conditional draws; draw j uses sub-seed draw_seed(seed, j) (simulate.py:174-192).
+
+    ``keep_draws=False`` skips materialising the (n_draws, m2, m1) stack (the
+    reference always returns it; at 4096^2 x 256 it is 34 GB) — mean and SE
+    are accumulated on the fly either way.
+    """
+    if n_draws < 2:
+        raise DomainError(f"need at least 2 draws, got {n_draws}")
+    f, xd, dp = _prepare(krig, setup, grid_covariates)
+    m1, m2 = setup.grid.interior_dims
+    draws = D.empty((n_draws, m2, m1)) if keep_draws else None
+    parts = []
+    for j0, j1 in ensemble_chunks(n_draws):
+        dv = None if draws is None else draws[j0:j1]
+        parts.append(accumulate_chunk(setup, f, seed, j0, j1, xd, dp, dv, batch))
+    s1, s2 = combine_chunks(parts)
+    mean, se = finalize(dp, s1, s2, n_draws)
+    if device:
+        return Ensemble(draws, int(seed), int(n_draws), mean, se)
+    return Ensemble(None if draws is None else draws.cpu().numpy(), int(seed), int(n_draws),
+                    mean.cpu().numpy(), se.cpu().numpy())
