@@ -545,18 +545,23 @@ static Status build_setup(const rk_model* model, const rk_grid* grid, int L, con
   const size_t wsm = M <= 64 ? sizeof(double) * 2 * M * M : 0;
   const int wblocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 16);
   const int mpl = (M + 31) / 32;
+  auto launch_w = [&](auto kern) -> Status {
+    RK_TRY(set_smem_attr((const void*)kern, wsm));
+    kern<<<wblocks, 256, wsm>>>(wa);
+    return Status::ok();
+  };
   if (mpl <= 1) {
-    weights_kernel<1><<<wblocks, 256, wsm>>>(wa);
+    RK_TRY(launch_w(weights_kernel<1>));
   } else if (mpl <= 2) {
-    weights_kernel<2><<<wblocks, 256, wsm>>>(wa);
+    RK_TRY(launch_w(weights_kernel<2>));
   } else if (mpl <= 4) {
-    weights_kernel<4><<<wblocks, 256, wsm>>>(wa);
+    RK_TRY(launch_w(weights_kernel<4>));
   } else if (mpl <= 8) {
-    weights_kernel<8><<<wblocks, 256, wsm>>>(wa);
+    RK_TRY(launch_w(weights_kernel<8>));
   } else if (mpl <= 16) {
-    weights_kernel<16><<<wblocks, 256, wsm>>>(wa);
+    RK_TRY(launch_w(weights_kernel<16>));
   } else {
-    weights_kernel<32><<<wblocks, 256, wsm>>>(wa);
+    RK_TRY(launch_w(weights_kernel<32>));
   }
   count_launch();
   RK_LAUNCH_CHECK();
