@@ -1,0 +1,506 @@
+"""Benchmark of the B200 rapid-Kriging hot path (contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-extra]
+
+Headline (``value``): predicted grid points/s (fp64) of ``predict_rapid`` on
+BASELINE.json configs[1] (cfg2: n = 1368 mixture obs, 350 x 350 grid, L = 3,
+Matern nu = 1.0, universal Kriging with [1, x, y] covariates), inputs resident in
+HBM, L2 flushed between timed steps, device time from CUDA events on the
+launching stream.  Under torchrun each rank runs an independent replica
+("replicas only": a single predict does not shard) and ``value`` = points of all
+ranks / max-over-ranks time.  ``e2e`` = the same call through the public API on
+pinned HOST buffers (H2D of c / beta / X_g and D2H of the field inside the timed
+region).  ``extra.cs_cfg4`` = CS realizations/s for configs[3] (n = 5000,
+512^2, L = 3, R = 1024), realizations sharded over the ranks with one NCCL
+all-gather; ``extra.predict_cfg3`` = the 2048^2 large-grid predict.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+numpy oracle port, oracle/rk_oracle.py — /root/reference is not on the GPU box)
+on all host cores (one process per core, each running predicts) on the same
+workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+FP64_TFLOPS_MEASURED = 34.0   # tools/microbench.cu DFMA loop on this pool (profiles/round1_microbench.json)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if "Active" in v and "Not" not in v:
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+class L2Flush:
+    def __init__(self):
+        import torch
+        self.buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
+
+    def __call__(self):
+        self.buf.zero_()
+
+
+def build_predict_case(pk, wl, c_variants=4):
+    """Inputs of one predict workload, resident in HBM: setup (timed separately), c
+    from the GPU exact fit, beta, grid covariates."""
+    import torch
+    from paper_2605_29284_b200 import workloads
+    model = pk.CovarianceModel(wl.sigma2, wl.alpha, wl.nu, wl.tau2)
+    t0 = time.perf_counter()
+    f = pk.fit(model, wl.obs, wl.z, wl.X)
+    torch.cuda.synchronize()
+    t_fit = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    grid = pk.build_padded_grid(wl.domain, wl.dims, wl.L, wl.obs)
+    st = pk.build_setup(model, grid, wl.L, wl.obs)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    xg = workloads.grid_covariates_for(grid.interior_nodes(), wl.grid_covariates)
+    rng = np.random.default_rng(123)
+    cs = [f.c * (1.0 + 1e-3 * k) + (0 if k == 0 else 1e-3 * rng.normal(size=f.c.shape)) for k in range(c_variants)]
+    return dict(model=model, fit=f, grid=grid, setup=st, xg=xg, cs=cs, beta=f.beta_hat,
+                t_fit=t_fit, t_setup=t_setup)
+
+
+def time_predict_device(pk, case, steps, warmup, flush):
+    """Device-resident predict: per-step CUDA-event time, L2 flushed before each step."""
+    import torch
+    from paper_2605_29284_b200 import _native as N
+    st = case["setup"]
+    cds = [torch.as_tensor(c, device="cuda") for c in case["cs"]]
+    bd = torch.as_tensor(case["beta"], device="cuda")
+    xd = None if case["xg"] is None else torch.as_tensor(case["xg"], device="cuda").contiguous()
+    m1, m2 = st.grid.interior_dims
+    out = torch.empty((m2, m1), dtype=torch.float64, device="cuda")
+    for k in range(warmup):
+        pk.predict_rapid(st, cds[k % len(cds)], bd, xd, out=out)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    l0 = N.launch_count()
+    for k in range(steps):
+        flush()
+        ev[k][0].record()
+        pk.predict_rapid(st, cds[k % len(cds)], bd, xd, out=out)
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    launches = N.launch_count() - l0
+    ms = [a.elapsed_time(b) for a, b in ev]
+    return ms, launches, out
+
+
+def profile_passes(pk, case, reps, flush):
+    """Per-pass kernel times (CUDA events on the launching stream) and algorithmic bytes."""
+    import ctypes as C
+    import torch
+    from paper_2605_29284_b200 import _native as N
+    st = case["setup"]
+    cd = torch.as_tensor(case["cs"][0], device="cuda")
+    bd = torch.as_tensor(case["beta"], device="cuda")
+    xd = None if case["xg"] is None else torch.as_tensor(case["xg"], device="cuda").contiguous()
+    p = int(bd.numel())
+    m1, m2 = st.grid.interior_dims
+    out = torch.empty((m2, m1), dtype=torch.float64, device="cuda")
+    acc = np.zeros(3)
+    for r in range(reps + 1):
+        flush()
+        ms = (C.c_float * 3)()
+        N.call("rk_predict_profile", st.handle, N.ptr(cd), N.ptr(bd), p, N.ptr(xd), N.ptr(out),
+               N.stream_ptr(), C.byref(ms))
+        if r:
+            acc += np.array(list(ms))
+    b = (C.c_double * 3)()
+    N.call("rk_predict_traffic", st.handle, p if xd is not None else 0, C.byref(b))
+    return acc / reps, np.array(list(b))
+
+
+def fft_flops(n):
+    """Real fp64 flops of one complex length-n transform in our radix-9/6/8/4/2 schedule."""
+    per_pt = {9: 16.0, 6: 12.7, 8: 10.5, 4: 8.5, 3: 12.0, 2: 6.0}   # codelet + twiddle flops per point
+    rad, a, b, m = [], 0, 0, n
+    while m % 2 == 0:
+        m //= 2
+        a += 1
+    while m % 3 == 0:
+        m //= 3
+        b += 1
+    rad += [9] * (b // 2)
+    b -= 2 * (b // 2)
+    if b:
+        if a:
+            rad.append(6)
+            a -= 1
+        else:
+            rad.append(3)
+    rad += [8] * (a // 3)
+    a -= 3 * (a // 3)
+    if a:
+        rad.append(4 if a == 2 else 2)
+    return n * sum(per_pt[r] for r in rad)
+
+
+def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind):
+    st = case["setup"]
+    p1, p2 = st.embed_dims
+    H1 = p1 // 2 + 1
+    m1, m2 = st.grid.interior_dims
+    M1, M2 = st.grid.total_dims
+    flops = [ (M2 + 1) // 2 * fft_flops(p1), H1 * 2 * fft_flops(p2), (m2 + 1) // 2 * fft_flops(p1)]
+    dom = int(np.argmax(pass_ms))
+    names = ["pass1_gather_rowfft", "pass2_column_filter", "pass3_rowifft_epilogue"]
+    ach = pass_bytes[dom] / (pass_ms[dom] * 1e-3) / 1e9
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    fl = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
+    return {
+        "bound": "hbm", "kernel": names[dom], "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(ach / peak, 4), "traffic": None, "peak_source": peaks_kind,
+        "algorithmic_bytes": float(pass_bytes[dom]), "kernel_ms": round(float(pass_ms[dom]), 5),
+        "fp64_tflops": round(fl, 3), "fp64_peak_tflops": FP64_TFLOPS_MEASURED,
+        "fp64_frac": round(fl / FP64_TFLOPS_MEASURED, 4),
+        "passes": {names[i]: {"ms": round(float(pass_ms[i]), 5), "GB/s": round(pass_bytes[i] / (pass_ms[i] * 1e-3) / 1e9, 1),
+                              "fp64_TF/s": round(flops[i] / (pass_ms[i] * 1e-3) / 1e12, 3)} for i in range(3)},
+    }
+
+
+def time_predict_e2e(pk, case, steps, warmup, flush):
+    """Public API on pinned HOST buffers: H2D of c / beta / X_g, D2H of the field."""
+    import torch
+    st = case["setup"]
+    m1, m2 = st.grid.interior_dims
+    ch = [torch.from_numpy(np.ascontiguousarray(c)).pin_memory().numpy() for c in case["cs"]]
+    xg = None if case["xg"] is None else torch.from_numpy(np.ascontiguousarray(case["xg"])).pin_memory().numpy()
+    beta = np.ascontiguousarray(case["beta"])
+    out = torch.empty((m2, m1), dtype=torch.float64).pin_memory().numpy()
+    for k in range(warmup):
+        pk.predict_rapid(st, ch[k % len(ch)], beta, xg, out=out)
+    ms = []
+    for k in range(steps):
+        flush()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pk.predict_rapid(st, ch[k % len(ch)], beta, xg, out=out)
+        ms.append((time.perf_counter() - t0) * 1e3)
+    h2d = 8 * (ch[0].size + beta.size + (0 if xg is None else xg.size))
+    return ms, h2d, 8 * m1 * m2
+
+
+def cpu_baseline_predict(case, wl, seconds=10.0, min_reps=5):
+    """Oracle port (numpy/pocketfft, 1 core) on the same inputs — bounded sample."""
+    from oracle import rk_oracle as ro
+    from paper_2605_29284_b200 import workloads
+    model = ro.Model(wl.sigma2, wl.alpha, wl.nu, wl.tau2)
+    og = ro.make_grid(wl.domain, wl.dims, wl.L, wl.obs)
+    ost = ro.rapid_setup(model, og, wl.L, wl.obs)
+    xg = workloads.grid_covariates_for(og.interior_nodes(), wl.grid_covariates)
+    ref_field = ro.predict(ost, case["cs"][0], case["beta"], xg)   # warm-up + parity reference
+    times = []
+    t_start = time.perf_counter()
+    k = 0
+    while k < min_reps or time.perf_counter() - t_start < seconds:
+        t0 = time.perf_counter()
+        ro.predict(ost, case["cs"][k % len(case["cs"])], case["beta"], xg)
+        times.append(time.perf_counter() - t0)
+        k += 1
+    return times, ref_field
+
+
+# ------------------------------------------------------------------ CS
+def bench_cs(pk, steps, warmup, rank, world, R=1024, batch=32):
+    import torch
+    from paper_2605_29284_b200 import _native as N
+    from paper_2605_29284_b200 import workloads
+    from paper_2605_29284_b200.distributed import generate_ensemble_sharded
+    wl = workloads.cfg4()
+    model = pk.CovarianceModel(wl.sigma2, wl.alpha, wl.nu, wl.tau2)
+    t0 = time.perf_counter()
+    f = pk.fit(model, wl.obs, wl.z)
+    grid = pk.build_padded_grid(wl.domain, wl.dims, wl.L, wl.obs)
+    st = pk.build_setup(model, grid, wl.L, wl.obs)
+    from paper_2605_29284_b200.simulate import embedding_dims
+    emb = embedding_dims(model, st)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    seed = wl.extra["ens_seed"]
+    for _ in range(max(1, warmup)):
+        generate_ensemble_sharded(f, st, R, seed, batch=batch)
+    barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = N.launch_count()
+    ev0.record()
+    for _ in range(steps):
+        ens = generate_ensemble_sharded(f, st, R, seed, batch=batch)
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = N.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms, world)
+    barrier(world)
+    # e2e: public API, host outputs (mean / SE D2H) inside the timed region
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ens_h = generate_ensemble_sharded(f, st, R, seed, batch=batch, host=True)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
+    m1, m2 = grid.interior_dims
+    return {
+        "metric": "CS realizations/s", "value": round(R * steps / (ms * 1e-3), 2), "unit": "realizations/s",
+        "config": {"workload": "cfg4: n=5000, 512x512, L=3, nu=1.5, R=1024, seed 0",
+                   "cs_torus": list(emb[:2]), "doubled": bool(emb[2]), "batch": batch,
+                   "chunks": 8, "sharding": f"realization chunks over {world} rank(s), 1 all-gather"},
+        "ms_per_ensemble": round(ms / steps, 3), "ms_per_realization": round(ms / steps / R, 5),
+        "setup_s": round(t_setup, 3), "gpu_launches": int(launches),
+        "e2e": {"value": round(R * steps / (e2e_ms * 1e-3), 2), "unit": "realizations/s",
+                "h2d_bytes_per_step": 8, "d2h_bytes_per_step": 16 * m1 * m2},
+        "se_mean": float(np.mean(ens_h.empirical_se)),
+    }
+
+
+# ------------------------------------------------------------------ reference arm
+_W = {}
+
+
+def _ref_worker_init(cfg_name):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import rk_oracle as ro
+    from paper_2605_29284_b200 import workloads
+    wl = workloads.CONFIGS[cfg_name]()
+    model = ro.Model(wl.sigma2, wl.alpha, wl.nu, wl.tau2)
+    og = ro.make_grid(wl.domain, wl.dims, wl.L, wl.obs)
+    _W["st"] = ro.rapid_setup(model, og, wl.L, wl.obs)
+    _W["xg"] = workloads.grid_covariates_for(og.interior_nodes(), wl.grid_covariates)
+    rng = np.random.default_rng(7)
+    X = wl.X if wl.X is not None else np.ones((wl.obs.shape[0], 1))
+    _W["c"] = rng.normal(size=wl.obs.shape[0])
+    _W["beta"] = np.zeros(X.shape[1])
+    _W["ro"] = ro
+
+
+def _ref_predict(_):
+    ro = _W["ro"]
+    t0 = time.perf_counter()
+    ro.predict(_W["st"], _W["c"], _W["beta"], _W["xg"])
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    import multiprocessing as mp
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    from paper_2605_29284_b200 import workloads
+    wl = workloads.cfg2()
+    N = wl.dims[0] * wl.dims[1]
+    with ctx.Pool(cores, initializer=_ref_worker_init, initargs=("cfg2",)) as pool:
+        for _ in range(max(1, args.warmup)):
+            pool.map(_ref_predict, range(cores))
+        step_s = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_ref_predict, range(cores), chunksize=1)
+            step_s.append(time.perf_counter() - t0)
+    tot = sum(step_s)
+    value = N * cores * args.steps / tot
+    line = {
+        "impl": "reference", "metric": "predicted grid points/s (fp64)", "value": round(value, 1),
+        "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE configs[1] shapes)",
+        "config": {"workload": "cfg2: predict_rapid, n=1368 mixture obs, 350x350, L=3, nu=1.0, X_g=[1,x,y]"},
+        "cpu_baseline": {"value": round(value, 1), "unit": "points/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} steps x {cores} concurrent predicts (one process per core; "
+                                   "numpy/pocketfft oracle port of rapid.py:164-261)"},
+        "e2e": {"value": round(value, 1), "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg3 / CS extras")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    args.warmup = max(3, args.warmup)
+    rank, world, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2605_29284_b200 as pk
+    from paper_2605_29284_b200 import workloads
+    peaks, peaks_kind = _peaks()
+    flush = L2Flush()
+
+    wl = workloads.cfg2()
+    case = build_predict_case(pk, wl)
+    barrier(world)
+    with ClockSampler(local) as clk:
+        ms, launches, out = time_predict_device(pk, case, args.steps, args.warmup, flush)
+    tot_ms = max_over_ranks(sum(ms), world)
+    N = wl.dims[0] * wl.dims[1]
+    value = N * args.steps * world / (tot_ms * 1e-3)
+    pass_ms, pass_bytes = profile_passes(pk, case, 10, flush)
+    e2e_ms, h2d, d2h = time_predict_e2e(pk, case, args.steps, args.warmup, flush)
+    e2e_tot = max_over_ranks(sum(e2e_ms), world)
+    line = {
+        "metric": "predicted grid points/s (fp64)", "value": round(value, 1), "unit": "points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded; BASELINE configs[1] shapes: 3-comp mixture sd 0.15, exact GP z)",
+        "config": {"workload": "cfg2: predict_rapid, n=1368 mixture obs, 350x350, L=3, nu=1.0 (Bessel), X_g=[1,x,y]",
+                   "embed": list(case["setup"].embed_dims), "padded": list(case["setup"].grid.total_dims),
+                   "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}",
+                   "setup_s": round(case["t_setup"], 4), "fit_s": round(case["t_fit"], 4)},
+        "e2e": {"value": round(N * args.steps * world / (e2e_tot * 1e-3), 1), "unit": "points/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "roofline": roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind),
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        times, ref_field = cpu_baseline_predict(case, wl, seconds=args.cpu_seconds)
+        gpu_field = pk.predict_rapid(case["setup"], case["cs"][0], case["beta"], case["xg"])
+        cores = 1
+        line["cpu_baseline"] = {
+            "value": round(N / statistics.median(times), 1), "unit": "points/s", "cores": cores, "kind": "port",
+            "sample": f"{len(times)} predicts (median) of cfg2 with the numpy oracle port, single process "
+                      "(pocketfft is single-threaded)"}
+        line["parity"] = {"max_rel_vs_oracle": float(np.abs(gpu_field - ref_field).max() / np.abs(ref_field).max()),
+                          "tol": 1e-10}
+    if not args.no_extra:
+        extra = {}
+        # large-grid predict (configs[2]), replicas
+        wl3 = workloads.cfg3()
+        case3 = build_predict_case(pk, wl3, c_variants=2)
+        ms3, l3, _ = time_predict_device(pk, case3, max(5, args.steps // 5), 3, flush)
+        t3 = max_over_ranks(sum(ms3), world)
+        pm3, pb3 = profile_passes(pk, case3, 5, flush)
+        N3 = wl3.dims[0] * wl3.dims[1]
+        extra["predict_cfg3"] = {
+            "metric": "predicted grid points/s (fp64)", "value": round(N3 * len(ms3) * world / (t3 * 1e-3), 1),
+            "unit": "points/s", "ms_per_predict": round(t3 / len(ms3), 4),
+            "config": {"workload": "cfg3: n=20000, 2048x2048, L=4, nu=2.5", "embed": list(case3["setup"].embed_dims)},
+            "roofline": roofline_obj(case3, pm3, pb3, peaks, peaks_kind), "setup_s": round(case3["t_setup"], 3),
+            "fit_s": round(case3["t_fit"], 3)}
+        del case3
+        torch.cuda.empty_cache()
+        extra["cs_cfg4"] = bench_cs(pk, max(2, args.steps // 25), 1, rank, world)
+        line["extra"] = extra
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

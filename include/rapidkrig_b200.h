@@ -126,6 +126,16 @@ rk_status rk_predict_dev(const rk_setup* s, const double* c_dev, const double* b
 rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta, int32_t p,
                           const double* xg, double* out, void* stream);
 
+/* predict_rapid with per-pass CUDA-event timing on `stream` (benchmark support):
+ * ms_out[0..2] = pass 1 (gather + row FFT), pass 2 (column filter), pass 3
+ * (row IFFT + epilogue) durations in milliseconds; synchronises the stream. */
+rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const double* beta_dev,
+                             int32_t p, const double* xg_dev, double* out_dev, void* stream,
+                             float* ms_out);
+/* algorithmic bytes per pass of rk_predict_* for this setup:
+ * bytes_out[0..2] per pass, for p covariates (0 = no fixed part) */
+rk_status rk_predict_traffic(const rk_setup* s, int32_t p, double* bytes_out);
+
 /* ---- L2: exact fit / refit (exact.py:71-113) ---------------------------- */
 /* GPU fit: M = K + tau2 I (covariance.py:100-116), Cholesky with ridge retry
  * (exact.py:25-37), GLS (exact.py:59-68).  X_host (n, p) row-major or NULL. */

@@ -87,7 +87,8 @@ struct PredictBatch {
   const double* g = nullptr;      // CS: (batch, M2, M1) unconditional fields, or null
   double* out = nullptr;          // (batch, m2, m1): field, or e = interior(g) - field in CS mode
 };
-Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st);
+Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st,
+                     cudaEvent_t* ev = nullptr);
 
 // CS pieces (rk_sim.cu)
 Status ensure_embedding(rk_setup* s, cudaStream_t st);

@@ -378,7 +378,8 @@ static inline int64_t round_even(int64_t v) { return (v + 1) & ~int64_t(1); }
 // Shared 3-pass pipeline. src: SRC_GATHER (coefficients) or SRC_REAL (padded field).
 static Status conv_pipeline(const rk_setup* s, int src, const double* c, int64_t c_stride,
                             const double* real_in, int batch, int row0, int nout, int col0,
-                            int ncols, const RowInvArgs& epi, cudaStream_t st) {
+                            int ncols, const RowInvArgs& epi, cudaStream_t st,
+                            cudaEvent_t* ev = nullptr) {
   const int64_t ldT = round_even(s->M2);
   const int64_t ldU = round_even(nout);
   double2 *T = nullptr, *U = nullptr;
@@ -394,7 +395,9 @@ static Status conv_pipeline(const rk_setup* s, int src, const double* c, int64_t
   ra.T_bstride = (int64_t)s->H1 * ldT;
   ra.g = gather_src(s, c, c_stride);
   ra.real_in = real_in;
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[0], st));
   RK_TRY(launch_row_fwd(src, ra, batch, st));
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[1], st));
   ColArgs ca{};
   ca.pl = s->pl2;
   ca.lpc = pick_lpc(s->pl2, 4);
@@ -411,6 +414,7 @@ static Status conv_pipeline(const rk_setup* s, int src, const double* c, int64_t
   ca.ldU = ldU;
   ca.U_bstride = (int64_t)s->H1 * ldU;
   RK_TRY(launch_col(0, ca, batch, st));
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[2], st));
   RowInvArgs ia = epi;
   ia.pl = s->pl1;
   ia.lpc = pick_lpc(s->pl1, 4);
@@ -421,12 +425,13 @@ static Status conv_pipeline(const rk_setup* s, int src, const double* c, int64_t
   ia.col0 = col0;
   ia.ncols = ncols;
   RK_TRY(launch_row_inv(ia, batch, st));
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
   scratch_free(T, st);
   scratch_free(U, st);
   return Status::ok();
 }
 
-Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st) {
+Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st, cudaEvent_t* ev) {
   RowInvArgs e{};
   e.out = pb.out;
   e.ldo = s->m1;
@@ -441,7 +446,7 @@ Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st)
   e.g_row0 = s->grid.pad[2];
   e.g_col0 = s->grid.pad[0];
   return conv_pipeline(s, SRC_GATHER, pb.c, pb.c_stride, nullptr, pb.batch, s->grid.pad[2], s->m2,
-                       s->grid.pad[0], s->m1, e, st);
+                       s->grid.pad[0], s->m1, e, st, ev);
 }
 
 }  // namespace rk
@@ -526,6 +531,44 @@ rk_status rk_predict_dev(const rk_setup* s, const double* c_dev, const double* b
     return predict_batch(s, pb, (cudaStream_t)stream);
   };
   return (rk_status)finish_status(run());
+}
+
+rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const double* beta_dev,
+                             int32_t p, const double* xg_dev, double* out_dev, void* stream,
+                             float* ms_out) {
+  auto run = [&]() -> Status {
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaEvent_t ev[4];
+    for (int i = 0; i < 4; ++i) RK_CUDA_TRY(cudaEventCreate(&ev[i]));
+    PredictBatch pb;
+    pb.batch = 1;
+    pb.c = c_dev;
+    pb.c_stride = s->n;
+    pb.beta = beta_dev;
+    pb.p = p;
+    pb.xg = xg_dev;
+    pb.out = out_dev;
+    Status r = predict_batch(s, pb, st, ev);
+    if (r.good()) {
+      RK_CUDA_TRY(cudaEventSynchronize(ev[3]));
+      for (int i = 0; i < 3; ++i) RK_CUDA_TRY(cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]));
+    }
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+    return r;
+  };
+  return (rk_status)finish_status(run());
+}
+
+rk_status rk_predict_traffic(const rk_setup* s, int32_t p, double* b) {
+  // pass 1: weights (n M), sorted base/perm (8 n), c gathers (8 n), cell_start (4 (G + 1)),
+  //         T write (16 H1 M2); pass 2: T read, quarter spectrum (8 H1 Q2), U write (16 H1 m2);
+  // pass 3: U read, covariates (8 N p), field write (8 N)
+  const double n = (double)s->n, M = (double)s->M, G = (double)s->M1 * s->M2;
+  const double N = (double)s->m1 * s->m2, H = (double)s->H1;
+  b[0] = n * M * 8.0 + 16.0 * n + 4.0 * (G + 1.0) + 16.0 * H * s->M2;
+  b[1] = 16.0 * H * s->M2 + 8.0 * H * s->Q2 + 16.0 * H * s->m2;
+  b[2] = 16.0 * H * s->m2 + 8.0 * N * (double)p + 8.0 * N;
+  return RK_OK;
 }
 
 rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta, int32_t p,

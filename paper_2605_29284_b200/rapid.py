@@ -182,7 +182,10 @@ def _fixed_inputs(setup: RapidSetup, beta_hat, grid_covariates):
     """Validation of rapid.py:233-249; returns (beta f64 array | None, xg (N,p) | None)."""
     if beta_hat is None:
         return None, None
-    beta = D.host_f64(beta_hat.detach().cpu().numpy() if hasattr(beta_hat, "detach") else beta_hat).ravel()
+    if D.is_device_tensor(beta_hat):      # stays on the device: no host sync on the hot path
+        beta = beta_hat.reshape(-1)
+    else:
+        beta = D.host_f64(beta_hat).ravel()
     m1, m2 = setup.grid.interior_dims
     if grid_covariates is None:
         if beta.shape[0] != 1:
@@ -203,8 +206,11 @@ def _fixed_inputs(setup: RapidSetup, beta_hat, grid_covariates):
     return beta, xg
 
 
-def predict_rapid(setup: RapidSetup, c, beta_hat=None, grid_covariates=None):
-    """(m2, m1) interior field: FFT convolution of A'c with the covariance filter + X_g beta."""
+def predict_rapid(setup: RapidSetup, c, beta_hat=None, grid_covariates=None, *, out=None):
+    """(m2, m1) interior field: FFT convolution of A'c with the covariance filter + X_g beta.
+
+    ``out`` (optional) receives the result: a CUDA tensor on the device path, or a
+    host float64 array (e.g. a pinned buffer) on the host path."""
     m1, m2 = setup.grid.interior_dims
     beta, xg = _fixed_inputs(setup, beta_hat, grid_covariates)
     p = 0 if beta is None else beta.shape[0]
@@ -214,20 +220,22 @@ def predict_rapid(setup: RapidSetup, c, beta_hat=None, grid_covariates=None):
             cd = cd.to(dtype=D.torch().float64).contiguous()
         if cd.shape[0] != setup.n_obs:
             raise DomainError(f"coefficient vector has {cd.shape[0]} entries for {setup.n_obs} observations")
-        bd = None if beta is None else D.to_device(beta)
-        xd = None if xg is None else D.to_device(xg)
-        out = D.empty((m2, m1))
-        N.call("rk_predict_dev", setup.handle, N.ptr(cd), N.ptr(bd), p, N.ptr(xd), N.ptr(out),
+        bd = None if beta is None else (beta if D.is_device_tensor(beta) else D.to_device(beta))
+        xd = None if xg is None else (xg if D.is_device_tensor(xg) and xg.is_contiguous()
+                                      and xg.dtype == D.torch().float64 else D.to_device(xg))
+        res = D.empty((m2, m1)) if out is None else out
+        N.call("rk_predict_dev", setup.handle, N.ptr(cd), N.ptr(bd), p, N.ptr(xd), N.ptr(res),
                N.stream_ptr())
-        return out
+        return res
     ch = D.host_f64(c).ravel()
     if ch.shape[0] != setup.n_obs:
         raise DomainError(f"coefficient vector has {ch.shape[0]} entries for {setup.n_obs} observations")
-    xh = None if xg is None else (xg.detach().cpu().numpy() if hasattr(xg, "detach") else D.host_f64(xg))
-    out = np.empty((m2, m1))
-    N.call("rk_predict_host", setup.handle, N.ptr(ch), N.ptr(beta), p, N.ptr(xh), N.ptr(out),
+    bh = None if beta is None else (beta.cpu().numpy() if D.is_device_tensor(beta) else beta)
+    xh = None if xg is None else (xg.cpu().numpy() if D.is_device_tensor(xg) else D.host_f64(xg))
+    res = np.empty((m2, m1)) if out is None else out
+    N.call("rk_predict_host", setup.handle, N.ptr(ch), N.ptr(bh), p, N.ptr(xh), N.ptr(res),
            N.stream_ptr())
-    return out
+    return res
 
 
 class _GridSetupCache:
