@@ -198,15 +198,15 @@ def profile_passes(pk, case, reps, flush):
     p = int(bd.numel())
     m1, m2 = st.grid.interior_dims
     out = torch.empty((m2, m1), dtype=torch.float64, device="cuda")
-    acc = np.zeros(3)
+    acc = np.zeros(4)
     for r in range(reps + 1):
         flush()
-        ms = (C.c_float * 3)()
+        ms = (C.c_float * 4)()
         N.call("rk_predict_profile", st.handle, N.ptr(cd), N.ptr(bd), p, N.ptr(xd), N.ptr(out),
                N.stream_ptr(), C.byref(ms))
         if r:
             acc += np.array(list(ms))
-    b = (C.c_double * 3)()
+    b = (C.c_double * 4)()
     N.call("rk_predict_traffic", st.handle, p if xd is not None else 0, C.byref(b))
     return acc / reps, np.array(list(b))
 
@@ -242,9 +242,9 @@ def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind):
     H1 = p1 // 2 + 1
     m1, m2 = st.grid.interior_dims
     M1, M2 = st.grid.total_dims
-    flops = [ (M2 + 1) // 2 * fft_flops(p1), H1 * 2 * fft_flops(p2), (m2 + 1) // 2 * fft_flops(p1)]
+    flops = [0.0, (M2 + 1) // 2 * fft_flops(p1), H1 * 2 * fft_flops(p2), (m2 + 1) // 2 * fft_flops(p1)]
     dom = int(np.argmax(pass_ms))
-    names = ["pass1_gather_rowfft", "pass2_column_filter", "pass3_rowifft_epilogue"]
+    names = ["gather_cstar", "pass1_rowfft", "pass2_column_filter", "pass3_rowifft_epilogue"]
     ach = pass_bytes[dom] / (pass_ms[dom] * 1e-3) / 1e9
     peak = float(peaks.get("hbm_gbs", 6650.0))
     fl = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
@@ -255,7 +255,7 @@ def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind):
         "fp64_tflops": round(fl, 3), "fp64_peak_tflops": FP64_TFLOPS_MEASURED,
         "fp64_frac": round(fl / FP64_TFLOPS_MEASURED, 4),
         "passes": {names[i]: {"ms": round(float(pass_ms[i]), 5), "GB/s": round(pass_bytes[i] / (pass_ms[i] * 1e-3) / 1e9, 1),
-                              "fp64_TF/s": round(flops[i] / (pass_ms[i] * 1e-3) / 1e12, 3)} for i in range(3)},
+                              "fp64_TF/s": round(flops[i] / (pass_ms[i] * 1e-3) / 1e12, 3)} for i in range(4)},
     }
 
 

@@ -111,8 +111,8 @@ rk_status rk_coefficients_to_grid(const rk_setup* s, const double* c_dev, double
 rk_status rk_convolve_filter(const rk_setup* s, const double* values_dev, double* out_dev,
                              void* stream);
 /* convolve_filter (rapid.py:89-100) with a caller-supplied real-even spectrum in
- * quarter form spec_q[kx * (p2/2+1) + ky] = Re S[ky, kx] / (p1 p2), kx <= p1/2,
- * ky <= p2/2 (device); values/out (M2, M1) device. */
+ * quarter form spec_q[kx * ldq + ky] = Re S[ky, kx] / (p1 p2), kx <= p1/2, ky <= p2/2,
+ * ldq = p2/2+1 rounded up to even, 16-byte aligned (device); values/out (M2, M1) device. */
 rk_status rk_convolve_spectrum(const double* spec_q_dev, int32_t p1, int32_t p2,
                                const double* values_dev, int32_t M1, int32_t M2, double* out_dev,
                                void* stream);
@@ -126,14 +126,14 @@ rk_status rk_predict_dev(const rk_setup* s, const double* c_dev, const double* b
 rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta, int32_t p,
                           const double* xg, double* out, void* stream);
 
-/* predict_rapid with per-pass CUDA-event timing on `stream` (benchmark support):
- * ms_out[0..2] = pass 1 (gather + row FFT), pass 2 (column filter), pass 3
- * (row IFFT + epilogue) durations in milliseconds; synchronises the stream. */
+/* predict_rapid with per-kernel CUDA-event timing on `stream` (benchmark support):
+ * ms_out[0..3] = gather (c* = A'c), pass 1 (row FFT), pass 2 (column filter),
+ * pass 3 (row IFFT + epilogue) durations in milliseconds; synchronises the stream. */
 rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const double* beta_dev,
                              int32_t p, const double* xg_dev, double* out_dev, void* stream,
                              float* ms_out);
-/* algorithmic bytes per pass of rk_predict_* for this setup:
- * bytes_out[0..2] per pass, for p covariates (0 = no fixed part) */
+/* algorithmic bytes per kernel of rk_predict_* for this setup:
+ * bytes_out[0..3] as in rk_predict_profile, for p covariates (0 = no fixed part) */
 rk_status rk_predict_traffic(const rk_setup* s, int32_t p, double* bytes_out);
 
 /* ---- L2: exact fit / refit (exact.py:71-113) ---------------------------- */

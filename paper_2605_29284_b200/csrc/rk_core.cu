@@ -446,7 +446,8 @@ static void chol_inverse(const std::vector<double>& L, int M, std::vector<double
 }
 
 Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2, double scale,
-                        double* out_q, cudaStream_t st);  // rk_predict.cu
+                        double* out_q, int ldq, cudaStream_t st);  // rk_predict.cu
+int quarter_ld(int p2);                                             // rk_predict.cu
 
 static void free_setup(rk_setup* s) {
   if (!s) return;
@@ -634,12 +635,12 @@ spectrum:
   s->p1 = (int)next_fft_len(2 * (int64_t)s->M1 - 1);
   s->p2 = (int)next_fft_len(2 * (int64_t)s->M2 - 1);
   s->H1 = s->p1 / 2 + 1;
-  s->Q2 = s->p2 / 2 + 1;
+  s->Q2 = quarter_ld(s->p2);
   RK_TRY(plan_for(s->p1, &s->pl1));
   RK_TRY(plan_for(s->p2, &s->pl2));
   RK_CUDA_TRY(cudaMalloc(&s->spec_q, sizeof(double) * (size_t)s->H1 * s->Q2));
   RK_TRY(spectrum_quarter(s->mat, grid->hx, grid->hy, s->p1, s->p2,
-                          1.0 / ((double)s->p1 * (double)s->p2), s->spec_q, 0));
+                          1.0 / ((double)s->p1 * (double)s->p2), s->spec_q, s->Q2, 0));
   RK_CUDA_TRY(cudaDeviceSynchronize());
   *out = guard.release();
   return Status::ok();

@@ -1,16 +1,17 @@
 // rapidkrig B200: rapid predict = deterministic scatter + circulant FFT convolution.
 //
 // Reference mapping (/root/reference/pkg/src/rapidkrig/rapid.py):
-//   coefficients_to_grid 164-174 (np.add.at)  -> cstar_at(): per-node GATHER over the
-//       cell-sorted observations (fixed order, no atomics), fused into pass 1
+//   coefficients_to_grid 164-174 (np.add.at)  -> cstar_kernel: per-node GATHER over the
+//       cell-sorted observations (fixed order, no atomics), one thread per padded node
 //   convolve_filter 89-100 (fft2 * spectrum, ifft2, crop) -> 3 passes:
-//       pass 1 row_fwd_kernel : two real padded rows per complex FFT (length p1),
-//                               split into two half spectra, written transposed T[kx][y]
-//       pass 2 col_kernel     : column kx: FFT(p2) of the M2 nonzero rows, x real even
-//                               spectrum (quarter stored, 1/(p1 p2) folded in), IFFT,
-//                               keep only the m2 interior rows -> U[kx][y']
-//       pass 3 row_inv_kernel : Hermitian-combined pair of interior rows, IFFT(p1),
-//                               keep the m1 interior columns, fused epilogue
+//       pass 1 row_fwd_kernel : two real padded rows (TMA bulk-staged) per complex FFT of
+//                               length p1, split into two half spectra, written transposed
+//                               T[kx][y] (only the M2 nonzero rows exist)
+//       pass 2 col_kernel     : column kx (TMA bulk load) -> FFT(p2) -> x real-even spectrum
+//                               (quarter column prefetched by TMA during the FFT, 1/(p1 p2)
+//                               folded in) -> IFFT -> TMA bulk store of the m2 interior rows
+//       pass 3 row_inv_kernel : Hermitian-combined pair of interior rows, IFFT(p1), keep the
+//                               m1 interior columns, fused fixed-part / draw epilogue
 //   _fixed_part 233-249 / predict_rapid 252-261 -> epilogue of pass 3
 //   build_filter_spectrum 72-86 -> spectrum_quarter(): lag table on the quarter torus,
 //       pass 1 (lag mode) + pass 2 (spectrum mode, real part of ky <= p2/2)
@@ -33,40 +34,59 @@ struct GatherSrc {
 
 // c*[y, x] = sum over observations whose 2L x 2L block covers (y, x) of w * c,
 // visiting base rows by = y .. y-2L+1 and, inside each, the contiguous sorted
-// range of bases bx in [x-2L+1, x].
+// range of bases bx in [x-2L+1, x].  BS = 2L as a template (0 = runtime) so the
+// 2 x 2L cell-range loads are independent and issued together.
+template <int BS>
 __device__ __forceinline__ double cstar_at(const GatherSrc& g, const double* __restrict__ c, int y,
                                            int x) {
-  double acc = 0.0;
-  const int xlo = max(0, x - g.bs + 1);
-  const int xhi = min(x, g.M1 - g.bs);
+  const int bs = BS ? BS : g.bs;
+  const int xlo = max(0, x - bs + 1);
+  const int xhi = min(x, g.M1 - bs);
   if (xlo > xhi) return 0.0;
-  for (int dy = 0; dy < g.bs; ++dy) {
-    const int by = y - dy;
-    if (by < 0 || by > g.M2 - g.bs) continue;
-    const int rowb = by * g.M1;
-    const int j0 = __ldg(&g.cell_start[rowb + xlo]);
-    const int j1 = __ldg(&g.cell_start[rowb + xhi + 1]);
-    for (int j = j0; j < j1; ++j) {
-      const int bx = __ldg(&g.bsort[j]) - rowb;
-      const double w = __ldg(&g.wsort[(int64_t)j * g.M + dy * g.bs + (x - bx)]);
-      const double cj = __ldg(&c[__ldg(&g.perm[j])]);
-      acc = __dadd_rn(acc, __dmul_rn(w, cj));   // (w * c) then add, as np.add.at
+  double acc = 0.0;
+  constexpr int U = BS ? BS : 1;
+  for (int d0 = 0; d0 < bs; d0 += U) {
+    int j0[U], j1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int by = y - (d0 + u);
+      j0[u] = j1[u] = 0;
+      if (by >= 0 && by <= g.M2 - bs) {
+        j0[u] = __ldg(&g.cell_start[by * g.M1 + xlo]);
+        j1[u] = __ldg(&g.cell_start[by * g.M1 + xhi + 1]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int dy = d0 + u;
+      const int rowb = (y - dy) * g.M1;
+      for (int j = j0[u]; j < j1[u]; ++j) {
+        const int bx = __ldg(&g.bsort[j]) - rowb;
+        const double w = __ldg(&g.wsort[(int64_t)j * g.M + dy * bs + (x - bx)]);
+        const double cj = __ldg(&c[__ldg(&g.perm[j])]);
+        acc = __dadd_rn(acc, __dmul_rn(w, cj));   // (w * c) then add, as np.add.at
+      }
     }
   }
   return acc;
 }
 
-__global__ void cstar_kernel(GatherSrc g, double* __restrict__ out) {
+template <int BS>
+__global__ void __launch_bounds__(256) cstar_kernel(GatherSrc g, double* __restrict__ out, int64_t ldo,
+                                                    int64_t out_bstride) {
+  const int b = blockIdx.y;
+  const double* c = g.c + (int64_t)b * g.c_stride;
+  double* o = out + (int64_t)b * out_bstride;
   const int64_t tot = (int64_t)g.M1 * g.M2;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int y = (int)(e / g.M1), x = (int)(e % g.M1);
-    out[e] = cstar_at(g, g.c, y, x);
+    o[(int64_t)y * ldo + x] = cstar_at<BS>(g, c, y, x);
   }
 }
 
 // ----------------------------------------------------------------- pass 1
-enum RowSrc { SRC_GATHER = 0, SRC_REAL = 1, SRC_LAG = 2 };
+enum RowSrc { SRC_ROWS = 1, SRC_LAG = 2 };
 
 struct RowFwdArgs {
   FftPlan pl;
@@ -75,15 +95,16 @@ struct RowFwdArgs {
   int ncols;                 // nonzero input columns
   double2* T;                // (H, ldT) per batch
   int64_t ldT, T_bstride;
-  GatherSrc g;               // SRC_GATHER
-  const double* real_in;     // SRC_REAL: (nrows, ncols) row-major
+  const double* rows;        // SRC_ROWS: (nrows, ld_in) per batch
+  int64_t ld_in, in_bstride;
+  int tma;                   // SRC_ROWS: rows are 16-byte aligned -> TMA bulk staging
   const double* lagq;        // SRC_LAG: quarter lag table (p2/2+1, p1/2+1)
   int lag_ld, p2;
 };
 
 template <int SRC>
 __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
   const int line = threadIdx.x / nthr;
@@ -93,23 +114,52 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
   const int ya = 2 * (blockIdx.x * a.lpc + line);
   const int yb = ya + 1;
   const bool va = ya < a.nrows, vb = yb < a.nrows;
-  const double* cb = (SRC == SRC_GATHER) ? a.g.c + (int64_t)b * a.g.c_stride : nullptr;
-  for (int x = tl; x < n; x += nthr) {
-    double u = 0.0, v = 0.0;
-    if (x < a.ncols) {
-      if (SRC == SRC_GATHER) {
-        if (va) u = cstar_at(a.g, cb, ya, x);
-        if (vb) v = cstar_at(a.g, cb, yb, x);
-      } else if (SRC == SRC_REAL) {
-        if (va) u = a.real_in[(int64_t)ya * a.ncols + x];
-        if (vb) v = a.real_in[(int64_t)yb * a.ncols + x];
-      } else {
-        const int bx = min(x, n - x);
-        if (va) u = __ldg(&a.lagq[(int64_t)min(ya, a.p2 - ya) * a.lag_ld + bx]);
-        if (vb) v = __ldg(&a.lagq[(int64_t)min(yb, a.p2 - yb) * a.lag_ld + bx]);
+  if (SRC == SRC_ROWS) {
+    const double* rin = a.rows + (int64_t)b * a.in_bstride;
+    double* stage = (double*)(smem + (size_t)a.lpc * n);        // lpc x 2 x ld_in doubles
+    uint64_t* bar = (uint64_t*)(stage + (size_t)a.lpc * 2 * a.ld_in);
+    double* sa = stage + (size_t)line * 2 * a.ld_in;
+    double* sb = sa + a.ld_in;
+    if (a.tma) {
+      if (threadIdx.x == 0) mbar_init(bar, 1);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t cnt = 0;
+        for (int l = 0; l < a.lpc; ++l) {
+          const int r0 = 2 * (blockIdx.x * a.lpc + l);
+          cnt += (r0 < a.nrows ? 1u : 0u) + (r0 + 1 < a.nrows ? 1u : 0u);
+        }
+        mbar_expect_tx(bar, cnt * (uint32_t)(a.ld_in * 8));
+        for (int l = 0; l < a.lpc; ++l) {
+          const int r0 = 2 * (blockIdx.x * a.lpc + l);
+          double* d = stage + (size_t)l * 2 * a.ld_in;
+          if (r0 < a.nrows) bulk_g2s(d, rin + (int64_t)r0 * a.ld_in, (uint32_t)(a.ld_in * 8), bar);
+          if (r0 + 1 < a.nrows)
+            bulk_g2s(d + a.ld_in, rin + (int64_t)(r0 + 1) * a.ld_in, (uint32_t)(a.ld_in * 8), bar);
+        }
+      }
+      // zero padding beyond the nonzero columns while the copies fly
+      for (int x = a.ncols + tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
+      mbar_wait(bar, 0);
+      for (int x = tl; x < a.ncols; x += nthr)
+        buf[x] = make_double2(va ? sa[x] : 0.0, vb ? sb[x] : 0.0);
+    } else {
+      for (int x = tl; x < n; x += nthr) {
+        double u = 0.0, v = 0.0;
+        if (x < a.ncols) {
+          if (va) u = rin[(int64_t)ya * a.ld_in + x];
+          if (vb) v = rin[(int64_t)yb * a.ld_in + x];
+        }
+        buf[x] = make_double2(u, v);
       }
     }
-    buf[x] = make_double2(u, v);
+  } else {
+    for (int x = tl; x < n; x += nthr) {
+      const int bx = min(x, n - x);
+      const double u = va ? __ldg(&a.lagq[(int64_t)min(ya, a.p2 - ya) * a.lag_ld + bx]) : 0.0;
+      const double v = vb ? __ldg(&a.lagq[(int64_t)min(yb, a.p2 - yb) * a.lag_ld + bx]) : 0.0;
+      buf[x] = make_double2(u, v);
+    }
   }
   __syncthreads();
   fft_line<false>(buf, a.pl, tl);
@@ -140,18 +190,18 @@ struct ColArgs {
   int nin;                   // nonzero input rows
   const double2* T;
   int64_t ldT, T_bstride;
-  const double* spec_q;      // filter mode: (ncols, Q2)
-  int Q2;
+  const double* spec_q;      // filter mode: (ncols, ldq)
+  int ldq;                   // even, >= p2/2 + 1
   int row0, nout;            // filter mode: keep rows [row0, row0 + nout)
   double2* U;
   int64_t ldU, U_bstride;
-  double* out_q;             // spectrum mode: out_q[kx * Q2 + ky] = Re * scale
+  double* out_q;             // spectrum mode: out_q[kx * ldq + ky] = Re * scale, ky <= p2/2
   double scale;
 };
 
 template <int MODE>  // 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
 __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
   const int line = threadIdx.x / nthr;
@@ -160,25 +210,52 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
   const int kx = blockIdx.x * a.lpc + line;
   const bool valid = kx < a.ncols;
   double2* buf = smem + (size_t)line * n;
-  const double2* T = a.T + (int64_t)b * a.T_bstride + (int64_t)kx * a.ldT;
-  for (int y = tl; y < n; y += nthr)
-    buf[y] = (valid && y < a.nin) ? T[y] : make_double2(0.0, 0.0);
+  double* specs = (double*)(smem + (size_t)a.lpc * n);          // lpc x ldq (filter mode)
+  uint64_t* bar = (uint64_t*)(specs + (MODE == 0 ? (size_t)a.lpc * a.ldq : 0));
+  const double2* Tb = a.T + (int64_t)b * a.T_bstride;
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nv = 0;
+    for (int l = 0; l < a.lpc; ++l) nv += (blockIdx.x * a.lpc + l) < a.ncols;
+    const uint32_t colb = (uint32_t)a.nin * 16u;
+    const uint32_t specb = MODE == 0 ? (uint32_t)a.ldq * 8u : 0u;
+    mbar_expect_tx(bar, (uint32_t)nv * (colb + specb));
+    for (int l = 0; l < a.lpc; ++l) {
+      const int k = blockIdx.x * a.lpc + l;
+      if (k >= a.ncols) continue;
+      bulk_g2s(smem + (size_t)l * n, Tb + (int64_t)k * a.ldT, colb, bar);
+      if (MODE == 0) bulk_g2s(specs + (size_t)l * a.ldq, a.spec_q + (int64_t)k * a.ldq, specb, bar);
+    }
+  }
+  for (int y = a.nin + tl; y < n; y += nthr) buf[y] = make_double2(0.0, 0.0);
+  if (!valid)
+    for (int y = tl; y < a.nin; y += nthr) buf[y] = make_double2(0.0, 0.0);
+  mbar_wait(bar, 0);
   __syncthreads();
   fft_line<false>(buf, a.pl, tl);
   if (MODE == 0) {
-    if (valid) {
-      const double* S = a.spec_q + (int64_t)kx * a.Q2;
-      for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], __ldg(&S[min(ky, n - ky)]));
-    }
+    const double* S = specs + (size_t)line * a.ldq;
+    for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     __syncthreads();
     fft_line<true>(buf, a.pl, tl);
-    if (valid) {
-      double2* U = a.U + (int64_t)b * a.U_bstride + (int64_t)kx * a.ldU;
-      for (int y = tl; y < a.nout; y += nthr) U[y] = buf[a.row0 + y];
+    // TMA bulk store of the kept rows
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int l = 0; l < a.lpc; ++l) {
+        const int k = blockIdx.x * a.lpc + l;
+        if (k >= a.ncols) continue;
+        bulk_s2g(a.U + (int64_t)b * a.U_bstride + (int64_t)k * a.ldU, smem + (size_t)l * n + a.row0,
+                 (uint32_t)a.nout * 16u);
+      }
+      bulk_commit();
+      bulk_wait_read0();
     }
+    __syncthreads();
   } else {
     if (valid)
-      for (int ky = tl; ky < a.Q2; ky += nthr) a.out_q[(int64_t)kx * a.Q2 + ky] = buf[ky].x * a.scale;
+      for (int ky = tl; ky <= n / 2; ky += nthr) a.out_q[(int64_t)kx * a.ldq + ky] = buf[ky].x * a.scale;
   }
 }
 
@@ -202,7 +279,7 @@ struct RowInvArgs {
 };
 
 __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
   const int line = threadIdx.x / nthr;
@@ -210,15 +287,34 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   const int b = blockIdx.y;
   const int H = n / 2 + 1;
   const double2* U = a.U + (int64_t)b * a.U_bstride;
-  // coalesced load of both rows of every line: Z[k] = A[k] + i B[k], Hermitian upper half
-  for (int idx = threadIdx.x; idx < a.lpc * H; idx += blockDim.x) {
-    const int l = idx % a.lpc, k = idx / a.lpc;
-    const int ya = 2 * (blockIdx.x * a.lpc + l);
-    const double2 A = ya < a.nrows ? U[(int64_t)k * a.ldU + ya] : make_double2(0.0, 0.0);
-    const double2 B = ya + 1 < a.nrows ? U[(int64_t)k * a.ldU + ya + 1] : make_double2(0.0, 0.0);
-    double2* bl = smem + (size_t)l * n;
-    bl[k] = make_double2(A.x - B.y, A.y + B.x);
-    if (k >= 1 && k <= n - H) bl[n - k] = make_double2(A.x + B.y, B.x - A.y);
+  // strided gather of both rows of every line (Z[k] = A[k] + i B[k], Hermitian upper half),
+  // batched 4 deep per thread for memory-level parallelism
+  const int tot = a.lpc * H;
+  constexpr int D = 4;
+  for (int base = threadIdx.x; base < tot; base += D * blockDim.x) {
+    double2 A[D], B[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int idx = base + d * blockDim.x;
+      A[d] = B[d] = make_double2(0.0, 0.0);
+      if (idx < tot) {
+        const int l = idx % a.lpc, k = idx / a.lpc;
+        const int ya = 2 * (blockIdx.x * a.lpc + l);
+        const double2* u = U + (int64_t)k * a.ldU + ya;
+        if (ya < a.nrows) A[d] = u[0];
+        if (ya + 1 < a.nrows) B[d] = u[1];
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int idx = base + d * blockDim.x;
+      if (idx < tot) {
+        const int l = idx % a.lpc, k = idx / a.lpc;
+        double2* bl = smem + (size_t)l * n;
+        bl[k] = make_double2(A[d].x - B[d].y, A[d].y + B[d].x);
+        if (k >= 1 && k <= n - H) bl[n - k] = make_double2(A[d].x + B[d].y, B[d].x - A[d].y);
+      }
+    }
   }
   __syncthreads();
   double2* buf = smem + (size_t)line * n;
@@ -248,18 +344,15 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
 }
 
 // ----------------------------------------------------------------- launches
-static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStream_t st) {
-  RowFwdArgs a = a0;
+static Status launch_row_fwd(int src, const RowFwdArgs& a, int batch, cudaStream_t st) {
   const int pairs = (a.nrows + 1) / 2;
   const dim3 grid((unsigned)ceil_div(pairs, a.lpc), (unsigned)batch);
-  const size_t smem = sizeof(double2) * a.pl.n * a.lpc;
+  size_t smem = sizeof(double2) * a.pl.n * a.lpc;
   const int threads = a.lpc * a.pl.nthr;
-  if (src == SRC_GATHER) {
-    RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_GATHER>, smem));
-    row_fwd_kernel<SRC_GATHER><<<grid, threads, smem, st>>>(a);
-  } else if (src == SRC_REAL) {
-    RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_REAL>, smem));
-    row_fwd_kernel<SRC_REAL><<<grid, threads, smem, st>>>(a);
+  if (src == SRC_ROWS) {
+    smem += (size_t)a.lpc * 2 * a.ld_in * sizeof(double) + 16;
+    RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_ROWS>, smem));
+    row_fwd_kernel<SRC_ROWS><<<grid, threads, smem, st>>>(a);
   } else {
     RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_LAG>, smem));
     row_fwd_kernel<SRC_LAG><<<grid, threads, smem, st>>>(a);
@@ -271,9 +364,10 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStrea
 
 static Status launch_col(int mode, const ColArgs& a, int batch, cudaStream_t st) {
   const dim3 grid((unsigned)ceil_div(a.ncols, a.lpc), (unsigned)batch);
-  const size_t smem = sizeof(double2) * a.pl.n * a.lpc;
+  size_t smem = sizeof(double2) * a.pl.n * a.lpc + 16;
   const int threads = a.lpc * a.pl.nthr;
   if (mode == 0) {
+    smem += sizeof(double) * (size_t)a.lpc * a.ldq;
     RK_TRY(set_smem_attr((const void*)col_kernel<0>, smem));
     col_kernel<0><<<grid, threads, smem, st>>>(a);
   } else {
@@ -307,9 +401,11 @@ __global__ void lagq_kernel(MaternDev P, double hx, double hy, int H1, int Q2, d
   }
 }
 
-// Re(fft2(lag filter))[ky, kx] * scale for kx <= p1/2, ky <= p2/2, stored out_q[kx * Q2 + ky]
+int quarter_ld(int p2) { return ((p2 / 2 + 1) + 1) & ~1; }
+
+// Re(fft2(lag filter))[ky, kx] * scale for kx <= p1/2, ky <= p2/2, stored out_q[kx * ldq + ky]
 Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2, double scale,
-                        double* out_q, cudaStream_t st) {
+                        double* out_q, int ldq, cudaStream_t st) {
   FftPlan pl1, pl2;
   RK_TRY(plan_for(p1, &pl1));
   RK_TRY(plan_for(p2, &pl2));
@@ -321,6 +417,7 @@ Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2
   RK_TRY(scratch_alloc((void**)&T, sizeof(double2) * (size_t)H1 * p2, st));
   RK_TRY(scratch_alloc((void**)&bad, sizeof(int), st));
   RK_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  RK_CUDA_TRY(cudaMemsetAsync(out_q, 0, sizeof(double) * (size_t)H1 * ldq, st));
   lagq_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)H1 * Q2, 256), 148 * 64), 256, 0, st>>>(
       P, hx, hy, H1, Q2, lagq, bad);
   count_launch();
@@ -344,7 +441,7 @@ Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2
   ca.nin = p2;
   ca.T = T;
   ca.ldT = p2;
-  ca.Q2 = Q2;
+  ca.ldq = ldq;
   ca.out_q = out_q;
   ca.scale = scale;
   RK_TRY(launch_col(1, ca, 1, st));
@@ -373,13 +470,31 @@ static GatherSrc gather_src(const rk_setup* s, const double* c, int64_t c_stride
   return g;
 }
 
+static Status launch_cstar(const rk_setup* s, const double* c, int64_t c_stride, double* out,
+                           int64_t ldo, int batch, cudaStream_t st) {
+  const GatherSrc g = gather_src(s, c, c_stride);
+  const int64_t tot = (int64_t)s->M1 * s->M2;
+  const dim3 grid((unsigned)std::min<int64_t>(ceil_div(tot, 256), 148 * 16), (unsigned)batch);
+  const int64_t bstr = ldo * s->M2;
+  switch (s->bs) {
+    case 2: cstar_kernel<2><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
+    case 4: cstar_kernel<4><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
+    case 6: cstar_kernel<6><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
+    case 8: cstar_kernel<8><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
+    default: cstar_kernel<0><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
+  }
+  count_launch();
+  RK_LAUNCH_CHECK();
+  return Status::ok();
+}
+
 static inline int64_t round_even(int64_t v) { return (v + 1) & ~int64_t(1); }
 
-// Shared 3-pass pipeline. src: SRC_GATHER (coefficients) or SRC_REAL (padded field).
-static Status conv_pipeline(const rk_setup* s, int src, const double* c, int64_t c_stride,
-                            const double* real_in, int batch, int row0, int nout, int col0,
-                            int ncols, const RowInvArgs& epi, cudaStream_t st,
-                            cudaEvent_t* ev = nullptr) {
+// Shared 3-pass convolution. `rows` (nrows = M2, ld_in) holds the padded real input
+// (c* or a caller field); output rows [row0, row0 + nout) x cols [col0, col0 + ncols).
+static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in, int64_t in_bstride,
+                            int batch, int row0, int nout, int col0, int ncols, const RowInvArgs& epi,
+                            cudaStream_t st, cudaEvent_t* ev = nullptr) {
   const int64_t ldT = round_even(s->M2);
   const int64_t ldU = round_even(nout);
   double2 *T = nullptr, *U = nullptr;
@@ -393,11 +508,14 @@ static Status conv_pipeline(const rk_setup* s, int src, const double* c, int64_t
   ra.T = T;
   ra.ldT = ldT;
   ra.T_bstride = (int64_t)s->H1 * ldT;
-  ra.g = gather_src(s, c, c_stride);
-  ra.real_in = real_in;
-  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[0], st));
-  RK_TRY(launch_row_fwd(src, ra, batch, st));
+  ra.rows = rows;
+  ra.ld_in = ld_in;
+  ra.in_bstride = in_bstride;
+  ra.tma = ((ld_in * 8) % 16 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0) &&
+           ((in_bstride * 8) % 16 == 0);
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[1], st));
+  RK_TRY(launch_row_fwd(SRC_ROWS, ra, batch, st));
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[2], st));
   ColArgs ca{};
   ca.pl = s->pl2;
   ca.lpc = pick_lpc(s->pl2, 4);
@@ -407,14 +525,14 @@ static Status conv_pipeline(const rk_setup* s, int src, const double* c, int64_t
   ca.ldT = ldT;
   ca.T_bstride = ra.T_bstride;
   ca.spec_q = s->spec_q;
-  ca.Q2 = s->Q2;
+  ca.ldq = s->Q2;
   ca.row0 = row0;
   ca.nout = nout;
   ca.U = U;
   ca.ldU = ldU;
   ca.U_bstride = (int64_t)s->H1 * ldU;
   RK_TRY(launch_col(0, ca, batch, st));
-  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[2], st));
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
   RowInvArgs ia = epi;
   ia.pl = s->pl1;
   ia.lpc = pick_lpc(s->pl1, 4);
@@ -425,7 +543,7 @@ static Status conv_pipeline(const rk_setup* s, int src, const double* c, int64_t
   ia.col0 = col0;
   ia.ncols = ncols;
   RK_TRY(launch_row_inv(ia, batch, st));
-  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[4], st));
   scratch_free(T, st);
   scratch_free(U, st);
   return Status::ok();
@@ -445,8 +563,15 @@ Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st,
   e.g_ld = s->M1;
   e.g_row0 = s->grid.pad[2];
   e.g_col0 = s->grid.pad[0];
-  return conv_pipeline(s, SRC_GATHER, pb.c, pb.c_stride, nullptr, pb.batch, s->grid.pad[2], s->m2,
-                       s->grid.pad[0], s->m1, e, st, ev);
+  const int64_t ldc = round_even(s->M1);
+  double* cstar = nullptr;
+  RK_TRY(scratch_alloc((void**)&cstar, sizeof(double) * (size_t)ldc * s->M2 * pb.batch, st));
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[0], st));
+  RK_TRY(launch_cstar(s, pb.c, pb.c_stride, cstar, ldc, pb.batch, st));
+  Status r = conv_pipeline(s, cstar, ldc, ldc * s->M2, pb.batch, s->grid.pad[2], s->m2,
+                           s->grid.pad[0], s->m1, e, st, ev);
+  scratch_free(cstar, st);
+  return r;
 }
 
 }  // namespace rk
@@ -462,16 +587,7 @@ extern "C" {
 
 rk_status rk_coefficients_to_grid(const rk_setup* s, const double* c_dev, double* cstar_dev,
                                   void* stream) {
-  auto run = [&]() -> Status {
-    GatherSrc g = gather_src(s, c_dev, 0);
-    const int64_t tot = (int64_t)s->M1 * s->M2;
-    cstar_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 148 * 16), 256, 0,
-                   (cudaStream_t)stream>>>(g, cstar_dev);
-    count_launch();
-    RK_LAUNCH_CHECK();
-    return Status::ok();
-  };
-  return (rk_status)finish_status(run());
+  return (rk_status)finish_status(launch_cstar(s, c_dev, 0, cstar_dev, s->M1, 1, (cudaStream_t)stream));
 }
 
 rk_status rk_convolve_filter(const rk_setup* s, const double* values_dev, double* out_dev,
@@ -481,8 +597,7 @@ rk_status rk_convolve_filter(const rk_setup* s, const double* values_dev, double
     e.out = out_dev;
     e.ldo = s->M1;
     e.epi = EPI_PLAIN;
-    return conv_pipeline(s, SRC_REAL, nullptr, 0, values_dev, 1, 0, s->M2, 0, s->M1, e,
-                         (cudaStream_t)stream);
+    return conv_pipeline(s, values_dev, s->M1, 0, 1, 0, s->M2, 0, s->M1, e, (cudaStream_t)stream);
   };
   return (rk_status)finish_status(run());
 }
@@ -493,13 +608,15 @@ rk_status rk_convolve_spectrum(const double* spec_q_dev, int32_t p1, int32_t p2,
   auto run = [&]() -> Status {
     if (p1 < 2 * M1 - 2 || p2 < 2 * M2 - 2)
       return Status::err(RK_DOMAIN, "embedding dims too small for the padded grid");
+    if (reinterpret_cast<uintptr_t>(spec_q_dev) & 15)
+      return Status::err(RK_DOMAIN, "quarter spectrum must be 16-byte aligned");
     rk_setup t;   // descriptor only: the pipeline reads plans, dims and the spectrum
     t.M1 = M1;
     t.M2 = M2;
     t.p1 = p1;
     t.p2 = p2;
     t.H1 = p1 / 2 + 1;
-    t.Q2 = p2 / 2 + 1;
+    t.Q2 = quarter_ld(p2);
     t.spec_q = const_cast<double*>(spec_q_dev);
     RK_TRY(plan_for(p1, &t.pl1));
     RK_TRY(plan_for(p2, &t.pl2));
@@ -507,8 +624,7 @@ rk_status rk_convolve_spectrum(const double* spec_q_dev, int32_t p1, int32_t p2,
     e.out = out_dev;
     e.ldo = M1;
     e.epi = EPI_PLAIN;
-    Status st = conv_pipeline(&t, SRC_REAL, nullptr, 0, values_dev, 1, 0, M2, 0, M1, e,
-                              (cudaStream_t)stream);
+    Status st = conv_pipeline(&t, values_dev, M1, 0, 1, 0, M2, 0, M1, e, (cudaStream_t)stream);
     t.spec_q = nullptr;
     return st;
   };
@@ -538,8 +654,8 @@ rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const doubl
                              float* ms_out) {
   auto run = [&]() -> Status {
     cudaStream_t st = (cudaStream_t)stream;
-    cudaEvent_t ev[4];
-    for (int i = 0; i < 4; ++i) RK_CUDA_TRY(cudaEventCreate(&ev[i]));
+    cudaEvent_t ev[5];
+    for (int i = 0; i < 5; ++i) RK_CUDA_TRY(cudaEventCreate(&ev[i]));
     PredictBatch pb;
     pb.batch = 1;
     pb.c = c_dev;
@@ -550,24 +666,25 @@ rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const doubl
     pb.out = out_dev;
     Status r = predict_batch(s, pb, st, ev);
     if (r.good()) {
-      RK_CUDA_TRY(cudaEventSynchronize(ev[3]));
-      for (int i = 0; i < 3; ++i) RK_CUDA_TRY(cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]));
+      RK_CUDA_TRY(cudaEventSynchronize(ev[4]));
+      for (int i = 0; i < 4; ++i) RK_CUDA_TRY(cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]));
     }
-    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+    for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
     return r;
   };
   return (rk_status)finish_status(run());
 }
 
 rk_status rk_predict_traffic(const rk_setup* s, int32_t p, double* b) {
-  // pass 1: weights (n M), sorted base/perm (8 n), c gathers (8 n), cell_start (4 (G + 1)),
-  //         T write (16 H1 M2); pass 2: T read, quarter spectrum (8 H1 Q2), U write (16 H1 m2);
-  // pass 3: U read, covariates (8 N p), field write (8 N)
+  // gather: weights (n M), sorted base/perm (8 n), c (8 n), cell_start (4 (G + 1)), c* write (8 G)
+  // pass 1: c* read (8 G), T write (16 H1 M2); pass 2: T read, quarter spectrum (8 H1 (p2/2+1)),
+  // U write (16 H1 m2); pass 3: U read, covariates (8 N p), field write (8 N)
   const double n = (double)s->n, M = (double)s->M, G = (double)s->M1 * s->M2;
   const double N = (double)s->m1 * s->m2, H = (double)s->H1;
-  b[0] = n * M * 8.0 + 16.0 * n + 4.0 * (G + 1.0) + 16.0 * H * s->M2;
-  b[1] = 16.0 * H * s->M2 + 8.0 * H * s->Q2 + 16.0 * H * s->m2;
-  b[2] = 16.0 * H * s->m2 + 8.0 * N * (double)p + 8.0 * N;
+  b[0] = n * M * 8.0 + 16.0 * n + 4.0 * (G + 1.0) + 8.0 * G;
+  b[1] = 8.0 * G + 16.0 * H * s->M2;
+  b[2] = 16.0 * H * s->M2 + 8.0 * H * (s->p2 / 2 + 1) + 16.0 * H * s->m2;
+  b[3] = 16.0 * H * s->m2 + 8.0 * N * (double)p + 8.0 * N;
   return RK_OK;
 }
 
@@ -578,17 +695,18 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
     if (beta && !xg && p != 1)
       return Status::err(RK_DOMAIN, "grid covariates are required when beta_hat has more than one entry");
     const int64_t N = (int64_t)s->m1 * s->m2;
-    const size_t bc = sizeof(double) * s->n, bb = beta ? sizeof(double) * p : 0,
-                 bx = xg ? sizeof(double) * N * p : 0, bo = sizeof(double) * N;
+    auto up16 = [](size_t v) { return (v + 15) & ~size_t(15); };
+    const size_t bc = up16(sizeof(double) * s->n), bb = beta ? up16(sizeof(double) * p) : 0,
+                 bx = xg ? up16(sizeof(double) * N * p) : 0, bo = sizeof(double) * N;
     char* ws = nullptr;
     RK_TRY(scratch_alloc((void**)&ws, bc + bb + bx + bo + 64, st));
     double* dc = (double*)ws;
     double* db = beta ? (double*)(ws + bc) : nullptr;
     double* dx = xg ? (double*)(ws + bc + bb) : nullptr;
     double* dout = (double*)(ws + bc + bb + bx);
-    RK_CUDA_TRY(cudaMemcpyAsync(dc, c, bc, cudaMemcpyHostToDevice, st));
-    if (beta) RK_CUDA_TRY(cudaMemcpyAsync(db, beta, bb, cudaMemcpyHostToDevice, st));
-    if (xg) RK_CUDA_TRY(cudaMemcpyAsync(dx, xg, bx, cudaMemcpyHostToDevice, st));
+    RK_CUDA_TRY(cudaMemcpyAsync(dc, c, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
+    if (beta) RK_CUDA_TRY(cudaMemcpyAsync(db, beta, sizeof(double) * p, cudaMemcpyHostToDevice, st));
+    if (xg) RK_CUDA_TRY(cudaMemcpyAsync(dx, xg, sizeof(double) * N * p, cudaMemcpyHostToDevice, st));
     PredictBatch pb;
     pb.batch = 1;
     pb.c = dc;

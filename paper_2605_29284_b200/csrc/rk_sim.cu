@@ -245,7 +245,7 @@ __global__ void root_q_kernel(const double* __restrict__ lam_q, int hs1, int qs2
 }
 
 Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2, double scale,
-                        double* out_q, cudaStream_t st);
+                        double* out_q, int ldq, cudaStream_t st);
 
 static int64_t next_fft_len(int64_t m) {
   if (m <= 1) return 1;
@@ -266,7 +266,7 @@ Status ensure_embedding(rk_setup* s, cudaStream_t st) {
     const int hs1 = (int)(p1 / 2 + 1), qs2 = (int)(p2 / 2 + 1);
     double* lam = nullptr;
     RK_CUDA_TRY(cudaMalloc(&lam, sizeof(double) * (size_t)hs1 * qs2));
-    Status sp = spectrum_quarter(s->mat, s->grid.hx, s->grid.hy, (int)p1, (int)p2, 1.0, lam, st);
+    Status sp = spectrum_quarter(s->mat, s->grid.hx, s->grid.hy, (int)p1, (int)p2, 1.0, lam, qs2, st);
     if (!sp.good()) { cudaFree(lam); return sp; }
     std::vector<double> h((size_t)hs1 * qs2);
     RK_CUDA_TRY(cudaMemcpy(h.data(), lam, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));

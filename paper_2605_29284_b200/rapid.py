@@ -296,8 +296,10 @@ def _quarter_from_full(spec, p1, p2):
     if s.shape != (p2, p1):
         raise DomainError(f"spectrum shape {s.shape} does not match embed dims {(p2, p1)}")
     re = np.real(s)
-    q = re[: p2 // 2 + 1, : p1 // 2 + 1].T / (float(p1) * float(p2))
-    return D.to_device(np.ascontiguousarray(q))
+    ldq = ((p2 // 2 + 1) + 1) & ~1
+    q = np.zeros((p1 // 2 + 1, ldq))
+    q[:, : p2 // 2 + 1] = re[: p2 // 2 + 1, : p1 // 2 + 1].T / (float(p1) * float(p2))
+    return D.to_device(q)
 
 
 def neighbor_cov(model: CovarianceModel, grid: PaddedGrid, L: int):
