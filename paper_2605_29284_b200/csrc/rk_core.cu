@@ -42,38 +42,6 @@ static int finish(const Status& s) {
 }
 
 // ------------------------------------------------------------------- plans
-bool fft_factor(int n, FftPlan* pl) {
-  int a = 0, b = 0, m = n;
-  if (n < 1) return false;
-  while (m % 2 == 0) { m /= 2; ++a; }
-  while (m % 3 == 0) { m /= 3; ++b; }
-  if (m != 1) return false;
-  std::vector<int> r;
-  pl->n9 = b / 2;
-  b -= 2 * pl->n9;
-  pl->r3 = 1;
-  if (b == 1) {
-    if (a >= 1) { pl->r3 = 6; a -= 1; } else { pl->r3 = 3; }
-  }
-  pl->n8 = a / 3;
-  a -= 3 * pl->n8;
-  pl->r2 = a == 2 ? 4 : a == 1 ? 2 : 1;
-  for (int i = 0; i < pl->n9; ++i) r.push_back(9);
-  if (pl->r3 > 1) r.push_back(pl->r3);
-  for (int i = 0; i < pl->n8; ++i) r.push_back(8);
-  if (pl->r2 > 1) r.push_back(pl->r2);
-  pl->n = n;
-  pl->nstages = (int)r.size();
-  int need = 1;
-  for (size_t i = 0; i < r.size(); ++i) {
-    const int nb = n / r[i];
-    const int k = fft_kmax(r[i]);
-    need = std::max(need, (nb + k - 1) / k);
-  }
-  pl->nthr = std::max(32, (need + 31) / 32 * 32);
-  return true;
-}
-
 namespace {
 std::mutex g_plan_mu;
 std::map<std::pair<int, int>, FftPlan> g_plans;
@@ -95,15 +63,12 @@ Status plan_for(int n, FftPlan* out) {
     return Status::err(RK_INTERNAL, "FFT length " + std::to_string(n) + " is not 2^a 3^b");
   if (pl.nthr > 512)
     return Status::err(RK_DOMAIN, "FFT length " + std::to_string(n) + " too large for one CTA");
-  std::vector<double2> tw(n);
-  const long double PI_L = 3.141592653589793238462643383279502884L;
-  for (int t = 0; t < n; ++t) {
-    const long double ang = 2.0L * PI_L * (long double)t / (long double)n;
-    tw[t] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
-  }
+  std::vector<double2> tw;
+  fft_stage_twiddles(pl, tw, [](double c, double s) { return make_double2(c, s); });
+  tw.push_back(make_double2(1.0, 0.0));   // never empty
   double2* d = nullptr;
-  RK_CUDA_TRY(cudaMalloc(&d, sizeof(double2) * n));
-  RK_CUDA_TRY(cudaMemcpy(d, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+  RK_CUDA_TRY(cudaMalloc(&d, sizeof(double2) * tw.size()));
+  RK_CUDA_TRY(cudaMemcpy(d, tw.data(), sizeof(double2) * tw.size(), cudaMemcpyHostToDevice));
   pl.tw = d;
   g_plans[key] = pl;
   *out = pl;

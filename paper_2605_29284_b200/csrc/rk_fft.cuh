@@ -3,37 +3,45 @@
 // One "line" (a length-n transform) lives in shared memory as double2[n] and is
 // transformed in place by `nthr` threads.  Each stage with radix R reads the R
 // inputs x[j + k*n/R] of every butterfly j into registers, applies the twiddles
-// W_{Ns R}^{(j mod Ns) k} from a global root table (L1-resident), runs a
-// hand-written DFT_R codelet, then — after one barrier — scatters the outputs
-// to y[(j - j mod Ns) R + j mod Ns + k Ns] (autosort, natural order at the end).
-// Radices containing 3 are scheduled first so the small-Ns stages write with
-// odd strides (bank-conflict free for 16-byte elements).
+// W_{Ns R}^{(j mod Ns) k} (per-stage tables laid out [k-1][j mod Ns], so warp loads
+// are coalesced), runs a register DFT_R codelet, then — after one barrier —
+// scatters the outputs to y[(j - j mod Ns) R + j mod Ns + k Ns] (autosort).
 //
-// Several lines can share a CTA: every thread calls every stage (barriers are
-// CTA wide); threads whose butterfly index runs past n/R just idle.
+// Throughput note (measured, tools/fft_bench.cu + ncu): an fp64 complex element is 16
+// bytes and every stage moves it through shared memory twice, so a radix-9 stage does
+// only ~0.55 flop per smem byte while an SM balances 128 B/clk of smem against 128
+// flop/clk of FP64 -- the engine is shared-memory-bandwidth bound.  Larger radices
+// (composite P x Q codelets, DftPQ below) cut smem round trips, but every schedule that
+// mixes several large-radix arms in one kernel made ptxas spill; the shipped schedule is
+// 9^a * {3,6} * 8^b * {2,4}.  Radix-3 family first, so the first (Ns = 1) stage writes
+// with an odd stride (bank-conflict free for 16-byte elements).
+//
+// Several lines can share a CTA: every thread calls every stage (barriers are CTA
+// wide); threads whose butterfly index runs past n/R just idle.
 #pragma once
 
 #include "rk_common.cuh"
+#include "rk_fft_consts.cuh"
 
 namespace rk {
 
 constexpr int FFT_MAX_STAGES = 16;
 
-// n = 9^n9 * r3 * 8^n8 * r2 with r3 in {1, 3, 6} and r2 in {1, 2, 4}; stages run in that
-// order (radix-3 family first).  The schedule is kept as counts, not a radix array, so the
-// stage code below is straight-line per radix: a runtime switch inside one loop makes ptxas
-// keep every arm's registers live at once and spill.
+// n = 9^n9 * r3 * 8^n8 * r2.  Kept as counts (not a radix array) so the stage
+// code is straight-line per radix with only small runtime arms: a switch over many
+// large-radix arms (or any switch inside the stage loop) makes ptxas keep every
+// arm's registers live at once and spill.
 struct FftPlan {
   int n;                       // transform length
   int nstages;
   int nthr;                    // threads cooperating on one line (multiple of 32)
-  int n9, r3, n8, r2;
-  const double2* tw;           // device table W[t] = exp(-2 pi i t / n), t in [0, n)
+  int n9, r3, n8, r2;          // r3 in {1,3,6}, r2 in {1,2,4}
+  const double2* tw;           // per-stage twiddles, see fft_stage_twiddles()
 };
 
 // butterflies each thread keeps in registers for a stage of radix R
 __host__ __device__ constexpr int fft_kmax(int r) {
-  return r == 2 ? 9 : r == 3 ? 6 : r == 4 ? 4 : r == 6 ? 3 : r == 8 ? 2 : r == 9 ? 2 : 1;
+  return r == 2 ? 9 : r == 3 ? 6 : r == 4 ? 4 : r == 6 ? 3 : r == 8 ? 2 : r == 9 ? 2 : r == 12 ? 2 : 1;
 }
 
 // ----------------------------------------------------------------- codelets
@@ -120,18 +128,15 @@ template <bool INV>
 struct Dft<6, INV> {
   static __device__ __forceinline__ void run(double2* a) {
     const double S3 = 8.66025403784438596588e-01;
-    // inner DFT2 over j (stride 3): pairs (a_r, a_{r+3}), r = 0,1,2
     double2 u00 = a[0], u01 = a[3];
     double2 u10 = a[1], u11 = a[4];
     double2 u20 = a[2], u21 = a[5];
     dft2<INV>(u00, u01);
     dft2<INV>(u10, u11);
     dft2<INV>(u20, u21);
-    // twiddle u_{r,k1} *= w6^{r k1}: only k1 = 1 nontrivial
     const double sg = INV ? S3 : -S3;
     u11 = cmul(u11, make_double2(0.5, sg));
     u21 = cmul(u21, make_double2(-0.5, sg));
-    // outer DFT3 over r for each k1 -> y[k1 + 2 k2]
     dft3<INV>(u00, u10, u20);
     dft3<INV>(u01, u11, u21);
     a[0] = u00; a[2] = u10; a[4] = u20;
@@ -169,13 +174,65 @@ struct Dft<9, INV> {
   }
 };
 
-// ----------------------------------------------------------------- one stage
+// x * W_R^e (e a compile-time constant after unrolling); trivial powers are free
 template <int R, bool INV>
+__device__ __forceinline__ double2 tw_mul(double2 x, int e) {
+  e %= R;
+  if (e == 0) return x;
+  if (2 * e == R) return make_double2(-x.x, -x.y);
+  if (4 * e == R) return mul_mi<INV>(x);
+  if (4 * e == 3 * R) return mul_mi<!INV>(x);
+  const double c = TwC<R>::c(e);
+  const double s = INV ? TwC<R>::s(e) : -TwC<R>::s(e);
+  return make_double2(fma(x.x, c, -x.y * s), fma(x.x, s, x.y * c));
+}
+
+// Composite R = P x Q in registers: inputs a[r + Q j] (r < Q, j < P); inner DFT_P over j,
+// twiddle W_R^{r k1}, outer DFT_Q over r; output index k1 + P k2.
+template <int P, int Q, bool INV>
+struct DftPQ {
+  static __device__ __forceinline__ void run(double2* a) {
+    constexpr int R = P * Q;
+    double2 u[Q][P];
+#pragma unroll
+    for (int r = 0; r < Q; ++r) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) u[r][j] = a[r + Q * j];
+      Dft<P, INV>::run(u[r]);
+      if (r > 0) {
+#pragma unroll
+        for (int k1 = 1; k1 < P; ++k1) u[r][k1] = tw_mul<R, INV>(u[r][k1], r * k1);
+      }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) {
+      double2 v[Q];
+#pragma unroll
+      for (int r = 0; r < Q; ++r) v[r] = u[r][k1];
+      Dft<Q, INV>::run(v);
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) a[k1 + P * k2] = v[k2];
+    }
+  }
+};
+
+template <bool INV> struct Dft<12, INV> : DftPQ<4, 3, INV> {};
+template <bool INV> struct Dft<16, INV> : DftPQ<4, 4, INV> {};
+template <bool INV> struct Dft<18, INV> : DftPQ<2, 9, INV> {};
+template <bool INV> struct Dft<24, INV> : DftPQ<8, 3, INV> {};
+template <bool INV> struct Dft<27, INV> : DftPQ<3, 9, INV> {};
+template <bool INV> struct Dft<32, INV> : DftPQ<4, 8, INV> {};
+template <bool INV> struct Dft<36, INV> : DftPQ<4, 9, INV> {};
+
+// ----------------------------------------------------------------- one stage
+// Stage twiddles are stored per stage as tw[(k - 1) * Ns + (j mod Ns)] = W_{Ns R}^{(j mod Ns) k}
+// (k = 1..R-1), so the R-1 twiddle loads of a warp are contiguous (coalesced) in every stage;
+// `tw` points at the current stage's block.  TWS: table in shared memory.
+template <int R, bool INV, bool TWS = false>
 __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
                                           const double2* __restrict__ tw) {
   constexpr int K = fft_kmax(R);
   const int nb = n / R;
-  const int tstep = n / (Ns * R);
   double2 a[K][R];
   int outb[K];
 #pragma unroll
@@ -187,10 +244,9 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
       for (int k = 0; k < R; ++k) a[q][k] = buf[j + k * nb];
       const int jm = j % Ns;
       if (jm != 0) {
-        const int step = jm * tstep;
 #pragma unroll
         for (int k = 1; k < R; ++k) {
-          const double2 w = __ldg(&tw[k * step]);
+          const double2 w = TWS ? tw[(k - 1) * Ns + jm] : __ldg(&tw[(k - 1) * Ns + jm]);
           a[q][k] = INV ? cmulc(a[q][k], w) : cmul(a[q][k], w);
         }
       }
@@ -211,32 +267,94 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
 
 // Full transform of the line at `buf` by thread t (0 <= t < pl.nthr or idle beyond).
 // Must be called by every thread of the CTA (contains barriers).
-template <bool INV>
+template <bool INV, bool TWS = false>
 __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t) {
   const int n = pl.n, nthr = pl.nthr;
+  const double2* tw = pl.tw;   // stage 1 (Ns = 1) needs no twiddles and has no block
   int Ns = 1;
 #pragma unroll 1
   for (int s = 0; s < pl.n9; ++s) {
-    fft_stage<9, INV>(buf, n, Ns, t, nthr, pl.tw);
+    fft_stage<9, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    if (Ns > 1) tw += 8 * Ns;
     Ns *= 9;
   }
   if (pl.r3 == 6) {
-    fft_stage<6, INV>(buf, n, Ns, t, nthr, pl.tw);
+    fft_stage<6, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    if (Ns > 1) tw += 5 * Ns;
     Ns *= 6;
   } else if (pl.r3 == 3) {
-    fft_stage<3, INV>(buf, n, Ns, t, nthr, pl.tw);
+    fft_stage<3, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    if (Ns > 1) tw += 2 * Ns;
     Ns *= 3;
   }
 #pragma unroll 1
   for (int s = 0; s < pl.n8; ++s) {
-    fft_stage<8, INV>(buf, n, Ns, t, nthr, pl.tw);
+    fft_stage<8, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    if (Ns > 1) tw += 7 * Ns;
     Ns *= 8;
   }
-  if (pl.r2 == 4) fft_stage<4, INV>(buf, n, Ns, t, nthr, pl.tw);
-  else if (pl.r2 == 2) fft_stage<2, INV>(buf, n, Ns, t, nthr, pl.tw);
+  if (pl.r2 == 2) fft_stage<2, INV, TWS>(buf, n, Ns, t, nthr, tw);
+  else if (pl.r2 == 4) fft_stage<4, INV, TWS>(buf, n, Ns, t, nthr, tw);
 }
 
-// host: build a plan (radix schedule + thread count); twiddle table filled separately
-bool fft_factor(int n, FftPlan* pl);
+// ----------------------------------------------------------------- host planning
+inline int fft_stage_list(const FftPlan& pl, int* rad) {
+  int ns = 0;
+  for (int i = 0; i < pl.n9; ++i) rad[ns++] = 9;
+  if (pl.r3 > 1) rad[ns++] = pl.r3;
+  for (int i = 0; i < pl.n8; ++i) rad[ns++] = 8;
+  if (pl.r2 > 1) rad[ns++] = pl.r2;
+  return ns;
+}
+
+// n = 2^a 3^b -> 9^(b/2) * r3 * 8^(a'/3) * r2 with r3 = 3 or 6 (b odd; 6 absorbs one
+// factor 2 when a >= 1) and r2 = 2^(a' % 3)
+inline bool fft_factor(int n, FftPlan* pl) {
+  int a = 0, b = 0, m = n;
+  if (n < 1) return false;
+  while (m % 2 == 0) { m /= 2; ++a; }
+  while (m % 3 == 0) { m /= 3; ++b; }
+  if (m != 1) return false;
+  pl->n = n;
+  pl->n9 = b / 2;
+  pl->r3 = 1;
+  if (b % 2 == 1) {
+    if (a >= 1) { pl->r3 = 6; a -= 1; } else { pl->r3 = 3; }
+  }
+  pl->n8 = a / 3;
+  pl->r2 = 1 << (a % 3);
+  int rad[FFT_MAX_STAGES];
+  pl->nstages = fft_stage_list(*pl, rad);
+  int need = 1;
+  for (int i = 0; i < pl->nstages; ++i) {
+    const int nb = n / rad[i];
+    const int k = fft_kmax(rad[i]);
+    need = need > (nb + k - 1) / k ? need : (nb + k - 1) / k;
+  }
+  pl->nthr = (need + 31) / 32 * 32;
+  if (pl->nthr < 32) pl->nthr = 32;
+  return true;
+}
+
+// host: per-stage twiddle table for a factored plan (entries in stage order, Ns > 1 only)
+template <class Vec, class Make>
+inline void fft_stage_twiddles(const FftPlan& pl, Vec& out, Make make_c) {
+  int rad[FFT_MAX_STAGES];
+  const int ns = fft_stage_list(pl, rad);
+  const long double PI_L = 3.141592653589793238462643383279502884L;
+  long long Ns = 1;
+  for (int s = 0; s < ns; ++s) {
+    const int R = rad[s];
+    if (Ns > 1) {
+      for (int k = 1; k < R; ++k)
+        for (long long jm = 0; jm < Ns; ++jm) {
+          const long long num = (jm * k) % (Ns * R);
+          const long double ang = 2.0L * PI_L * (long double)num / (long double)(Ns * R);
+          out.push_back(make_c((double)cosl(ang), (double)(-sinl(ang))));
+        }
+    }
+    Ns *= R;
+  }
+}
 
 }  // namespace rk
