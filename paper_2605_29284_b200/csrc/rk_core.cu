@@ -416,6 +416,7 @@ int quarter_ld(int p2);                                             // rk_predic
 
 static void free_setup(rk_setup* s) {
   if (!s) return;
+  free_workspaces(s);
   cudaFree(s->obs);
   cudaFree(s->base);
   cudaFree(s->weights);

@@ -1,6 +1,8 @@
 // Internal structures shared by the rapidkrig B200 translation units.
 #pragma once
 
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "rk_common.cuh"
@@ -26,6 +28,35 @@ struct Embedding {
   int hs1 = 0, qs2 = 0;          // ps1/2+1, ps2/2+1
   FftPlan pl1{}, pl2{};
   double* root_q = nullptr;      // (qs2, hs1) row-major: sqrt(clip(lambda,0)) * sqrt(P)/P
+};
+
+// Per-(setup, stream) persistent predict workspace: intermediate buffers for one
+// field, staging buffers for the host-buffer path, and a cache of instantiated CUDA
+// graphs of the 4-kernel predict keyed by the caller's pointers.
+struct GraphKey {
+  uintptr_t c, beta, xg, out;
+  int p;
+  bool operator<(const GraphKey& o) const {
+    if (c != o.c) return c < o.c;
+    if (beta != o.beta) return beta < o.beta;
+    if (xg != o.xg) return xg < o.xg;
+    if (out != o.out) return out < o.out;
+    return p < o.p;
+  }
+};
+
+struct Workspace {
+  double* cstar = nullptr;      // (M2, ldc)
+  double2* T = nullptr;         // (H1, ldT)
+  double2* U = nullptr;         // (H1, ldU)
+  double* c_in = nullptr;       // host-path staging
+  double* beta_in = nullptr;
+  double* xg_in = nullptr;
+  size_t xg_cap = 0;
+  double* out = nullptr;
+  cudaStream_t cap = nullptr;   // private stream used only for graph capture
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, int> seen;
 };
 
 }  // namespace rk
@@ -55,6 +86,8 @@ struct rk_setup {
   std::vector<double> kn_chol, kn_inv;
   double cond_var_min = 0;
   rk::Embedding emb;
+  std::mutex ws_mu;
+  std::map<cudaStream_t, rk::Workspace*> ws;
 };
 
 struct rk_fit {
@@ -88,7 +121,8 @@ struct PredictBatch {
   double* out = nullptr;          // (batch, m2, m1): field, or e = interior(g) - field in CS mode
 };
 Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st,
-                     cudaEvent_t* ev = nullptr);
+                     cudaEvent_t* ev = nullptr, Workspace* ws = nullptr);
+void free_workspaces(rk_setup* s);
 
 // CS pieces (rk_sim.cu)
 Status ensure_embedding(rk_setup* s, cudaStream_t st);

@@ -16,6 +16,8 @@
 //   build_filter_spectrum 72-86 -> spectrum_quarter(): lag table on the quarter torus,
 //       pass 1 (lag mode) + pass 2 (spectrum mode, real part of ky <= p2/2)
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "rk_internal.cuh"
 
@@ -494,12 +496,18 @@ static inline int64_t round_even(int64_t v) { return (v + 1) & ~int64_t(1); }
 // (c* or a caller field); output rows [row0, row0 + nout) x cols [col0, col0 + ncols).
 static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in, int64_t in_bstride,
                             int batch, int row0, int nout, int col0, int ncols, const RowInvArgs& epi,
-                            cudaStream_t st, cudaEvent_t* ev = nullptr) {
+                            cudaStream_t st, cudaEvent_t* ev = nullptr, Workspace* ws = nullptr) {
   const int64_t ldT = round_even(s->M2);
   const int64_t ldU = round_even(nout);
   double2 *T = nullptr, *U = nullptr;
-  RK_TRY(scratch_alloc((void**)&T, sizeof(double2) * (size_t)s->H1 * ldT * batch, st));
-  RK_TRY(scratch_alloc((void**)&U, sizeof(double2) * (size_t)s->H1 * ldU * batch, st));
+  const bool own = !(ws && batch == 1);
+  if (own) {
+    RK_TRY(scratch_alloc((void**)&T, sizeof(double2) * (size_t)s->H1 * ldT * batch, st));
+    RK_TRY(scratch_alloc((void**)&U, sizeof(double2) * (size_t)s->H1 * ldU * batch, st));
+  } else {
+    T = ws->T;
+    U = ws->U;
+  }
   RowFwdArgs ra{};
   ra.pl = s->pl1;
   ra.lpc = pick_lpc(s->pl1, 4);
@@ -544,12 +552,15 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   ia.ncols = ncols;
   RK_TRY(launch_row_inv(ia, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[4], st));
-  scratch_free(T, st);
-  scratch_free(U, st);
+  if (own) {
+    scratch_free(T, st);
+    scratch_free(U, st);
+  }
   return Status::ok();
 }
 
-Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st, cudaEvent_t* ev) {
+Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st, cudaEvent_t* ev,
+                     Workspace* ws) {
   RowInvArgs e{};
   e.out = pb.out;
   e.ldo = s->m1;
@@ -565,13 +576,94 @@ Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st,
   e.g_col0 = s->grid.pad[0];
   const int64_t ldc = round_even(s->M1);
   double* cstar = nullptr;
-  RK_TRY(scratch_alloc((void**)&cstar, sizeof(double) * (size_t)ldc * s->M2 * pb.batch, st));
+  const bool own = !(ws && pb.batch == 1);
+  if (own) RK_TRY(scratch_alloc((void**)&cstar, sizeof(double) * (size_t)ldc * s->M2 * pb.batch, st));
+  else cstar = ws->cstar;
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[0], st));
   RK_TRY(launch_cstar(s, pb.c, pb.c_stride, cstar, ldc, pb.batch, st));
   Status r = conv_pipeline(s, cstar, ldc, ldc * s->M2, pb.batch, s->grid.pad[2], s->m2,
-                           s->grid.pad[0], s->m1, e, st, ev);
-  scratch_free(cstar, st);
+                           s->grid.pad[0], s->m1, e, st, ev, ws);
+  if (own) scratch_free(cstar, st);
   return r;
+}
+
+// ------------------------------------------------- persistent workspace + graph replay
+static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
+  std::lock_guard<std::mutex> lk(s->ws_mu);
+  auto it = s->ws.find(st);
+  if (it != s->ws.end()) {
+    *out = it->second;
+    return Status::ok();
+  }
+  Workspace* w = new Workspace();
+  const int64_t ldc = round_even(s->M1), ldT = round_even(s->M2), ldU = round_even(s->m2);
+  RK_CUDA_TRY(cudaMalloc(&w->cstar, sizeof(double) * (size_t)ldc * s->M2));
+  RK_CUDA_TRY(cudaMalloc(&w->T, sizeof(double2) * (size_t)s->H1 * ldT));
+  RK_CUDA_TRY(cudaMalloc(&w->U, sizeof(double2) * (size_t)s->H1 * ldU));
+  RK_CUDA_TRY(cudaMalloc(&w->c_in, sizeof(double) * std::max<int64_t>(s->n, 2)));
+  RK_CUDA_TRY(cudaMalloc(&w->beta_in, sizeof(double) * 16));
+  RK_CUDA_TRY(cudaMalloc(&w->out, sizeof(double) * (size_t)s->m1 * s->m2));
+  RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
+  s->ws[st] = w;
+  *out = w;
+  return Status::ok();
+}
+
+void free_workspaces(rk_setup* s) {
+  for (auto& kv : s->ws) {
+    Workspace* w = kv.second;
+    for (auto& g : w->graphs) cudaGraphExecDestroy(g.second);
+    cudaFree(w->cstar);
+    cudaFree(w->T);
+    cudaFree(w->U);
+    cudaFree(w->c_in);
+    cudaFree(w->beta_in);
+    cudaFree(w->xg_in);
+    cudaFree(w->out);
+    if (w->cap) cudaStreamDestroy(w->cap);
+    delete w;
+  }
+  s->ws.clear();
+}
+
+// Predict of one field through the workspace: direct launches the first time a pointer
+// set is seen, a CUDA graph (captured on the workspace's private stream, replayed on
+// `st`) from the second time on.
+static Status predict_graphed(rk_setup* s, Workspace* w, const PredictBatch& pb, cudaStream_t st) {
+  const GraphKey key{(uintptr_t)pb.c, (uintptr_t)pb.beta, (uintptr_t)pb.xg, (uintptr_t)pb.out, pb.p};
+  cudaGraphExec_t exec = nullptr;
+  bool capture = false;
+  {
+    std::lock_guard<std::mutex> lk(s->ws_mu);
+    auto it = w->graphs.find(key);
+    if (it != w->graphs.end()) exec = it->second;
+    else capture = (++w->seen[key] >= 2) && w->graphs.size() < 64;
+  }
+  if (exec) {
+    RK_CUDA_TRY(cudaGraphLaunch(exec, st));
+    count_launch(4);
+    return Status::ok();
+  }
+  if (!capture) return predict_batch(s, pb, st, nullptr, w);
+  cudaGraph_t g = nullptr;
+  RK_CUDA_TRY(cudaStreamBeginCapture(w->cap, cudaStreamCaptureModeThreadLocal));
+  Status r = predict_batch(s, pb, w->cap, nullptr, w);
+  const cudaError_t ec = cudaStreamEndCapture(w->cap, &g);
+  count_launch(-4);   // captured, not executed
+  if (!r.good()) {
+    if (g) cudaGraphDestroy(g);
+    return r;
+  }
+  RK_CUDA_TRY(ec);
+  RK_CUDA_TRY(cudaGraphInstantiate(&exec, g, 0));
+  cudaGraphDestroy(g);
+  {
+    std::lock_guard<std::mutex> lk(s->ws_mu);
+    w->graphs[key] = exec;
+  }
+  RK_CUDA_TRY(cudaGraphLaunch(exec, st));
+  count_launch(4);
+  return Status::ok();
 }
 
 }  // namespace rk
@@ -644,7 +736,10 @@ rk_status rk_predict_dev(const rk_setup* s, const double* c_dev, const double* b
     pb.p = p;
     pb.xg = xg_dev;
     pb.out = out_dev;
-    return predict_batch(s, pb, (cudaStream_t)stream);
+    rk_setup* ms = const_cast<rk_setup*>(s);
+    Workspace* w = nullptr;
+    RK_TRY(get_ws(ms, (cudaStream_t)stream, &w));
+    return predict_graphed(ms, w, pb, (cudaStream_t)stream);
   };
   return (rk_status)finish_status(run());
 }
@@ -664,7 +759,9 @@ rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const doubl
     pb.p = p;
     pb.xg = xg_dev;
     pb.out = out_dev;
-    Status r = predict_batch(s, pb, st, ev);
+    Workspace* w = nullptr;
+    RK_TRY(get_ws(const_cast<rk_setup*>(s), st, &w));
+    Status r = predict_batch(s, pb, st, ev, w);
     if (r.good()) {
       RK_CUDA_TRY(cudaEventSynchronize(ev[4]));
       for (int i = 0; i < 4; ++i) RK_CUDA_TRY(cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]));
@@ -694,30 +791,34 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
     cudaStream_t st = (cudaStream_t)stream;
     if (beta && !xg && p != 1)
       return Status::err(RK_DOMAIN, "grid covariates are required when beta_hat has more than one entry");
+    if (p > 16) return Status::err(RK_DOMAIN, "at most 16 covariates");
+    rk_setup* ms = const_cast<rk_setup*>(s);
+    Workspace* w = nullptr;
+    RK_TRY(get_ws(ms, st, &w));
     const int64_t N = (int64_t)s->m1 * s->m2;
-    auto up16 = [](size_t v) { return (v + 15) & ~size_t(15); };
-    const size_t bc = up16(sizeof(double) * s->n), bb = beta ? up16(sizeof(double) * p) : 0,
-                 bx = xg ? up16(sizeof(double) * N * p) : 0, bo = sizeof(double) * N;
-    char* ws = nullptr;
-    RK_TRY(scratch_alloc((void**)&ws, bc + bb + bx + bo + 64, st));
-    double* dc = (double*)ws;
-    double* db = beta ? (double*)(ws + bc) : nullptr;
-    double* dx = xg ? (double*)(ws + bc + bb) : nullptr;
-    double* dout = (double*)(ws + bc + bb + bx);
-    RK_CUDA_TRY(cudaMemcpyAsync(dc, c, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
-    if (beta) RK_CUDA_TRY(cudaMemcpyAsync(db, beta, sizeof(double) * p, cudaMemcpyHostToDevice, st));
-    if (xg) RK_CUDA_TRY(cudaMemcpyAsync(dx, xg, sizeof(double) * N * p, cudaMemcpyHostToDevice, st));
+    if (xg && w->xg_cap < (size_t)(N * p)) {
+      std::lock_guard<std::mutex> lk(ms->ws_mu);
+      cudaFree(w->xg_in);
+      for (auto& g : w->graphs) cudaGraphExecDestroy(g.second);   // keys held the old pointer
+      w->graphs.clear();
+      w->seen.clear();
+      w->xg_in = nullptr;
+      RK_CUDA_TRY(cudaMalloc(&w->xg_in, sizeof(double) * N * p));
+      w->xg_cap = (size_t)(N * p);
+    }
+    RK_CUDA_TRY(cudaMemcpyAsync(w->c_in, c, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
+    if (beta) RK_CUDA_TRY(cudaMemcpyAsync(w->beta_in, beta, sizeof(double) * p, cudaMemcpyHostToDevice, st));
+    if (xg) RK_CUDA_TRY(cudaMemcpyAsync(w->xg_in, xg, sizeof(double) * N * p, cudaMemcpyHostToDevice, st));
     PredictBatch pb;
     pb.batch = 1;
-    pb.c = dc;
+    pb.c = w->c_in;
     pb.c_stride = s->n;
-    pb.beta = db;
+    pb.beta = beta ? w->beta_in : nullptr;
     pb.p = p;
-    pb.xg = dx;
-    pb.out = dout;
-    RK_TRY(predict_batch(s, pb, st));
-    RK_CUDA_TRY(cudaMemcpyAsync(out, dout, bo, cudaMemcpyDeviceToHost, st));
-    scratch_free(ws, st);
+    pb.xg = xg ? w->xg_in : nullptr;
+    pb.out = w->out;
+    RK_TRY(predict_graphed(ms, w, pb, st));
+    RK_CUDA_TRY(cudaMemcpyAsync(out, w->out, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
     RK_CUDA_TRY(cudaStreamSynchronize(st));
     return Status::ok();
   };
