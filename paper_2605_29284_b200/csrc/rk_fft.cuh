@@ -235,20 +235,41 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
   const int nb = n / R;
   double2 a[K][R];
   int outb[K];
+  // j mod Ns for j = t + q nthr, updated incrementally (one division per stage, not per butterfly)
+  int jm = t % Ns;
+  const int jstep = nthr % Ns;
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     const int j = t + q * nthr;
     outb[q] = -1;
+    if (q > 0) {
+      jm += jstep;
+      if (jm >= Ns) jm -= Ns;
+    }
     if (j < nb) {
 #pragma unroll
       for (int k = 0; k < R; ++k) a[q][k] = buf[j + k * nb];
-      const int jm = j % Ns;
       if (jm != 0) {
+#ifndef RK_TW_POWERS
+#define RK_TW_POWERS 1
+#endif
+#if RK_TW_POWERS
+        // one coalesced load of w = W^{jm}; w^k by complex products (trades the L1/smem
+        // bandwidth the engine is bound by for FP64 work it has spare)
+        const double2 w1 = TWS ? tw[jm] : __ldg(&tw[jm]);
+        double2 wk = w1;
+#pragma unroll
+        for (int k = 1; k < R; ++k) {
+          if (k > 1) wk = cmul(wk, w1);
+          a[q][k] = INV ? cmulc(a[q][k], wk) : cmul(a[q][k], wk);
+        }
+#else
 #pragma unroll
         for (int k = 1; k < R; ++k) {
           const double2 w = TWS ? tw[(k - 1) * Ns + jm] : __ldg(&tw[(k - 1) * Ns + jm]);
           a[q][k] = INV ? cmulc(a[q][k], w) : cmul(a[q][k], w);
         }
+#endif
       }
       Dft<R, INV>::run(a[q]);
       outb[q] = (j - jm) * R + jm;

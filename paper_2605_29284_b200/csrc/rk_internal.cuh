@@ -98,6 +98,7 @@ struct rk_fit {
   double* U = nullptr;          // (n, n) column-major UPPER factor = row-major lower L
   double* X = nullptr;          // (n, p) column-major
   double* B = nullptr;          // L^-1 X (n, p) column-major
+  double* Uinv = nullptr;       // U^-1 = L^-T (n, n) column-major upper, built on first batched refit
   double* beta = nullptr;       // (p)
   double* c = nullptr;          // (n)
   std::vector<double> gram_lu;  // (p, p) LU of B'B with partial pivoting (row-major)

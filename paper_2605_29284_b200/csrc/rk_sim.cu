@@ -490,8 +490,9 @@ static GramLU gram_args(const rk_fit* f) {
   return g;
 }
 
-// GLS for `batch` right-hand sides Z (n x batch, column-major) -> beta (p x batch), C (n x batch)
-static Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C,
+// GLS by triangular solves (exact.py:59-68) for `batch` right-hand sides Z (n x batch,
+// column-major) -> beta (p x batch), C (n x batch).  Used once per fit.
+static Status gls_trsm(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C,
                         cudaStream_t st) {
   cublasHandle_t h = (cublasHandle_t)f->cublas;
   RK_CUBLAS_TRY(cublasSetStream(h, st));
@@ -520,8 +521,40 @@ static Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double*
   return Status::ok();
 }
 
+static Status ensure_uinv(rk_fit* f, cudaStream_t st);
+
+// Batched refit (exact.py:108-113) with the precomputed inverse factor: two FP64
+// tensor-core GEMMs per batch instead of three triangular solves.
+//   A = L^-1 Z ; beta = (B'B)^-1 B'A ; H = A - B beta (= L^-1 (Z - X beta)) ; C = L^-T H
+static Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C,
+                        cudaStream_t st) {
+  cublasHandle_t h = (cublasHandle_t)f->cublas;
+  RK_CUBLAS_TRY(cublasSetStream(h, st));
+  const int n = (int)f->n, p = f->p, nb = (int)batch;
+  const double one = 1.0, zero = 0.0;
+  RK_TRY(ensure_uinv(const_cast<rk_fit*>(f), st));
+  double *A = nullptr, *H = nullptr;
+  RK_TRY(scratch_alloc((void**)&A, sizeof(double) * (size_t)n * nb, st));
+  RK_TRY(scratch_alloc((void**)&H, sizeof(double) * (size_t)n * nb, st));
+  // L^-1 = U^-T
+  RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, n, nb, n, &one, f->Uinv, n, Z, n, &zero, A, n));
+  RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, nb, n, &one, f->B, n, A, n, &zero, beta, p));
+  gram_solve_kernel<<<(nb + 127) / 128, 128, 0, st>>>(gram_args(f), beta, nb);
+  count_launch();
+  resid_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)n * nb, 256), 148 * 32), 256, 0, st>>>(
+      A, f->B, n, p, beta, nb, H);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  // L^-T = U^-1
+  RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, nb, n, &one, f->Uinv, n, H, n, &zero, C, n));
+  scratch_free(A, st);
+  scratch_free(H, st);
+  return Status::ok();
+}
+
 static void free_fit(rk_fit* f) {
   if (!f) return;
+  cudaFree(f->Uinv);
   cudaFree(f->U);
   cudaFree(f->X);
   cudaFree(f->B);
@@ -561,6 +594,44 @@ static Status fit_prepare_x(rk_fit* f, const double* X_host) {
   f->gram_lu = gr;
   if (!lu_factor(f->gram_lu, p, f->gram_piv))
     return Status::err(RK_NUMERIC, "singular GLS Gram matrix X' M^-1 X");
+  return Status::ok();
+}
+
+// U^-1 (= L^-T) by blocked triangular inversion (cuSOLVER trtri), once per fit
+static Status ensure_uinv(rk_fit* f, cudaStream_t st) {
+  if (f->Uinv) return Status::ok();
+  const int64_t n = f->n;
+  double* Ui = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&Ui, sizeof(double) * (size_t)n * n));
+  RK_CUDA_TRY(cudaMemcpyAsync(Ui, f->U, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, st));
+  cusolverDnHandle_t sh;
+  if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) return Status::err(RK_CUDA, "cusolverDnCreate failed");
+  cusolverDnSetStream(sh, st);
+  size_t dbytes = 0, hbytes = 0;
+  if (cusolverDnXtrtri_bufferSize(sh, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, Ui, n,
+                                  &dbytes, &hbytes) != CUSOLVER_STATUS_SUCCESS) {
+    cusolverDnDestroy(sh);
+    cudaFree(Ui);
+    return Status::err(RK_CUDA, "cusolverDnXtrtri_bufferSize failed");
+  }
+  void* dwork = nullptr;
+  std::vector<char> hwork(hbytes + 1);
+  int* info = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&dwork, dbytes + 16));
+  RK_CUDA_TRY(cudaMalloc(&info, sizeof(int)));
+  const cusolverStatus_t cs = cusolverDnXtrtri(sh, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F,
+                                               Ui, n, dwork, dbytes, hwork.data(), hbytes, info);
+  int hinfo = 0;
+  RK_CUDA_TRY(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RK_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFree(dwork);
+  cudaFree(info);
+  cusolverDnDestroy(sh);
+  if (cs != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+    cudaFree(Ui);
+    return Status::err(RK_NUMERIC, "triangular inverse of the Cholesky factor failed");
+  }
+  f->Uinv = Ui;
   return Status::ok();
 }
 
@@ -691,7 +762,7 @@ rk_status rk_fit_create(const rk_model* model, const double* obs_host, int64_t n
     double* z = nullptr;
     RK_CUDA_TRY(cudaMalloc(&z, sizeof(double) * n));
     RK_CUDA_TRY(cudaMemcpy(z, z_host, sizeof(double) * n, cudaMemcpyHostToDevice));
-    RK_TRY(gls_batch(f, z, 1, f->beta, f->c, 0));
+    RK_TRY(gls_trsm(f, z, 1, f->beta, f->c, 0));
     RK_CUDA_TRY(cudaDeviceSynchronize());
     cudaFree(z);
     *out = guard.release();
