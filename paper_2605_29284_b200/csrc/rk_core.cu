@@ -65,6 +65,7 @@ Status plan_for(int n, FftPlan* out) {
     return Status::err(RK_DOMAIN, "FFT length " + std::to_string(n) + " too large for one CTA");
   std::vector<double2> tw;
   fft_stage_twiddles(pl, tw, [](double c, double s) { return make_double2(c, s); });
+  pl.ntw = (int)tw.size();
   tw.push_back(make_double2(1.0, 0.0));   // never empty
   double2* d = nullptr;
   RK_CUDA_TRY(cudaMalloc(&d, sizeof(double2) * tw.size()));
@@ -75,10 +76,12 @@ Status plan_for(int n, FftPlan* out) {
   return Status::ok();
 }
 
-int pick_lpc(const FftPlan& pl, int max_lines) {
+int pick_lpc(const FftPlan& pl, int max_lines, int64_t total_lines) {
   const size_t line_bytes = (size_t)pl.n * sizeof(double2);
   int lpc = std::max(1, max_lines);
-  while (lpc > 1 && ((size_t)lpc * line_bytes > 96 * 1024 || lpc * pl.nthr > 512)) --lpc;
+  while (lpc > 1 && ((size_t)lpc * line_bytes > 96 * 1024 || lpc * pl.nthr > 512 ||
+                     ceil_div(total_lines, lpc) < 2 * 148))
+    --lpc;
   return lpc;
 }
 

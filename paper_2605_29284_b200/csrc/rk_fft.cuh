@@ -36,8 +36,18 @@ struct FftPlan {
   int nstages;
   int nthr;                    // threads cooperating on one line (multiple of 32)
   int n9, r3, n8, r2;          // r3 in {1,3,6}, r2 in {1,2,4}
+  int ntw;                     // entries of the stage twiddle table (sum of Ns > 1)
   const double2* tw;           // per-stage twiddles, see fft_stage_twiddles()
 };
+
+// Cooperative copy of the plan's twiddle table into shared memory (caller syncs before
+// the first fft_line that uses it); returns a plan that reads from smem.
+__device__ __forceinline__ FftPlan fft_twiddles_to_smem(const FftPlan& pl, double2* dst) {
+  for (int i = threadIdx.x; i < pl.ntw; i += blockDim.x) dst[i] = __ldg(&pl.tw[i]);
+  FftPlan p = pl;
+  p.tw = dst;
+  return p;
+}
 
 // butterflies each thread keeps in registers for a stage of radix R
 __host__ __device__ constexpr int fft_kmax(int r) {
@@ -225,9 +235,11 @@ template <bool INV> struct Dft<32, INV> : DftPQ<4, 8, INV> {};
 template <bool INV> struct Dft<36, INV> : DftPQ<4, 9, INV> {};
 
 // ----------------------------------------------------------------- one stage
-// Stage twiddles are stored per stage as tw[(k - 1) * Ns + (j mod Ns)] = W_{Ns R}^{(j mod Ns) k}
-// (k = 1..R-1), so the R-1 twiddle loads of a warp are contiguous (coalesced) in every stage;
-// `tw` points at the current stage's block.  TWS: table in shared memory.
+// Stage twiddles: each stage with Ns > 1 owns a block tw[jm] = W_{Ns R}^{jm}, jm < Ns (the
+// k = 1 column); w^k for k >= 2 is formed by complex products, trading the smem/L1
+// bandwidth the engine is bound by for FP64 work it has spare.  The whole table has
+// sum(Ns) entries (~n / R_last), small enough to stage in shared memory per CTA
+// (fft_twiddles_to_smem); warp loads are contiguous.  TWS: table in shared memory.
 template <int R, bool INV, bool TWS = false>
 __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
                                           const double2* __restrict__ tw) {
@@ -250,12 +262,6 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
 #pragma unroll
       for (int k = 0; k < R; ++k) a[q][k] = buf[j + k * nb];
       if (jm != 0) {
-#ifndef RK_TW_POWERS
-#define RK_TW_POWERS 1
-#endif
-#if RK_TW_POWERS
-        // one coalesced load of w = W^{jm}; w^k by complex products (trades the L1/smem
-        // bandwidth the engine is bound by for FP64 work it has spare)
         const double2 w1 = TWS ? tw[jm] : __ldg(&tw[jm]);
         double2 wk = w1;
 #pragma unroll
@@ -263,13 +269,6 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
           if (k > 1) wk = cmul(wk, w1);
           a[q][k] = INV ? cmulc(a[q][k], wk) : cmul(a[q][k], wk);
         }
-#else
-#pragma unroll
-        for (int k = 1; k < R; ++k) {
-          const double2 w = TWS ? tw[(k - 1) * Ns + jm] : __ldg(&tw[(k - 1) * Ns + jm]);
-          a[q][k] = INV ? cmulc(a[q][k], w) : cmul(a[q][k], w);
-        }
-#endif
       }
       Dft<R, INV>::run(a[q]);
       outb[q] = (j - jm) * R + jm;
@@ -296,22 +295,22 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
 #pragma unroll 1
   for (int s = 0; s < pl.n9; ++s) {
     fft_stage<9, INV, TWS>(buf, n, Ns, t, nthr, tw);
-    if (Ns > 1) tw += 8 * Ns;
+    if (Ns > 1) tw += Ns;
     Ns *= 9;
   }
   if (pl.r3 == 6) {
     fft_stage<6, INV, TWS>(buf, n, Ns, t, nthr, tw);
-    if (Ns > 1) tw += 5 * Ns;
+    if (Ns > 1) tw += Ns;
     Ns *= 6;
   } else if (pl.r3 == 3) {
     fft_stage<3, INV, TWS>(buf, n, Ns, t, nthr, tw);
-    if (Ns > 1) tw += 2 * Ns;
+    if (Ns > 1) tw += Ns;
     Ns *= 3;
   }
 #pragma unroll 1
   for (int s = 0; s < pl.n8; ++s) {
     fft_stage<8, INV, TWS>(buf, n, Ns, t, nthr, tw);
-    if (Ns > 1) tw += 7 * Ns;
+    if (Ns > 1) tw += Ns;
     Ns *= 8;
   }
   if (pl.r2 == 2) fft_stage<2, INV, TWS>(buf, n, Ns, t, nthr, tw);
@@ -367,12 +366,10 @@ inline void fft_stage_twiddles(const FftPlan& pl, Vec& out, Make make_c) {
   for (int s = 0; s < ns; ++s) {
     const int R = rad[s];
     if (Ns > 1) {
-      for (int k = 1; k < R; ++k)
-        for (long long jm = 0; jm < Ns; ++jm) {
-          const long long num = (jm * k) % (Ns * R);
-          const long double ang = 2.0L * PI_L * (long double)num / (long double)(Ns * R);
-          out.push_back(make_c((double)cosl(ang), (double)(-sinl(ang))));
-        }
+      for (long long jm = 0; jm < Ns; ++jm) {
+        const long double ang = 2.0L * PI_L * (long double)jm / (long double)(Ns * R);
+        out.push_back(make_c((double)cosl(ang), (double)(-sinl(ang))));
+      }
     }
     Ns *= R;
   }

@@ -14,7 +14,9 @@ namespace rk {
 // --------------------------------------------------------------- bookkeeping
 void count_launch(int k = 1);
 Status plan_for(int n, FftPlan* out);            // cached per (device, n)
-int pick_lpc(const FftPlan& pl, int max_lines);  // lines per CTA for a kernel
+// lines per CTA for a kernel: pack up to max_lines, but only while the launch still has
+// >= 2 CTAs per SM for `total_lines` lines (small grids are latency bound, not occupancy)
+int pick_lpc(const FftPlan& pl, int max_lines, int64_t total_lines = (int64_t)1 << 40);
 Status set_smem_attr(const void* fn, size_t bytes);
 
 // RAII-free stream-ordered scratch (cudaMallocAsync pool)

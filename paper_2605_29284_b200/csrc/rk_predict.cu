@@ -102,6 +102,7 @@ struct RowFwdArgs {
   int tma;                   // SRC_ROWS: rows are 16-byte aligned -> TMA bulk staging
   const double* lagq;        // SRC_LAG: quarter lag table (p2/2+1, p1/2+1)
   int lag_ld, p2;
+  int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
 template <int SRC>
@@ -116,12 +117,19 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
   const int ya = 2 * (blockIdx.x * a.lpc + line);
   const int yb = ya + 1;
   const bool va = ya < a.nrows, vb = yb < a.nrows;
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   if (SRC == SRC_ROWS) {
     const double* rin = a.rows + (int64_t)b * a.in_bstride;
-    double* stage = (double*)(smem + (size_t)a.lpc * n);        // lpc x 2 x ld_in doubles
-    uint64_t* bar = (uint64_t*)(stage + (size_t)a.lpc * 2 * a.ld_in);
-    double* sa = stage + (size_t)line * 2 * a.ld_in;
-    double* sb = sa + a.ld_in;
+    // staging of the two real rows: tma == 2 puts them in the zero-pad tail of the line
+    // buffer itself (no extra smem; needs n - ld_in >= ncols), tma == 1 in a separate area
+    const bool inl = a.tma == 2;
+    double* extra = (double*)(smem + (size_t)a.lpc * n);
+    auto stage_of = [&](int l) -> double* {
+      return inl ? (double*)(smem + (size_t)(l + 1) * n) - 2 * a.ld_in : extra + (size_t)l * 2 * a.ld_in;
+    };
+    uint64_t* bar = inl ? (uint64_t*)extra : (uint64_t*)(extra + (size_t)a.lpc * 2 * a.ld_in);
+    const double* sa = stage_of(line);
+    const double* sb = sa + a.ld_in;
     if (a.tma) {
       if (threadIdx.x == 0) mbar_init(bar, 1);
       __syncthreads();
@@ -134,17 +142,22 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
         mbar_expect_tx(bar, cnt * (uint32_t)(a.ld_in * 8));
         for (int l = 0; l < a.lpc; ++l) {
           const int r0 = 2 * (blockIdx.x * a.lpc + l);
-          double* d = stage + (size_t)l * 2 * a.ld_in;
+          double* d = stage_of(l);
           if (r0 < a.nrows) bulk_g2s(d, rin + (int64_t)r0 * a.ld_in, (uint32_t)(a.ld_in * 8), bar);
           if (r0 + 1 < a.nrows)
             bulk_g2s(d + a.ld_in, rin + (int64_t)(r0 + 1) * a.ld_in, (uint32_t)(a.ld_in * 8), bar);
         }
       }
-      // zero padding beyond the nonzero columns while the copies fly
-      for (int x = a.ncols + tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
+      // zero padding beyond the nonzero columns while the copies fly (separate staging)
+      if (!inl)
+        for (int x = a.ncols + tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
       mbar_wait(bar, 0);
       for (int x = tl; x < a.ncols; x += nthr)
         buf[x] = make_double2(va ? sa[x] : 0.0, vb ? sb[x] : 0.0);
+      if (inl) {   // the staging tail is consumed: now zero it
+        __syncthreads();
+        for (int x = a.ncols + tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
+      }
     } else {
       for (int x = tl; x < n; x += nthr) {
         double u = 0.0, v = 0.0;
@@ -164,7 +177,7 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
     }
   }
   __syncthreads();
-  fft_line<false>(buf, a.pl, tl);
+  fft_line<false, true>(buf, pls, tl);
   // split Z = FFT(u + i v) into U = (Z + conj Z[-k]) / 2, V = (Z - conj Z[-k]) / 2i
   const int nr = 2 * a.lpc;
   const int H = n / 2 + 1;
@@ -199,6 +212,7 @@ struct ColArgs {
   int64_t ldU, U_bstride;
   double* out_q;             // spectrum mode: out_q[kx * ldq + ky] = Re * scale, ky <= p2/2
   double scale;
+  int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
 template <int MODE>  // 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
@@ -230,17 +244,18 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
       if (MODE == 0) bulk_g2s(specs + (size_t)l * a.ldq, a.spec_q + (int64_t)k * a.ldq, specb, bar);
     }
   }
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   for (int y = a.nin + tl; y < n; y += nthr) buf[y] = make_double2(0.0, 0.0);
   if (!valid)
     for (int y = tl; y < a.nin; y += nthr) buf[y] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
-  fft_line<false>(buf, a.pl, tl);
+  fft_line<false, true>(buf, pls, tl);
   if (MODE == 0) {
     const double* S = specs + (size_t)line * a.ldq;
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     __syncthreads();
-    fft_line<true>(buf, a.pl, tl);
+    fft_line<true, true>(buf, pls, tl);
     // TMA bulk store of the kept rows
     fence_async_smem();
     __syncthreads();
@@ -278,6 +293,7 @@ struct RowInvArgs {
   const double* g;           // CS: unconditional fields (batch, M2, M1), or null
   int64_t g_bstride;
   int g_ld, g_row0, g_col0;
+  int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
 __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
@@ -289,6 +305,7 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   const int b = blockIdx.y;
   const int H = n / 2 + 1;
   const double2* U = a.U + (int64_t)b * a.U_bstride;
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   // strided gather of both rows of every line (Z[k] = A[k] + i B[k], Hermitian upper half),
   // batched 4 deep per thread for memory-level parallelism
   const int tot = a.lpc * H;
@@ -320,7 +337,7 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   }
   __syncthreads();
   double2* buf = smem + (size_t)line * n;
-  fft_line<true>(buf, a.pl, tl);
+  fft_line<true, true>(buf, pls, tl);
   const int ya = 2 * (blockIdx.x * a.lpc + line);
   const double* beta = a.beta ? a.beta + (int64_t)b * a.p : nullptr;
   double* out = a.out + (int64_t)b * a.out_bstride;
@@ -346,13 +363,22 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
 }
 
 // ----------------------------------------------------------------- launches
-static Status launch_row_fwd(int src, const RowFwdArgs& a, int batch, cudaStream_t st) {
+// dynamic smem = kernel-specific region (bytes, 16-aligned) + the staged twiddle table
+static inline int tw_slot(size_t bytes_before) { return (int)((bytes_before + 15) / 16); }
+static inline size_t with_tw(size_t bytes_before, const FftPlan& pl) {
+  return (size_t)tw_slot(bytes_before) * 16 + (size_t)pl.ntw * 16;
+}
+
+static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStream_t st) {
+  RowFwdArgs a = a0;
   const int pairs = (a.nrows + 1) / 2;
   const dim3 grid((unsigned)ceil_div(pairs, a.lpc), (unsigned)batch);
   size_t smem = sizeof(double2) * a.pl.n * a.lpc;
   const int threads = a.lpc * a.pl.nthr;
+  if (src == SRC_ROWS) smem += (a.tma == 2 ? 0 : (size_t)a.lpc * 2 * a.ld_in * sizeof(double)) + 16;
+  a.tw_off = tw_slot(smem);
+  smem = with_tw(smem, a.pl);
   if (src == SRC_ROWS) {
-    smem += (size_t)a.lpc * 2 * a.ld_in * sizeof(double) + 16;
     RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_ROWS>, smem));
     row_fwd_kernel<SRC_ROWS><<<grid, threads, smem, st>>>(a);
   } else {
@@ -364,12 +390,15 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a, int batch, cudaStream
   return Status::ok();
 }
 
-static Status launch_col(int mode, const ColArgs& a, int batch, cudaStream_t st) {
+static Status launch_col(int mode, const ColArgs& a0, int batch, cudaStream_t st) {
+  ColArgs a = a0;
   const dim3 grid((unsigned)ceil_div(a.ncols, a.lpc), (unsigned)batch);
   size_t smem = sizeof(double2) * a.pl.n * a.lpc + 16;
   const int threads = a.lpc * a.pl.nthr;
+  if (mode == 0) smem += sizeof(double) * (size_t)a.lpc * a.ldq;
+  a.tw_off = tw_slot(smem);
+  smem = with_tw(smem, a.pl);
   if (mode == 0) {
-    smem += sizeof(double) * (size_t)a.lpc * a.ldq;
     RK_TRY(set_smem_attr((const void*)col_kernel<0>, smem));
     col_kernel<0><<<grid, threads, smem, st>>>(a);
   } else {
@@ -381,10 +410,13 @@ static Status launch_col(int mode, const ColArgs& a, int batch, cudaStream_t st)
   return Status::ok();
 }
 
-static Status launch_row_inv(const RowInvArgs& a, int batch, cudaStream_t st) {
+static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
+  RowInvArgs a = a0;
   const int pairs = (a.nrows + 1) / 2;
   const dim3 grid((unsigned)ceil_div(pairs, a.lpc), (unsigned)batch);
-  const size_t smem = sizeof(double2) * a.pl.n * a.lpc;
+  size_t smem = sizeof(double2) * a.pl.n * a.lpc;
+  a.tw_off = tw_slot(smem);
+  smem = with_tw(smem, a.pl);
   RK_TRY(set_smem_attr((const void*)row_inv_kernel, smem));
   row_inv_kernel<<<grid, a.lpc * a.pl.nthr, smem, st>>>(a);
   count_launch();
@@ -510,7 +542,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   }
   RowFwdArgs ra{};
   ra.pl = s->pl1;
-  ra.lpc = pick_lpc(s->pl1, 4);
+  ra.lpc = pick_lpc(s->pl1, 4, (int64_t)((s->M2 + 1) / 2) * batch);
   ra.nrows = s->M2;
   ra.ncols = s->M1;
   ra.T = T;
@@ -521,12 +553,13 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   ra.in_bstride = in_bstride;
   ra.tma = ((ld_in * 8) % 16 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0) &&
            ((in_bstride * 8) % 16 == 0);
+  if (ra.tma && s->pl1.n - ld_in >= s->M1) ra.tma = 2;   // stage inside the line's zero tail
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[1], st));
   RK_TRY(launch_row_fwd(SRC_ROWS, ra, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[2], st));
   ColArgs ca{};
   ca.pl = s->pl2;
-  ca.lpc = pick_lpc(s->pl2, 4);
+  ca.lpc = pick_lpc(s->pl2, 4, (int64_t)s->H1 * batch);
   ca.ncols = s->H1;
   ca.nin = s->M2;
   ca.T = T;
@@ -543,7 +576,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
   RowInvArgs ia = epi;
   ia.pl = s->pl1;
-  ia.lpc = pick_lpc(s->pl1, 4);
+  ia.lpc = pick_lpc(s->pl1, 4, (int64_t)((nout + 1) / 2) * batch);
   ia.nrows = nout;
   ia.U = U;
   ia.ldU = ldU;

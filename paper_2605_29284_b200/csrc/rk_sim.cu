@@ -88,16 +88,18 @@ struct CsRowArgs {
   int direct;                // ... or 1: `seed` is the field seed itself
   double2* V;                // (batch, keep, ldV)
   int64_t ldV, V_bstride;
+  int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
 __global__ void __launch_bounds__(512, 1) cs_row_kernel(const CsRowArgs a) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
   const int line = threadIdx.x / nthr;
   const int tl = threadIdx.x - line * nthr;
   const int b = blockIdx.y;
   const int iy = blockIdx.x * a.lpc + line;
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   const bool valid = iy < a.ps2;
   double2* buf = smem + (size_t)line * n;
   const uint64_t fs =
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(512, 1) cs_row_kernel(const CsRowArgs a) {
     for (int ix = tl; ix < n; ix += nthr) buf[ix] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  fft_line<true>(buf, a.pl, tl);
+  fft_line<true, true>(buf, pls, tl);
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, ix = idx / a.lpc;
@@ -150,10 +152,11 @@ struct CsColArgs {
   int64_t ldV, V_bstride;
   double* g;                 // (batch, M2, M1)
   int64_t g_bstride;
+  int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
 __global__ void __launch_bounds__(512, 1) cs_col_kernel(const CsColArgs a) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
   const int line = threadIdx.x / nthr;
@@ -162,9 +165,10 @@ __global__ void __launch_bounds__(512, 1) cs_col_kernel(const CsColArgs a) {
   const int ix = blockIdx.x * a.lpc + line;
   double2* buf = smem + (size_t)line * n;
   const double2* V = a.V + (int64_t)b * a.V_bstride + (int64_t)ix * a.ldV;
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   for (int y = tl; y < n; y += nthr) buf[y] = ix < a.ncols ? V[y] : make_double2(0.0, 0.0);
   __syncthreads();
-  fft_line<true>(buf, a.pl, tl);
+  fft_line<true, true>(buf, pls, tl);
   double* g = a.g + (int64_t)b * a.g_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, y = idx / a.lpc;
@@ -313,7 +317,7 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   RK_TRY(scratch_alloc((void**)&V, sizeof(double2) * (size_t)s->M1 * ldV * batch, st));
   CsRowArgs ra{};
   ra.pl = e.pl1;
-  ra.lpc = pick_lpc(e.pl1, 4);
+  ra.lpc = pick_lpc(e.pl1, 4, (int64_t)e.ps2 * batch);
   ra.ps1 = e.ps1;
   ra.ps2 = e.ps2;
   ra.keep = s->M1;
@@ -327,7 +331,8 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   ra.V_bstride = (int64_t)s->M1 * ldV;
   {
     const dim3 grid((unsigned)ceil_div(e.ps2, ra.lpc), (unsigned)batch);
-    const size_t smem = sizeof(double2) * e.ps1 * ra.lpc;
+    ra.tw_off = (int)(ra.lpc * (size_t)e.ps1);
+    const size_t smem = sizeof(double2) * (e.ps1 * (size_t)ra.lpc + e.pl1.ntw);
     RK_TRY(set_smem_attr((const void*)cs_row_kernel, smem));
     cs_row_kernel<<<grid, ra.lpc * e.pl1.nthr, smem, st>>>(ra);
     count_launch();
@@ -335,7 +340,7 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   }
   CsColArgs ca{};
   ca.pl = e.pl2;
-  ca.lpc = pick_lpc(e.pl2, 4);
+  ca.lpc = pick_lpc(e.pl2, 4, (int64_t)s->M1 * batch);
   ca.ncols = s->M1;
   ca.keep = s->M2;
   ca.V = V;
@@ -345,7 +350,8 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   ca.g_bstride = (int64_t)s->M1 * s->M2;
   {
     const dim3 grid((unsigned)ceil_div(s->M1, ca.lpc), (unsigned)batch);
-    const size_t smem = sizeof(double2) * e.ps2 * ca.lpc;
+    ca.tw_off = (int)(ca.lpc * (size_t)e.ps2);
+    const size_t smem = sizeof(double2) * (e.ps2 * (size_t)ca.lpc + e.pl2.ntw);
     RK_TRY(set_smem_attr((const void*)cs_col_kernel, smem));
     cs_col_kernel<<<grid, ca.lpc * e.pl2.nthr, smem, st>>>(ca);
     count_launch();
