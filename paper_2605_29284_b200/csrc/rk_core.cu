@@ -417,6 +417,119 @@ Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2
                         double* out_q, int ldq, cudaStream_t st);  // rk_predict.cu
 int quarter_ld(int p2);                                             // rk_predict.cu
 
+// ---------------------------------------------------- sparse gather plan (setup)
+// Every (sorted obs j, block entry m) contributes w * c to node q = base_j + (m / BS) M1 +
+// (m % BS).  A stable sort by (q, dy) keeps j ascending inside each (q, dy), which is the
+// accumulation order of the dense gather; the per-predict gather then touches only the
+// n M contributions instead of testing 2L cell ranges at every padded node.
+__global__ void ent_gen_kernel(const int32_t* __restrict__ bsort, int64_t n, int M, int BS, int M1,
+                               uint64_t* __restrict__ key, int32_t* __restrict__ val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * M;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / M;
+    const int m = (int)(i % M);
+    const int dy = m / BS, dx = m % BS;
+    const int64_t q = (int64_t)bsort[j] + (int64_t)dy * M1 + dx;
+    key[i] = (uint64_t)q * BS + dy;
+    val[i] = (int32_t)i;
+  }
+}
+
+__global__ void ent_fin_kernel(const uint64_t* __restrict__ key, const int32_t* __restrict__ val,
+                               const int32_t* __restrict__ perm, int64_t tot, int M, int BS,
+                               int32_t* ent_w, int32_t* ent_c, int32_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    ent_w[i] = val[i];
+    ent_c[i] = perm[val[i] / M];
+    flag[i] = (i == 0 || key[i] / BS != key[i - 1] / BS) ? 1 : 0;
+  }
+}
+
+__global__ void node_fill_kernel(const uint64_t* __restrict__ key, const int32_t* __restrict__ flag,
+                                 const int32_t* __restrict__ pos, int64_t tot, int BS,
+                                 int32_t* node_q, int32_t* node_off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (flag[i]) {
+      node_q[pos[i]] = (int32_t)(key[i] / BS);
+      node_off[pos[i]] = (int32_t)i;
+    }
+  }
+}
+
+__global__ void row_node_kernel(const int32_t* __restrict__ node_q, int64_t nnodes, int M1, int M2,
+                                int32_t* row_node) {
+  for (int64_t y = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; y <= M2;
+       y += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t target = y * M1;
+    int64_t lo = 0, hi = nnodes;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (node_q[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    row_node[y] = (int32_t)lo;
+  }
+}
+
+static Status build_sparse_gather(rk_setup* s) {
+  const int64_t tot = s->n * s->M;
+  if (tot >= ((int64_t)1 << 31)) return Status::err(RK_DOMAIN, "n * M too large for the gather plan");
+  uint64_t *key = nullptr, *key2 = nullptr;
+  int32_t *val = nullptr, *val2 = nullptr, *flag = nullptr, *pos = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&key, sizeof(uint64_t) * tot));
+  RK_CUDA_TRY(cudaMalloc(&key2, sizeof(uint64_t) * tot));
+  RK_CUDA_TRY(cudaMalloc(&val, sizeof(int32_t) * tot));
+  RK_CUDA_TRY(cudaMalloc(&val2, sizeof(int32_t) * tot));
+  RK_CUDA_TRY(cudaMalloc(&flag, sizeof(int32_t) * tot));
+  RK_CUDA_TRY(cudaMalloc(&pos, sizeof(int32_t) * tot));
+  RK_CUDA_TRY(cudaMalloc(&s->ent_w, sizeof(int32_t) * tot));
+  RK_CUDA_TRY(cudaMalloc(&s->ent_c, sizeof(int32_t) * tot));
+  const int grid = (int)std::min<int64_t>(ceil_div(tot, 256), 148 * 32);
+  ent_gen_kernel<<<grid, 256>>>(s->bsort, s->n, s->M, s->bs, s->M1, key, val);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  const uint64_t maxkey = (uint64_t)s->M1 * s->M2 * s->bs;
+  int end_bit = 1;
+  while (end_bit < 63 && ((uint64_t)1 << end_bit) <= maxkey) ++end_bit;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, val, val2, (int)tot, 0, end_bit);
+  void* tmp = nullptr;
+  size_t tb2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag, pos, (int)tot);
+  RK_CUDA_TRY(cudaMalloc(&tmp, std::max(tb, tb2) + 16));
+  RK_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, val, val2, (int)tot, 0, end_bit));
+  count_launch();
+  ent_fin_kernel<<<grid, 256>>>(key2, val2, s->perm, tot, s->M, s->bs, s->ent_w, s->ent_c, flag);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  RK_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb2, flag, pos, (int)tot));
+  count_launch();
+  int32_t last_pos = 0, last_flag = 0;
+  RK_CUDA_TRY(cudaMemcpy(&last_pos, pos + tot - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  RK_CUDA_TRY(cudaMemcpy(&last_flag, flag + tot - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  s->nnodes = (int64_t)last_pos + last_flag;
+  RK_CUDA_TRY(cudaMalloc(&s->node_q, sizeof(int32_t) * (s->nnodes + 1)));
+  RK_CUDA_TRY(cudaMalloc(&s->node_off, sizeof(int32_t) * (s->nnodes + 1)));
+  RK_CUDA_TRY(cudaMalloc(&s->row_node, sizeof(int32_t) * (s->M2 + 1)));
+  node_fill_kernel<<<grid, 256>>>(key2, flag, pos, tot, s->bs, s->node_q, s->node_off);
+  count_launch();
+  const int32_t end = (int32_t)tot;
+  RK_CUDA_TRY(cudaMemcpy(s->node_off + s->nnodes, &end, sizeof(int32_t), cudaMemcpyHostToDevice));
+  row_node_kernel<<<(int)ceil_div(s->M2 + 1, 256), 256>>>(s->node_q, s->nnodes, s->M1, s->M2, s->row_node);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  RK_CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(tmp);
+  cudaFree(key);
+  cudaFree(key2);
+  cudaFree(val);
+  cudaFree(val2);
+  cudaFree(flag);
+  cudaFree(pos);
+  return Status::ok();
+}
+
 static void free_setup(rk_setup* s) {
   if (!s) return;
   free_workspaces(s);
@@ -428,6 +541,11 @@ static void free_setup(rk_setup* s) {
   cudaFree(s->bsort);
   cudaFree(s->wsort);
   cudaFree(s->cell_start);
+  cudaFree(s->node_q);
+  cudaFree(s->node_off);
+  cudaFree(s->row_node);
+  cudaFree(s->ent_w);
+  cudaFree(s->ent_c);
   cudaFree(s->spec_q);
   cudaFree(s->kn_chol_dev);
   cudaFree(s->emb.root_q);
@@ -584,6 +702,7 @@ static Status build_setup(const rk_model* model, const rk_grid* grid, int L, con
       s->weights, s->perm, s->wsort, n, M);
   count_launch();
   RK_LAUNCH_CHECK();
+  RK_TRY(build_sparse_gather(s));
 
   std::vector<double> cv(n);
   RK_CUDA_TRY(cudaMemcpy(cv.data(), s->cond_var, sizeof(double) * n, cudaMemcpyDeviceToHost));

@@ -83,6 +83,14 @@ struct rk_setup {
   int32_t* bsort = nullptr;     // sorted base keys
   double* wsort = nullptr;      // (n, M) sorted order
   int32_t* cell_start = nullptr;  // (M1*M2 + 1) lower bounds of base keys
+  // sparse gather plan (fixed per observation layout): active padded nodes, each with its
+  // contributions (index into wsort, original obs index) in the order dy asc, sorted j asc
+  int64_t nnodes = 0;
+  int32_t* node_q = nullptr;      // (nnodes) flat padded node index, ascending
+  int32_t* node_off = nullptr;    // (nnodes + 1) offsets into ent_w / ent_c
+  int32_t* row_node = nullptr;    // (M2 + 1) first active node of each padded row
+  int32_t* ent_w = nullptr;       // (n M) index into wsort
+  int32_t* ent_c = nullptr;       // (n M) original observation index (into c)
   double* spec_q = nullptr;     // (H1, Q2): Re fft2(filter)[ky, kx] / (p1 p2), ky <= p2/2
   double* kn_chol_dev = nullptr;  // (M, M) row-major lower
   std::vector<double> kn_chol, kn_inv;

@@ -504,19 +504,116 @@ static GatherSrc gather_src(const rk_setup* s, const double* c, int64_t c_stride
   return g;
 }
 
+// Tiled gather: a CTA owns TY x TX nodes (one warp per row, 4 columns per lane) and first
+// stages the tile's window of cell_start (base rows y0-BS+1 .. y0+TY-1, base columns
+// x0-BS+1 .. x0+TX) in shared memory, so each node's 2 BS range lookups are smem reads.
+// Accumulation order per node is the same as cstar_at (dy ascending, sorted j ascending).
+constexpr int CS_TY = 8, CS_TX = 128;
+
+template <int BS>
+__global__ void __launch_bounds__(256) cstar_tile_kernel(GatherSrc g, double* __restrict__ out,
+                                                         int64_t ldo, int64_t out_bstride) {
+  constexpr int RW = CS_TY + BS - 1, CW = CS_TX + BS;
+  __shared__ int cs[RW][CW];
+  const int b = blockIdx.z;
+  const double* c = g.c + (int64_t)b * g.c_stride;
+  double* o = out + (int64_t)b * out_bstride;
+  const int x0 = blockIdx.x * CS_TX, y0 = blockIdx.y * CS_TY;
+  const int by_lo = y0 - BS + 1, bx_lo = x0 - BS + 1;
+  const int nbase = g.M1 * g.M2;
+  for (int e = threadIdx.x; e < RW * CW; e += blockDim.x) {
+    const int r = e / CW, q = e % CW;
+    const int by = by_lo + r, bx = bx_lo + q;
+    int v = 0;
+    if (by >= 0 && by <= g.M2 - BS && bx >= 0)
+      v = __ldg(&g.cell_start[min(by * g.M1 + min(bx, g.M1), nbase)]);
+    cs[r][q] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int y = y0 + warp;
+  if (y >= g.M2) return;
+#pragma unroll
+  for (int k = 0; k < CS_TX / 32; ++k) {
+    const int x = x0 + lane + 32 * k;
+    if (x >= g.M1) continue;
+    const int xlo = max(0, x - BS + 1), xhi = min(x, g.M1 - BS);
+    double acc = 0.0;
+    if (xlo <= xhi) {
+#pragma unroll
+      for (int dy = 0; dy < BS; ++dy) {
+        const int by = y - dy;
+        if (by < 0 || by > g.M2 - BS) continue;
+        const int r = by - by_lo;
+        const int j0 = cs[r][xlo - bx_lo], j1 = cs[r][xhi + 1 - bx_lo];
+        const int rowb = by * g.M1;
+        for (int j = j0; j < j1; ++j) {
+          const int bx = __ldg(&g.bsort[j]) - rowb;
+          const double w = __ldg(&g.wsort[(int64_t)j * g.M + dy * BS + (x - bx)]);
+          const double cj = __ldg(&c[__ldg(&g.perm[j])]);
+          acc = __dadd_rn(acc, __dmul_rn(w, cj));
+        }
+      }
+    }
+    o[(int64_t)y * ldo + x] = acc;
+  }
+}
+
+// Sparse gather: one CTA per padded row; the row is zero-filled in smem, every active node of
+// the row sums its precomputed contributions (fixed order -> bitwise reproducible, identical
+// to cstar_at), then the row is written out coalesced.  Work ~ n M + G instead of G (2L)^2
+// range tests.
+struct SparseSrc {
+  const int32_t* node_q;
+  const int32_t* node_off;
+  const int32_t* row_node;
+  const int32_t* ent_w;
+  const int32_t* ent_c;
+  const double* wsort;
+  const double* c;
+  int64_t c_stride;
+  int M1;
+};
+
+__global__ void __launch_bounds__(256) cstar_rows_kernel(SparseSrc g, double* __restrict__ out,
+                                                         int64_t ldo, int64_t out_bstride) {
+  extern __shared__ __align__(16) double rowbuf[];
+  const int y = blockIdx.x, b = blockIdx.y;
+  const double* c = g.c + (int64_t)b * g.c_stride;
+  for (int x = threadIdx.x; x < g.M1; x += blockDim.x) rowbuf[x] = 0.0;
+  __syncthreads();
+  const int a0 = __ldg(&g.row_node[y]), a1 = __ldg(&g.row_node[y + 1]);
+  const int rowq = y * g.M1;
+  for (int a = a0 + threadIdx.x; a < a1; a += blockDim.x) {
+    const int e0 = __ldg(&g.node_off[a]), e1 = __ldg(&g.node_off[a + 1]);
+    double acc = 0.0;
+    for (int e = e0; e < e1; ++e) {
+      const double w = __ldg(&g.wsort[__ldg(&g.ent_w[e])]);
+      const double cj = __ldg(&c[__ldg(&g.ent_c[e])]);
+      acc = __dadd_rn(acc, __dmul_rn(w, cj));   // (w * c) then add, as np.add.at
+    }
+    rowbuf[__ldg(&g.node_q[a]) - rowq] = acc;
+  }
+  __syncthreads();
+  double* o = out + (int64_t)b * out_bstride + (int64_t)y * ldo;
+  for (int x = threadIdx.x; x < g.M1; x += blockDim.x) o[x] = rowbuf[x];
+}
+
 static Status launch_cstar(const rk_setup* s, const double* c, int64_t c_stride, double* out,
                            int64_t ldo, int batch, cudaStream_t st) {
-  const GatherSrc g = gather_src(s, c, c_stride);
-  const int64_t tot = (int64_t)s->M1 * s->M2;
-  const dim3 grid((unsigned)std::min<int64_t>(ceil_div(tot, 256), 148 * 16), (unsigned)batch);
-  const int64_t bstr = ldo * s->M2;
-  switch (s->bs) {
-    case 2: cstar_kernel<2><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
-    case 4: cstar_kernel<4><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
-    case 6: cstar_kernel<6><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
-    case 8: cstar_kernel<8><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
-    default: cstar_kernel<0><<<grid, 256, 0, st>>>(g, out, ldo, bstr); break;
-  }
+  SparseSrc g;
+  g.node_q = s->node_q;
+  g.node_off = s->node_off;
+  g.row_node = s->row_node;
+  g.ent_w = s->ent_w;
+  g.ent_c = s->ent_c;
+  g.wsort = s->wsort;
+  g.c = c;
+  g.c_stride = c_stride;
+  g.M1 = s->M1;
+  const size_t smem = sizeof(double) * (size_t)s->M1;
+  RK_TRY(set_smem_attr((const void*)cstar_rows_kernel, smem));
+  cstar_rows_kernel<<<dim3((unsigned)s->M2, (unsigned)batch), 256, smem, st>>>(g, out, ldo, ldo * s->M2);
   count_launch();
   RK_LAUNCH_CHECK();
   return Status::ok();
