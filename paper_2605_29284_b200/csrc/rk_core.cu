@@ -76,13 +76,32 @@ Status plan_for(int n, FftPlan* out) {
   return Status::ok();
 }
 
+// FFT kernels run at 128 registers/thread (__launch_bounds__(512, 1)), so an SM holds at
+// most 512 of their threads; pick the lines-per-CTA that maximises resident threads under
+// that and the shared-memory limit (line buffers + ~1/8 for twiddles/staging), preferring
+// more lines per CTA on ties (wider coalesced transposed I/O), and never packing so much
+// that the launch has fewer than 2 CTAs per SM.
 int pick_lpc(const FftPlan& pl, int max_lines, int64_t total_lines) {
   const size_t line_bytes = (size_t)pl.n * sizeof(double2);
-  int lpc = std::max(1, max_lines);
-  while (lpc > 1 && ((size_t)lpc * line_bytes > 96 * 1024 || lpc * pl.nthr > 512 ||
-                     ceil_div(total_lines, lpc) < 2 * 148))
-    --lpc;
-  return lpc;
+  static const size_t cap = [] {
+    const char* e = getenv("RK_LPC_SMEM_KB");
+    return (size_t)(e ? atoi(e) : 112) * 1024;
+  }();
+  int best = 1;
+  int64_t best_res = -1;
+  for (int lpc = 1; lpc <= std::max(1, max_lines); ++lpc) {
+    const int threads = lpc * pl.nthr;
+    const size_t smem = lpc * line_bytes + line_bytes / 8 + 64;
+    if (threads > 512 || (lpc > 1 && (smem > cap || ceil_div(total_lines, lpc) < 2 * 148))) break;
+    const int by_regs = 512 / threads;
+    const int by_smem = (int)((227 * 1024) / smem);
+    const int64_t res = (int64_t)std::min(by_regs, by_smem) * threads;
+    if (res >= best_res) {
+      best_res = res;
+      best = lpc;
+    }
+  }
+  return best;
 }
 
 Status set_smem_attr(const void* fn, size_t bytes) {

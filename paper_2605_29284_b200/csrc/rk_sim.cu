@@ -112,15 +112,20 @@ __global__ void __launch_bounds__(512, 1) cs_row_kernel(const CsRowArgs a) {
     for (int part = 0; part < 2; ++part) {
       const uint64_t w0 = wb + (part ? Ps : 0);
       const uint64_t b0 = w0 / 4, b1 = (w0 + (uint64_t)a.ps1 - 1) / 4;
-      for (uint64_t blk = b0 + tl; blk <= b1; blk += nthr) {
-        uint64_t o[4];
+      // two independent Philox blocks (8 normals) per iteration for ILP
+      for (uint64_t blk = b0 + tl; blk <= b1; blk += 2 * (uint64_t)nthr) {
+        const uint64_t blk2 = blk + nthr;
+        uint64_t o[8];
         philox4x64_10(blk + 1, fs, 0, o);
+        philox4x64_10(blk2 + 1, fs, 0, o + 4);
+        double z[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint64_t w = blk * 4 + q;
-          if (w >= w0 && w < w0 + (uint64_t)a.ps1) {
-            const double z = word_normal(o[q]);
-            if (part) buf[w - w0].y = z; else buf[w - w0].x = z;
+        for (int q = 0; q < 8; ++q) z[q] = word_normal(o[q]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint64_t w = (q < 4 ? blk : blk2) * 4 + (q & 3);
+          if ((q < 4 || blk2 <= b1) && w >= w0 && w < w0 + (uint64_t)a.ps1) {
+            if (part) buf[w - w0].y = z[q]; else buf[w - w0].x = z[q];
           }
         }
       }
@@ -308,6 +313,98 @@ Status ensure_embedding(rk_setup* s, cudaStream_t st) {
   return Status::err(RK_NUMERIC, b);
 }
 
+// CS pass A, part 1 (high occupancy): the 2 Ps normals of each realization (Philox words
+// [0, Ps) real, [Ps, 2 Ps) imaginary, row-major over (ps2, ps1); simulate.py:113-116) scaled by
+// sqrt(lambda) sqrt(P)/P, written as complex Z[p] (64-byte coalesced stores per thread).
+struct CsRngArgs {
+  uint64_t seed;
+  int64_t j0;
+  int direct;
+  int ps1, ps2;
+  const double* root_q;
+  int rq_ld;
+  double2* Z;                // (batch, ps2, ps1)
+  int64_t Z_bstride;
+};
+
+__global__ void __launch_bounds__(256) cs_rng_kernel(const CsRngArgs a) {
+  const int b = blockIdx.y;
+  const uint64_t fs = a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
+  const uint64_t Ps = (uint64_t)a.ps1 * (uint64_t)a.ps2;
+  const uint64_t nblk = (Ps + 3) / 4;
+  const int imoff = (int)(Ps & 3);
+  double2* Z = a.Z + (int64_t)b * a.Z_bstride;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nblk;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t re[4], im[8];
+    philox4x64_10(t + 1, fs, 0, re);
+    const uint64_t ib = (Ps + 4 * t) / 4;            // first block holding imaginary words
+    philox4x64_10(ib + 1, fs, 0, im);
+    if (imoff) philox4x64_10(ib + 2, fs, 0, im + 4);
+    uint64_t p = 4 * t;
+    int iy = (int)(p / a.ps1), ix = (int)(p - (uint64_t)iy * a.ps1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q, ++p) {
+      if (p < Ps) {
+        const double zr = word_normal(re[q]);
+        const double zi = word_normal(im[imoff + q]);
+        const double r = __ldg(&a.root_q[(int64_t)min(iy, a.ps2 - iy) * a.rq_ld + min(ix, a.ps1 - ix)]);
+        Z[p] = make_double2(r * zr, r * zi);
+      }
+      if (++ix == a.ps1) { ix = 0; ++iy; }
+    }
+  }
+}
+
+// CS pass A, part 2: TMA bulk load of each row of Z, inverse FFT along x, keep the M1
+// columns, write V[ix][iy] (transposed for the column pass).
+struct CsFftArgs {
+  FftPlan pl;
+  int lpc;
+  int ps2;
+  int keep;                  // M1
+  const double2* Z;
+  int64_t Z_bstride;
+  double2* V;
+  int64_t ldV, V_bstride;
+  int tw_off;
+};
+
+__global__ void __launch_bounds__(512, 1) cs_rowfft_kernel(const CsFftArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int n = a.pl.n;
+  const int nthr = a.pl.nthr;
+  const int line = threadIdx.x / nthr;
+  const int tl = threadIdx.x - line * nthr;
+  const int b = blockIdx.y;
+  double2* buf = smem + (size_t)line * n;
+  uint64_t* bar = (uint64_t*)(smem + (size_t)a.lpc * n);
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nv = 0;
+    for (int l = 0; l < a.lpc; ++l) nv += (blockIdx.x * a.lpc + l) < a.ps2;
+    mbar_expect_tx(bar, (uint32_t)nv * (uint32_t)n * 16u);
+    const double2* Zb = a.Z + (int64_t)b * a.Z_bstride;
+    for (int l = 0; l < a.lpc; ++l) {
+      const int iy = blockIdx.x * a.lpc + l;
+      if (iy < a.ps2) bulk_g2s(smem + (size_t)l * n, Zb + (int64_t)iy * n, (uint32_t)n * 16u, bar);
+    }
+  }
+  if (blockIdx.x * a.lpc + line >= a.ps2)
+    for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
+  mbar_wait(bar, 0);
+  __syncthreads();
+  fft_line<true, true>(buf, pls, tl);
+  double2* V = a.V + (int64_t)b * a.V_bstride;
+  for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
+    const int l = idx % a.lpc, ix = idx / a.lpc;
+    const int row = blockIdx.x * a.lpc + l;
+    if (row < a.ps2) V[(int64_t)ix * a.ldV + row] = smem[(size_t)l * n + ix];
+  }
+}
+
 static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, int batch,
                             double* g, cudaStream_t st) {
   RK_TRY(ensure_embedding(s, st));
@@ -315,28 +412,42 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   const int64_t ldV = (e.ps2 + 1) & ~1;
   double2* V = nullptr;
   RK_TRY(scratch_alloc((void**)&V, sizeof(double2) * (size_t)s->M1 * ldV * batch, st));
-  CsRowArgs ra{};
-  ra.pl = e.pl1;
-  ra.lpc = pick_lpc(e.pl1, 4, (int64_t)e.ps2 * batch);
-  ra.ps1 = e.ps1;
-  ra.ps2 = e.ps2;
-  ra.keep = s->M1;
-  ra.root_q = e.root_q;
-  ra.rq_ld = e.hs1;
-  ra.seed = seed;
-  ra.j0 = j0;
-  ra.direct = direct;
-  ra.V = V;
-  ra.ldV = ldV;
-  ra.V_bstride = (int64_t)s->M1 * ldV;
   {
-    const dim3 grid((unsigned)ceil_div(e.ps2, ra.lpc), (unsigned)batch);
-    ra.tw_off = (int)(ra.lpc * (size_t)e.ps1);
-    const size_t smem = sizeof(double2) * (e.ps1 * (size_t)ra.lpc + e.pl1.ntw);
-    RK_TRY(set_smem_attr((const void*)cs_row_kernel, smem));
-    cs_row_kernel<<<grid, ra.lpc * e.pl1.nthr, smem, st>>>(ra);
+    const int64_t Ps = (int64_t)e.ps1 * e.ps2;
+    double2* Z = nullptr;
+    RK_TRY(scratch_alloc((void**)&Z, sizeof(double2) * (size_t)Ps * batch, st));
+    CsRngArgs ga{};
+    ga.seed = seed;
+    ga.j0 = j0;
+    ga.direct = direct;
+    ga.ps1 = e.ps1;
+    ga.ps2 = e.ps2;
+    ga.root_q = e.root_q;
+    ga.rq_ld = e.hs1;
+    ga.Z = Z;
+    ga.Z_bstride = Ps;
+    const dim3 rgrid((unsigned)std::min<int64_t>(ceil_div(ceil_div(Ps, 4), 256), 148 * 8), (unsigned)batch);
+    cs_rng_kernel<<<rgrid, 256, 0, st>>>(ga);
     count_launch();
     RK_LAUNCH_CHECK();
+    CsFftArgs fa{};
+    fa.pl = e.pl1;
+    fa.lpc = pick_lpc(e.pl1, 4, (int64_t)e.ps2 * batch);
+    fa.ps2 = e.ps2;
+    fa.keep = s->M1;
+    fa.Z = Z;
+    fa.Z_bstride = Ps;
+    fa.V = V;
+    fa.ldV = ldV;
+    fa.V_bstride = (int64_t)s->M1 * ldV;
+    const dim3 grid((unsigned)ceil_div(e.ps2, fa.lpc), (unsigned)batch);
+    fa.tw_off = (int)(fa.lpc * (size_t)e.ps1) + 1;
+    const size_t smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1 + e.pl1.ntw);
+    RK_TRY(set_smem_attr((const void*)cs_rowfft_kernel, smem));
+    cs_rowfft_kernel<<<grid, fa.lpc * e.pl1.nthr, smem, st>>>(fa);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    scratch_free(Z, st);
   }
   CsColArgs ca{};
   ca.pl = e.pl2;
@@ -345,7 +456,7 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   ca.keep = s->M2;
   ca.V = V;
   ca.ldV = ldV;
-  ca.V_bstride = ra.V_bstride;
+  ca.V_bstride = (int64_t)s->M1 * ldV;
   ca.g = g;
   ca.g_bstride = (int64_t)s->M1 * s->M2;
   {
@@ -844,7 +955,11 @@ rk_status rk_ensemble_accumulate(rk_setup* s, const rk_fit* f, uint64_t seed, in
     if (!xg_dev && f->p != 1)
       return Status::err(RK_DOMAIN, "grid covariates are required when beta_hat has more than one entry");
     RK_TRY(ensure_embedding(s, st));
-    const int B = std::max(1, (int)batch);
+    // realizations per device pass, capped so the per-pass scratch (Z, V, T, U, g, e) stays
+    // within ~8 GB (a 8748^2 torus needs ~1.2 GB of Z per realization)
+    const double per_real = 16.0 * ((double)s->emb.ps1 * s->emb.ps2 + (double)s->M1 * s->emb.ps2 +
+                                    2.0 * s->H1 * s->M2) + 16.0 * (double)s->M1 * s->M2;
+    const int B = std::max(1, std::min((int)batch, (int)(8.0e9 / per_real)));
     const int64_t npix = (int64_t)s->m1 * s->m2;
     double *G = nullptr, *Z = nullptr, *C = nullptr, *BT = nullptr, *E = nullptr;
     RK_TRY(scratch_alloc((void**)&G, sizeof(double) * (size_t)s->M1 * s->M2 * B, st));
