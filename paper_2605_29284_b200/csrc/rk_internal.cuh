@@ -59,7 +59,26 @@ struct Workspace {
   cudaStream_t cap = nullptr;   // private stream used only for graph capture
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, int> seen;
+  // host-buffer path: X_g upload on a side stream, chunk by chunk, overlapped with the
+  // gather / FFT passes; graphs keyed by the (pinned) host pointers
+  static constexpr int kMaxChunks = 8;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t xev[kMaxChunks] = {};
+  double* beta_h = nullptr;     // pinned copy of beta (16)
+  std::map<GraphKey, cudaGraphExec_t> hgraphs;
+  std::map<GraphKey, int> hseen;
 };
+
+// Host-buffer predict: pass 3 runs in `chunks` row blocks; block k waits for xev[k] (its
+// covariate rows uploaded on the side stream) and its field rows are copied to out_host
+// right after it, so PCIe traffic in both directions overlaps the kernels.
+struct HostIo {
+  int chunks = 1;
+  const cudaEvent_t* xev = nullptr;
+  double* out_host = nullptr;
+};
+int chunk_rows(int nrows, int chunks);   // rows per block (even)
 
 }  // namespace rk
 
@@ -132,7 +151,7 @@ struct PredictBatch {
   double* out = nullptr;          // (batch, m2, m1): field, or e = interior(g) - field in CS mode
 };
 Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st,
-                     cudaEvent_t* ev = nullptr, Workspace* ws = nullptr);
+                     cudaEvent_t* ev = nullptr, Workspace* ws = nullptr, const HostIo* hio = nullptr);
 void free_workspaces(rk_setup* s);
 
 // CS pieces (rk_sim.cu)

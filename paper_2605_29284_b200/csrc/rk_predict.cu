@@ -16,6 +16,7 @@
 //   build_filter_spectrum 72-86 -> spectrum_quarter(): lag table on the quarter torus,
 //       pass 1 (lag mode) + pass 2 (spectrum mode, real part of ky <= p2/2)
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <mutex>
 
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
   const int yb = ya + 1;
   const bool va = ya < a.nrows, vb = yb < a.nrows;
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  pdl_wait();   // everything below reads the predecessor's output
   if (SRC == SRC_ROWS) {
     const double* rin = a.rows + (int64_t)b * a.in_bstride;
     // staging of the two real rows: tma == 2 puts them in the zero-pad tail of the line
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
   }
   __syncthreads();
   fft_line<false, true>(buf, pls, tl);
+  pdl_trigger();   // the column pass may start staging while the split rows are stored
   // split Z = FFT(u + i v) into U = (Z + conj Z[-k]) / 2, V = (Z - conj Z[-k]) / 2i
   const int nr = 2 * a.lpc;
   const int H = n / 2 + 1;
@@ -231,19 +234,24 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
   const double2* Tb = a.T + (int64_t)b * a.T_bstride;
   if (threadIdx.x == 0) mbar_init(bar, 1);
   __syncthreads();
+  const uint32_t colb = (uint32_t)a.nin * 16u;
   if (threadIdx.x == 0) {
     int nv = 0;
     for (int l = 0; l < a.lpc; ++l) nv += (blockIdx.x * a.lpc + l) < a.ncols;
-    const uint32_t colb = (uint32_t)a.nin * 16u;
     const uint32_t specb = MODE == 0 ? (uint32_t)a.ldq * 8u : 0u;
     mbar_expect_tx(bar, (uint32_t)nv * (colb + specb));
+    if (MODE == 0)
+      for (int l = 0; l < a.lpc; ++l) {
+        const int k = blockIdx.x * a.lpc + l;
+        if (k < a.ncols) bulk_g2s(specs + (size_t)l * a.ldq, a.spec_q + (int64_t)k * a.ldq, specb, bar);
+      }
+  }
+  pdl_wait();   // T is the predecessor's output
+  if (threadIdx.x == 0)
     for (int l = 0; l < a.lpc; ++l) {
       const int k = blockIdx.x * a.lpc + l;
-      if (k >= a.ncols) continue;
-      bulk_g2s(smem + (size_t)l * n, Tb + (int64_t)k * a.ldT, colb, bar);
-      if (MODE == 0) bulk_g2s(specs + (size_t)l * a.ldq, a.spec_q + (int64_t)k * a.ldq, specb, bar);
+      if (k < a.ncols) bulk_g2s(smem + (size_t)l * n, Tb + (int64_t)k * a.ldT, colb, bar);
     }
-  }
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   for (int y = a.nin + tl; y < n; y += nthr) buf[y] = make_double2(0.0, 0.0);
   if (!valid)
@@ -256,6 +264,7 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     __syncthreads();
     fft_line<true, true>(buf, pls, tl);
+    pdl_trigger();
     // TMA bulk store of the kept rows
     fence_async_smem();
     __syncthreads();
@@ -294,6 +303,7 @@ struct RowInvArgs {
   int64_t g_bstride;
   int g_ld, g_row0, g_col0;
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
+  int ep_off;                // smem offset (double2 units) of the prefetched epilogue operands
 };
 
 __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
@@ -306,10 +316,28 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   const int H = n / 2 + 1;
   const double2* U = a.U + (int64_t)b * a.U_bstride;
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  // prefetch the epilogue operands of every line's two rows (covariates X_g, CS field g)
+  // with async copies; they land while the U rows are gathered and transformed
+  const int pc = a.epi == EPI_COV ? a.p : 0;
+  const int hasg = a.g ? 1 : 0;
+  double* ep = (double*)(smem + a.ep_off);
+  const double* gb = a.g ? a.g + (int64_t)b * a.g_bstride : nullptr;
+  if (pc + hasg) {
+    const int per_row = a.ncols * (pc + hasg);
+    for (int e = threadIdx.x; e < a.lpc * 2 * per_row; e += blockDim.x) {
+      const int lr = e / per_row, r = e - lr * per_row;     // lr = 2 l + which
+      const int y = 2 * blockIdx.x * a.lpc + lr;
+      if (y >= a.nrows) continue;
+      const double* src = r < a.ncols * pc ? a.xg + (int64_t)y * a.ncols * pc + r
+                                           : gb + (int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + (r - a.ncols * pc);
+      cp_async8(ep + e, src);
+    }
+  }
+  pdl_wait();   // U is the predecessor's output
   // strided gather of both rows of every line (Z[k] = A[k] + i B[k], Hermitian upper half),
-  // batched 4 deep per thread for memory-level parallelism
+  // batched 8 deep per thread for memory-level parallelism
   const int tot = a.lpc * H;
-  constexpr int D = 4;
+  constexpr int D = 8;
   for (int base = threadIdx.x; base < tot; base += D * blockDim.x) {
     double2 A[D], B[D];
 #pragma unroll
@@ -335,13 +363,14 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
       }
     }
   }
+  cp_async_wait_all();
   __syncthreads();
   double2* buf = smem + (size_t)line * n;
   fft_line<true, true>(buf, pls, tl);
   const int ya = 2 * (blockIdx.x * a.lpc + line);
   const double* beta = a.beta ? a.beta + (int64_t)b * a.p : nullptr;
   double* out = a.out + (int64_t)b * a.out_bstride;
-  const double* gb = a.g ? a.g + (int64_t)b * a.g_bstride : nullptr;
+  const int per_row = a.ncols * (pc + hasg);
   for (int e = tl; e < 2 * a.ncols; e += nthr) {
     const int which = e >= a.ncols;
     const int x = e - which * a.ncols;
@@ -349,15 +378,16 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
     if (y >= a.nrows) continue;
     const double2 z = buf[a.col0 + x];
     double v = which ? z.y : z.x;
+    const double* er = ep + (2 * line + which) * per_row;
     if (a.epi == EPI_SCALAR) {
       v = v + beta[0];
     } else if (a.epi == EPI_COV) {
-      const double* xr = a.xg + ((int64_t)y * a.ncols + x) * a.p;
+      const double* xr = er + x * pc;
       double fx = 0.0;
-      for (int q = 0; q < a.p; ++q) fx = fma(xr[q], beta[q], fx);
+      for (int q = 0; q < pc; ++q) fx = fma(xr[q], beta[q], fx);
       v = v + fx;
     }
-    if (gb) v = gb[(int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + x] - v;
+    if (gb) v = er[a.ncols * pc + x] - v;
     out[(int64_t)y * a.ldo + x] = v;
   }
 }
@@ -380,10 +410,10 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStrea
   smem = with_tw(smem, a.pl);
   if (src == SRC_ROWS) {
     RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_ROWS>, smem));
-    row_fwd_kernel<SRC_ROWS><<<grid, threads, smem, st>>>(a);
+    RK_CUDA_TRY(launch_pdl(row_fwd_kernel<SRC_ROWS>, grid, dim3(threads), smem, st, a));
   } else {
     RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_LAG>, smem));
-    row_fwd_kernel<SRC_LAG><<<grid, threads, smem, st>>>(a);
+    RK_CUDA_TRY(launch_pdl(row_fwd_kernel<SRC_LAG>, grid, dim3(threads), smem, st, a));
   }
   count_launch();
   RK_LAUNCH_CHECK();
@@ -400,10 +430,10 @@ static Status launch_col(int mode, const ColArgs& a0, int batch, cudaStream_t st
   smem = with_tw(smem, a.pl);
   if (mode == 0) {
     RK_TRY(set_smem_attr((const void*)col_kernel<0>, smem));
-    col_kernel<0><<<grid, threads, smem, st>>>(a);
+    RK_CUDA_TRY(launch_pdl(col_kernel<0>, grid, dim3(threads), smem, st, a));
   } else {
     RK_TRY(set_smem_attr((const void*)col_kernel<1>, smem));
-    col_kernel<1><<<grid, threads, smem, st>>>(a);
+    RK_CUDA_TRY(launch_pdl(col_kernel<1>, grid, dim3(threads), smem, st, a));
   }
   count_launch();
   RK_LAUNCH_CHECK();
@@ -415,10 +445,13 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
   const int pairs = (a.nrows + 1) / 2;
   const dim3 grid((unsigned)ceil_div(pairs, a.lpc), (unsigned)batch);
   size_t smem = sizeof(double2) * a.pl.n * a.lpc;
+  a.ep_off = tw_slot(smem);
+  const int pc = a.epi == EPI_COV ? a.p : 0;
+  smem = (size_t)a.ep_off * 16 + sizeof(double) * (size_t)a.lpc * 2 * a.ncols * (pc + (a.g ? 1 : 0));
   a.tw_off = tw_slot(smem);
   smem = with_tw(smem, a.pl);
   RK_TRY(set_smem_attr((const void*)row_inv_kernel, smem));
-  row_inv_kernel<<<grid, a.lpc * a.pl.nthr, smem, st>>>(a);
+  RK_CUDA_TRY(launch_pdl(row_inv_kernel, grid, dim3(a.lpc * a.pl.nthr), smem, st, a));
   count_launch();
   RK_LAUNCH_CHECK();
   return Status::ok();
@@ -594,6 +627,7 @@ __global__ void __launch_bounds__(256) cstar_rows_kernel(SparseSrc g, double* __
     }
     rowbuf[__ldg(&g.node_q[a]) - rowq] = acc;
   }
+  pdl_trigger();   // the row-FFT pass may stage its twiddles while the rows are stored
   __syncthreads();
   double* o = out + (int64_t)b * out_bstride + (int64_t)y * ldo;
   for (int x = threadIdx.x; x < g.M1; x += blockDim.x) o[x] = rowbuf[x];
@@ -625,7 +659,8 @@ static inline int64_t round_even(int64_t v) { return (v + 1) & ~int64_t(1); }
 // (c* or a caller field); output rows [row0, row0 + nout) x cols [col0, col0 + ncols).
 static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in, int64_t in_bstride,
                             int batch, int row0, int nout, int col0, int ncols, const RowInvArgs& epi,
-                            cudaStream_t st, cudaEvent_t* ev = nullptr, Workspace* ws = nullptr) {
+                            cudaStream_t st, cudaEvent_t* ev = nullptr, Workspace* ws = nullptr,
+                            const HostIo* hio = nullptr) {
   const int64_t ldT = round_even(s->M2);
   const int64_t ldU = round_even(nout);
   double2 *T = nullptr, *U = nullptr;
@@ -680,7 +715,26 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   ia.U_bstride = ca.U_bstride;
   ia.col0 = col0;
   ia.ncols = ncols;
-  RK_TRY(launch_row_inv(ia, batch, st));
+  if (!hio) {
+    RK_TRY(launch_row_inv(ia, batch, st));
+  } else {   // batch == 1: row blocks, each followed by its device -> host copy
+    const int per = chunk_rows(nout, hio->chunks);
+    for (int k = 0, r0 = 0; r0 < nout; ++k, r0 += per) {
+      const int r1 = std::min(nout, r0 + per);
+      RowInvArgs ck = ia;
+      ck.nrows = r1 - r0;
+      ck.U = U + r0;
+      ck.out = ia.out + (int64_t)r0 * ia.ldo;
+      if (ck.xg) ck.xg = ia.xg + (int64_t)r0 * ncols * ia.p;
+      ck.g_row0 = ia.g_row0 + r0;
+      ck.lpc = pick_lpc(s->pl1, 4, (int64_t)((ck.nrows + 1) / 2));
+      if (hio->xev) RK_CUDA_TRY(cudaStreamWaitEvent(st, hio->xev[k], 0));
+      RK_TRY(launch_row_inv(ck, 1, st));
+      if (hio->out_host)
+        RK_CUDA_TRY(cudaMemcpyAsync(hio->out_host + (int64_t)r0 * ia.ldo, ck.out,
+                                    sizeof(double) * (size_t)(r1 - r0) * ia.ldo, cudaMemcpyDeviceToHost, st));
+    }
+  }
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[4], st));
   if (own) {
     scratch_free(T, st);
@@ -689,8 +743,13 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   return Status::ok();
 }
 
+int chunk_rows(int nrows, int chunks) {
+  const int per = (int)ceil_div(nrows, std::max(chunks, 1));
+  return std::max(2, per + (per & 1));
+}
+
 Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st, cudaEvent_t* ev,
-                     Workspace* ws) {
+                     Workspace* ws, const HostIo* hio) {
   RowInvArgs e{};
   e.out = pb.out;
   e.ldo = s->m1;
@@ -712,7 +771,7 @@ Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st,
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[0], st));
   RK_TRY(launch_cstar(s, pb.c, pb.c_stride, cstar, ldc, pb.batch, st));
   Status r = conv_pipeline(s, cstar, ldc, ldc * s->M2, pb.batch, s->grid.pad[2], s->m2,
-                           s->grid.pad[0], s->m1, e, st, ev, ws);
+                           s->grid.pad[0], s->m1, e, st, ev, ws, hio);
   if (own) scratch_free(cstar, st);
   return r;
 }
@@ -734,6 +793,10 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
   RK_CUDA_TRY(cudaMalloc(&w->beta_in, sizeof(double) * 16));
   RK_CUDA_TRY(cudaMalloc(&w->out, sizeof(double) * (size_t)s->m1 * s->m2));
   RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
+  RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->aux, cudaStreamNonBlocking));
+  RK_CUDA_TRY(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
+  for (auto& e : w->xev) RK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  RK_CUDA_TRY(cudaMallocHost(&w->beta_h, sizeof(double) * 16));
   s->ws[st] = w;
   *out = w;
   return Status::ok();
@@ -743,6 +806,12 @@ void free_workspaces(rk_setup* s) {
   for (auto& kv : s->ws) {
     Workspace* w = kv.second;
     for (auto& g : w->graphs) cudaGraphExecDestroy(g.second);
+    for (auto& g : w->hgraphs) cudaGraphExecDestroy(g.second);
+    if (w->aux) cudaStreamDestroy(w->aux);
+    if (w->fork) cudaEventDestroy(w->fork);
+    for (auto& e : w->xev)
+      if (e) cudaEventDestroy(e);
+    cudaFreeHost(w->beta_h);
     cudaFree(w->cstar);
     cudaFree(w->T);
     cudaFree(w->U);
@@ -799,6 +868,15 @@ static Status predict_graphed(rk_setup* s, Workspace* w, const PredictBatch& pb,
 }  // namespace rk
 
 using namespace rk;
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
 
 static int finish_status(const Status& s) {
   if (!s.good()) rk::set_error(s.code, s.msg);
@@ -928,17 +1006,18 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
     const int64_t N = (int64_t)s->m1 * s->m2;
     if (xg && w->xg_cap < (size_t)(N * p)) {
       std::lock_guard<std::mutex> lk(ms->ws_mu);
+      RK_CUDA_TRY(cudaStreamSynchronize(st));
       cudaFree(w->xg_in);
       for (auto& g : w->graphs) cudaGraphExecDestroy(g.second);   // keys held the old pointer
+      for (auto& g : w->hgraphs) cudaGraphExecDestroy(g.second);
       w->graphs.clear();
       w->seen.clear();
+      w->hgraphs.clear();
+      w->hseen.clear();
       w->xg_in = nullptr;
       RK_CUDA_TRY(cudaMalloc(&w->xg_in, sizeof(double) * N * p));
       w->xg_cap = (size_t)(N * p);
     }
-    RK_CUDA_TRY(cudaMemcpyAsync(w->c_in, c, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
-    if (beta) RK_CUDA_TRY(cudaMemcpyAsync(w->beta_in, beta, sizeof(double) * p, cudaMemcpyHostToDevice, st));
-    if (xg) RK_CUDA_TRY(cudaMemcpyAsync(w->xg_in, xg, sizeof(double) * N * p, cudaMemcpyHostToDevice, st));
     PredictBatch pb;
     pb.batch = 1;
     pb.c = w->c_in;
@@ -947,8 +1026,79 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
     pb.p = p;
     pb.xg = xg ? w->xg_in : nullptr;
     pb.out = w->out;
-    RK_TRY(predict_graphed(ms, w, pb, st));
-    RK_CUDA_TRY(cudaMemcpyAsync(out, w->out, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+    if (!(is_pinned(c) && is_pinned(out) && (!xg || is_pinned(xg)))) {
+      // pageable buffers: plain staged copies around the graphed device predict
+      RK_CUDA_TRY(cudaMemcpyAsync(w->c_in, c, sizeof(double) * s->n, cudaMemcpyHostToDevice, st));
+      if (beta) RK_CUDA_TRY(cudaMemcpyAsync(w->beta_in, beta, sizeof(double) * p, cudaMemcpyHostToDevice, st));
+      if (xg) RK_CUDA_TRY(cudaMemcpyAsync(w->xg_in, xg, sizeof(double) * N * p, cudaMemcpyHostToDevice, st));
+      RK_TRY(predict_graphed(ms, w, pb, st));
+      RK_CUDA_TRY(cudaMemcpyAsync(out, w->out, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+      RK_CUDA_TRY(cudaStreamSynchronize(st));
+      return Status::ok();
+    }
+    // pinned buffers: uploads, kernels and downloads in one graph; X_g rows go up on the
+    // side stream in row blocks that pass 3 consumes as they land
+    if (beta) memcpy(w->beta_h, beta, sizeof(double) * p);   // previous call has completed
+    // one block by default: on B200 (cfg2, 2.9 MB of X_g) the single side-stream upload
+    // hidden behind the gather / FFT passes measured 114 us per call; 2 / 4 / 8 row blocks
+    // 294 / 169 / 279 us (the interleaved small copies serialise on the copy engines)
+    static const int k_env = getenv("RK_HOST_CHUNKS") ? atoi(getenv("RK_HOST_CHUNKS")) : 1;
+    static const int graph_env = getenv("RK_HOST_GRAPH") ? atoi(getenv("RK_HOST_GRAPH")) : 1;
+    const int K = std::max(1, std::min(k_env, Workspace::kMaxChunks));
+    auto enqueue = [&](cudaStream_t q) -> Status {
+      RK_CUDA_TRY(cudaMemcpyAsync(w->c_in, c, sizeof(double) * s->n, cudaMemcpyHostToDevice, q));
+      if (beta) RK_CUDA_TRY(cudaMemcpyAsync(w->beta_in, w->beta_h, sizeof(double) * p, cudaMemcpyHostToDevice, q));
+      HostIo hio;
+      hio.chunks = K;
+      hio.out_host = out;
+      if (xg) {
+        RK_CUDA_TRY(cudaEventRecord(w->fork, q));
+        RK_CUDA_TRY(cudaStreamWaitEvent(w->aux, w->fork, 0));
+        const int per = chunk_rows(s->m2, K);
+        for (int k = 0, r0 = 0; r0 < s->m2; ++k, r0 += per) {
+          const int r1 = std::min(s->m2, r0 + per);
+          const size_t off = (size_t)r0 * s->m1 * p;
+          RK_CUDA_TRY(cudaMemcpyAsync(w->xg_in + off, xg + off, sizeof(double) * (size_t)(r1 - r0) * s->m1 * p,
+                                      cudaMemcpyHostToDevice, w->aux));
+          RK_CUDA_TRY(cudaEventRecord(w->xev[k], w->aux));
+        }
+        hio.xev = w->xev;
+      }
+      return predict_batch(s, pb, q, nullptr, w, &hio);
+    };
+    const GraphKey key{(uintptr_t)c, (uintptr_t)(beta ? 1 : 0), (uintptr_t)xg, (uintptr_t)out, p};
+    cudaGraphExec_t exec = nullptr;
+    bool capture = false;
+    {
+      std::lock_guard<std::mutex> lk(ms->ws_mu);
+      auto it = w->hgraphs.find(key);
+      if (it != w->hgraphs.end()) exec = it->second;
+      else capture = graph_env && (++w->hseen[key] >= 2) && w->hgraphs.size() < 64;
+    }
+    const int nk = 4 + (K - 1);
+    if (!exec && !capture) {
+      RK_TRY(enqueue(st));
+    } else {
+      if (!exec) {
+        cudaGraph_t g = nullptr;
+        RK_CUDA_TRY(cudaStreamBeginCapture(w->cap, cudaStreamCaptureModeThreadLocal));
+        const int64_t l0 = rk_launch_count();
+        Status r = enqueue(w->cap);
+        const cudaError_t ec = cudaStreamEndCapture(w->cap, &g);
+        count_launch((int)(l0 - rk_launch_count()));   // captured, not executed
+        if (!r.good()) {
+          if (g) cudaGraphDestroy(g);
+          return r;
+        }
+        RK_CUDA_TRY(ec);
+        RK_CUDA_TRY(cudaGraphInstantiate(&exec, g, 0));
+        cudaGraphDestroy(g);
+        std::lock_guard<std::mutex> lk(ms->ws_mu);
+        w->hgraphs[key] = exec;
+      }
+      RK_CUDA_TRY(cudaGraphLaunch(exec, st));
+      count_launch(nk);
+    }
     RK_CUDA_TRY(cudaStreamSynchronize(st));
     return Status::ok();
   };

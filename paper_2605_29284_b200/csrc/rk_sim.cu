@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(512, 1) cs_col_kernel(const CsColArgs a) {
   double2* buf = smem + (size_t)line * n;
   const double2* V = a.V + (int64_t)b * a.V_bstride + (int64_t)ix * a.ldV;
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  pdl_wait();   // V is the predecessor's output
   for (int y = tl; y < n; y += nthr) buf[y] = ix < a.ncols ? V[y] : make_double2(0.0, 0.0);
   __syncthreads();
   fft_line<true, true>(buf, pls, tl);
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(512, 1) cs_rowfft_kernel(const CsFftArgs a) {
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   if (threadIdx.x == 0) mbar_init(bar, 1);
   __syncthreads();
+  pdl_wait();   // Z is the predecessor's output
   if (threadIdx.x == 0) {
     int nv = 0;
     for (int l = 0; l < a.lpc; ++l) nv += (blockIdx.x * a.lpc + l) < a.ps2;
@@ -412,6 +414,7 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   const int64_t ldV = (e.ps2 + 1) & ~1;
   double2* V = nullptr;
   RK_TRY(scratch_alloc((void**)&V, sizeof(double2) * (size_t)s->M1 * ldV * batch, st));
+  double2* Zs = nullptr;   // freed after the column pass so the two FFT kernels stay adjacent
   {
     const int64_t Ps = (int64_t)e.ps1 * e.ps2;
     double2* Z = nullptr;
@@ -444,10 +447,9 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     fa.tw_off = (int)(fa.lpc * (size_t)e.ps1) + 1;
     const size_t smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1 + e.pl1.ntw);
     RK_TRY(set_smem_attr((const void*)cs_rowfft_kernel, smem));
-    cs_rowfft_kernel<<<grid, fa.lpc * e.pl1.nthr, smem, st>>>(fa);
+    RK_CUDA_TRY(launch_pdl(cs_rowfft_kernel, grid, dim3(fa.lpc * e.pl1.nthr), smem, st, fa));
     count_launch();
-    RK_LAUNCH_CHECK();
-    scratch_free(Z, st);
+    Zs = Z;
   }
   CsColArgs ca{};
   ca.pl = e.pl2;
@@ -464,10 +466,10 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     ca.tw_off = (int)(ca.lpc * (size_t)e.ps2);
     const size_t smem = sizeof(double2) * (e.ps2 * (size_t)ca.lpc + e.pl2.ntw);
     RK_TRY(set_smem_attr((const void*)cs_col_kernel, smem));
-    cs_col_kernel<<<grid, ca.lpc * e.pl2.nthr, smem, st>>>(ca);
+    RK_CUDA_TRY(launch_pdl(cs_col_kernel, grid, dim3(ca.lpc * e.pl2.nthr), smem, st, ca));
     count_launch();
-    RK_LAUNCH_CHECK();
   }
+  scratch_free(Zs, st);
   scratch_free(V, st);
   return Status::ok();
 }

@@ -91,6 +91,36 @@ def test_config_field_against_reference(pk, name):
     assert rel_err(fd.cpu().numpy(), g["field"]) < FIELD_TOL
 
 
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_pinned_host_path_chunked_upload(pk, name):
+    """Pinned host buffers take the chunked-upload path (eager call, graph capture on the
+    second, replay on the third): identical to the device path bit for bit."""
+    import torch
+    from paper_2605_29284_b200 import workloads
+    g = load_golden(name)
+    wl = workloads.CONFIGS[name]()
+    model = pk.CovarianceModel(wl.sigma2, wl.alpha, wl.nu, wl.tau2)
+    grid = pk.build_padded_grid(wl.domain, wl.dims, wl.L, wl.obs)
+    st = pk.build_setup(model, grid, wl.L, wl.obs)
+    xg = workloads.grid_covariates_for(grid.interior_nodes(), wl.grid_covariates)
+    m1, m2 = grid.interior_dims
+    ch = torch.from_numpy(np.ascontiguousarray(g["c"])).pin_memory().numpy()
+    xh = None if xg is None else torch.from_numpy(np.ascontiguousarray(xg)).pin_memory().numpy()
+    want = pk.predict_rapid(st, torch.as_tensor(g["c"], device="cuda"), g["beta"],
+                            None if xg is None else torch.as_tensor(xg, device="cuda")).cpu().numpy()
+    assert rel_err(want, g["field"]) < FIELD_TOL
+    out = torch.empty((m2, m1), dtype=torch.float64).pin_memory().numpy()
+    for it in range(4):
+        out[:] = np.nan
+        ch[:] = g["c"] * (1.0 + it)     # same pointers, new values: graph replays see them
+        got = pk.predict_rapid(st, ch, g["beta"], xh, out=out)
+        assert got is out
+        ref = want if it == 0 else pk.predict_rapid(
+            st, torch.as_tensor(g["c"] * (1.0 + it), device="cuda"), g["beta"],
+            None if xg is None else torch.as_tensor(xg, device="cuda")).cpu().numpy()
+        assert np.array_equal(out, ref), it
+
+
 @pytest.mark.parametrize("dims,L,nu", [((2, 2), 1, 1.0), ((3, 5), 1, 1.5), ((16, 11), 2, 0.5),
                                        ((37, 29), 3, 2.5), ((64, 70), 2, 1.0), ((120, 81), 4, 1.5)])
 def test_convolution_and_predict_vs_oracle(pk, dims, L, nu):
