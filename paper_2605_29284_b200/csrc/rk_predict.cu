@@ -106,7 +106,7 @@ struct RowFwdArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
-template <int SRC>
+template <int SRC, bool TWS>
 __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
   const int ya = 2 * (blockIdx.x * a.lpc + line);
   const int yb = ya + 1;
   const bool va = ya < a.nrows, vb = yb < a.nrows;
-  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
   pdl_wait();   // everything below reads the predecessor's output
   if (SRC == SRC_ROWS) {
     const double* rin = a.rows + (int64_t)b * a.in_bstride;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
     }
   }
   __syncthreads();
-  fft_line<false, true>(buf, pls, tl);
+  fft_line<false, TWS>(buf, pls, tl);
   pdl_trigger();   // the column pass may start staging while the split rows are stored
   // split Z = FFT(u + i v) into U = (Z + conj Z[-k]) / 2, V = (Z - conj Z[-k]) / 2i
   const int nr = 2 * a.lpc;
@@ -218,7 +218,7 @@ struct ColArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
-template <int MODE>  // 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
+template <int MODE, bool TWS>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
 __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
@@ -252,18 +252,18 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
       const int k = blockIdx.x * a.lpc + l;
       if (k < a.ncols) bulk_g2s(smem + (size_t)l * n, Tb + (int64_t)k * a.ldT, colb, bar);
     }
-  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
   for (int y = a.nin + tl; y < n; y += nthr) buf[y] = make_double2(0.0, 0.0);
   if (!valid)
     for (int y = tl; y < a.nin; y += nthr) buf[y] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
-  fft_line<false, true>(buf, pls, tl);
+  fft_line<false, TWS>(buf, pls, tl);
   if (MODE == 0) {
     const double* S = specs + (size_t)line * a.ldq;
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     __syncthreads();
-    fft_line<true, true>(buf, pls, tl);
+    fft_line<true, TWS>(buf, pls, tl);
     pdl_trigger();
     // TMA bulk store of the kept rows
     fence_async_smem();
@@ -304,8 +304,10 @@ struct RowInvArgs {
   int g_ld, g_row0, g_col0;
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
   int ep_off;                // smem offset (double2 units) of the prefetched epilogue operands
+  int ep_smem;               // 1: epilogue operands prefetched to smem, 0: read from global
 };
 
+template <bool TWS>
 __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
@@ -315,14 +317,14 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   const int b = blockIdx.y;
   const int H = n / 2 + 1;
   const double2* U = a.U + (int64_t)b * a.U_bstride;
-  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
   // prefetch the epilogue operands of every line's two rows (covariates X_g, CS field g)
   // with async copies; they land while the U rows are gathered and transformed
   const int pc = a.epi == EPI_COV ? a.p : 0;
   const int hasg = a.g ? 1 : 0;
   double* ep = (double*)(smem + a.ep_off);
   const double* gb = a.g ? a.g + (int64_t)b * a.g_bstride : nullptr;
-  if (pc + hasg) {
+  if (a.ep_smem && pc + hasg) {
     const int per_row = a.ncols * (pc + hasg);
     for (int e = threadIdx.x; e < a.lpc * 2 * per_row; e += blockDim.x) {
       const int lr = e / per_row, r = e - lr * per_row;     // lr = 2 l + which
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   cp_async_wait_all();
   __syncthreads();
   double2* buf = smem + (size_t)line * n;
-  fft_line<true, true>(buf, pls, tl);
+  fft_line<true, TWS>(buf, pls, tl);
   const int ya = 2 * (blockIdx.x * a.lpc + line);
   const double* beta = a.beta ? a.beta + (int64_t)b * a.p : nullptr;
   double* out = a.out + (int64_t)b * a.out_bstride;
@@ -382,12 +384,12 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
     if (a.epi == EPI_SCALAR) {
       v = v + beta[0];
     } else if (a.epi == EPI_COV) {
-      const double* xr = er + x * pc;
+      const double* xr = a.ep_smem ? er + x * pc : a.xg + ((int64_t)y * a.ncols + x) * pc;
       double fx = 0.0;
       for (int q = 0; q < pc; ++q) fx = fma(xr[q], beta[q], fx);
       v = v + fx;
     }
-    if (gb) v = er[a.ncols * pc + x] - v;
+    if (gb) v = (a.ep_smem ? er[a.ncols * pc + x] : gb[(int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + x]) - v;
     out[(int64_t)y * a.ldo + x] = v;
   }
 }
@@ -398,6 +400,9 @@ static inline int tw_slot(size_t bytes_before) { return (int)((bytes_before + 15
 static inline size_t with_tw(size_t bytes_before, const FftPlan& pl) {
   return (size_t)tw_slot(bytes_before) * 16 + (size_t)pl.ntw * 16;
 }
+// the table is staged in smem when it fits next to the lines (else read through L1/L2)
+static constexpr size_t kSmemMax = 227 * 1024;
+static inline bool tw_fits(size_t bytes_before, const FftPlan& pl) { return with_tw(bytes_before, pl) <= kSmemMax; }
 
 static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStream_t st) {
   RowFwdArgs a = a0;
@@ -407,14 +412,12 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStrea
   const int threads = a.lpc * a.pl.nthr;
   if (src == SRC_ROWS) smem += (a.tma == 2 ? 0 : (size_t)a.lpc * 2 * a.ld_in * sizeof(double)) + 16;
   a.tw_off = tw_slot(smem);
-  smem = with_tw(smem, a.pl);
-  if (src == SRC_ROWS) {
-    RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_ROWS>, smem));
-    RK_CUDA_TRY(launch_pdl(row_fwd_kernel<SRC_ROWS>, grid, dim3(threads), smem, st, a));
-  } else {
-    RK_TRY(set_smem_attr((const void*)row_fwd_kernel<SRC_LAG>, smem));
-    RK_CUDA_TRY(launch_pdl(row_fwd_kernel<SRC_LAG>, grid, dim3(threads), smem, st, a));
-  }
+  const bool tws = tw_fits(smem, a.pl);
+  if (tws) smem = with_tw(smem, a.pl);
+  auto kern = src == SRC_ROWS ? (tws ? row_fwd_kernel<SRC_ROWS, true> : row_fwd_kernel<SRC_ROWS, false>)
+                              : (tws ? row_fwd_kernel<SRC_LAG, true> : row_fwd_kernel<SRC_LAG, false>);
+  RK_TRY(set_smem_attr((const void*)kern, smem));
+  RK_CUDA_TRY(launch_pdl(kern, grid, dim3(threads), smem, st, a));
   count_launch();
   RK_LAUNCH_CHECK();
   return Status::ok();
@@ -427,14 +430,12 @@ static Status launch_col(int mode, const ColArgs& a0, int batch, cudaStream_t st
   const int threads = a.lpc * a.pl.nthr;
   if (mode == 0) smem += sizeof(double) * (size_t)a.lpc * a.ldq;
   a.tw_off = tw_slot(smem);
-  smem = with_tw(smem, a.pl);
-  if (mode == 0) {
-    RK_TRY(set_smem_attr((const void*)col_kernel<0>, smem));
-    RK_CUDA_TRY(launch_pdl(col_kernel<0>, grid, dim3(threads), smem, st, a));
-  } else {
-    RK_TRY(set_smem_attr((const void*)col_kernel<1>, smem));
-    RK_CUDA_TRY(launch_pdl(col_kernel<1>, grid, dim3(threads), smem, st, a));
-  }
+  const bool tws = tw_fits(smem, a.pl);
+  if (tws) smem = with_tw(smem, a.pl);
+  auto kern = mode == 0 ? (tws ? col_kernel<0, true> : col_kernel<0, false>)
+                        : (tws ? col_kernel<1, true> : col_kernel<1, false>);
+  RK_TRY(set_smem_attr((const void*)kern, smem));
+  RK_CUDA_TRY(launch_pdl(kern, grid, dim3(threads), smem, st, a));
   count_launch();
   RK_LAUNCH_CHECK();
   return Status::ok();
@@ -447,11 +448,17 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
   size_t smem = sizeof(double2) * a.pl.n * a.lpc;
   a.ep_off = tw_slot(smem);
   const int pc = a.epi == EPI_COV ? a.p : 0;
-  smem = (size_t)a.ep_off * 16 + sizeof(double) * (size_t)a.lpc * 2 * a.ncols * (pc + (a.g ? 1 : 0));
+  const size_t ep_bytes = sizeof(double) * (size_t)a.lpc * 2 * a.ncols * (pc + (a.g ? 1 : 0));
+  // prefetching the epilogue operands must not cost the twiddle table or occupancy: only
+  // when both fit (large rows read them from global in the epilogue instead)
+  a.ep_smem = (size_t)a.ep_off * 16 + ep_bytes + (size_t)a.pl.ntw * 16 + 16 <= kSmemMax;
+  if (a.ep_smem) smem = (size_t)a.ep_off * 16 + ep_bytes;
   a.tw_off = tw_slot(smem);
-  smem = with_tw(smem, a.pl);
-  RK_TRY(set_smem_attr((const void*)row_inv_kernel, smem));
-  RK_CUDA_TRY(launch_pdl(row_inv_kernel, grid, dim3(a.lpc * a.pl.nthr), smem, st, a));
+  const bool tws = tw_fits(smem, a.pl);
+  if (tws) smem = with_tw(smem, a.pl);
+  auto kern = tws ? row_inv_kernel<true> : row_inv_kernel<false>;
+  RK_TRY(set_smem_attr((const void*)kern, smem));
+  RK_CUDA_TRY(launch_pdl(kern, grid, dim3(a.lpc * a.pl.nthr), smem, st, a));
   count_launch();
   RK_LAUNCH_CHECK();
   return Status::ok();

@@ -5,7 +5,7 @@
 //   _rng / _std_normals       simulate.py:65-74   -> philox4x64_10() keyed (seed, stream),
 //        pre-incremented counter (block b uses counter b+1), normal = ndtri(((w>>11)+.5)/2^53)
 //   _embedding_root           simulate.py:82-100  -> ensure_embedding() (PSD test, one doubling)
-//   sim_unconditional_grid    simulate.py:103-118 -> cs_row_kernel + cs_col_kernel
+//   sim_unconditional_grid    simulate.py:103-118 -> cs_rng_kernel + cs_rowfft_kernel + cs_col_kernel
 //   sim_obs_local             simulate.py:121-143 -> obs_local_kernel
 //   refit_coefficients/_gls   exact.py:59-68,108-113 -> refit() (batched triangular solves)
 //   conditional_draw / generate_ensemble simulate.py:146-192 -> rk_ensemble_accumulate
@@ -76,78 +76,6 @@ __global__ void philox_kernel(uint64_t seed, uint64_t stream, uint64_t start, in
 }
 
 // ------------------------------------------------------------- CS field
-struct CsRowArgs {
-  FftPlan pl;
-  int lpc;
-  int ps1, ps2;
-  int keep;                  // M1 columns kept
-  const double* root_q;      // (ps2/2+1, ps1/2+1) row-major, sqrt(P)/P folded
-  int rq_ld;
-  uint64_t seed;             // ensemble seed (per-realization sub-seeds) ...
-  int64_t j0;
-  int direct;                // ... or 1: `seed` is the field seed itself
-  double2* V;                // (batch, keep, ldV)
-  int64_t ldV, V_bstride;
-  int tw_off;                // smem offset (double2 units) of the staged twiddle table
-};
-
-__global__ void __launch_bounds__(512, 1) cs_row_kernel(const CsRowArgs a) {
-  extern __shared__ __align__(16) double2 smem[];
-  const int n = a.pl.n;
-  const int nthr = a.pl.nthr;
-  const int line = threadIdx.x / nthr;
-  const int tl = threadIdx.x - line * nthr;
-  const int b = blockIdx.y;
-  const int iy = blockIdx.x * a.lpc + line;
-  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
-  const bool valid = iy < a.ps2;
-  double2* buf = smem + (size_t)line * n;
-  const uint64_t fs =
-      a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
-  if (valid) {
-    const uint64_t Ps = (uint64_t)a.ps1 * (uint64_t)a.ps2;
-    const uint64_t wb = (uint64_t)iy * (uint64_t)a.ps1;
-    // real parts: words [wb, wb + ps1); imaginary: [Ps + wb, Ps + wb + ps1)   (simulate.py:114-115)
-#pragma unroll
-    for (int part = 0; part < 2; ++part) {
-      const uint64_t w0 = wb + (part ? Ps : 0);
-      const uint64_t b0 = w0 / 4, b1 = (w0 + (uint64_t)a.ps1 - 1) / 4;
-      // two independent Philox blocks (8 normals) per iteration for ILP
-      for (uint64_t blk = b0 + tl; blk <= b1; blk += 2 * (uint64_t)nthr) {
-        const uint64_t blk2 = blk + nthr;
-        uint64_t o[8];
-        philox4x64_10(blk + 1, fs, 0, o);
-        philox4x64_10(blk2 + 1, fs, 0, o + 4);
-        double z[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) z[q] = word_normal(o[q]);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint64_t w = (q < 4 ? blk : blk2) * 4 + (q & 3);
-          if ((q < 4 || blk2 <= b1) && w >= w0 && w < w0 + (uint64_t)a.ps1) {
-            if (part) buf[w - w0].y = z[q]; else buf[w - w0].x = z[q];
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (valid) {
-    const double* R = a.root_q + (int64_t)min(iy, a.ps2 - iy) * a.rq_ld;
-    for (int ix = tl; ix < n; ix += nthr) buf[ix] = cscale(buf[ix], __ldg(&R[min(ix, n - ix)]));
-  } else {
-    for (int ix = tl; ix < n; ix += nthr) buf[ix] = make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  fft_line<true, true>(buf, pls, tl);
-  double2* V = a.V + (int64_t)b * a.V_bstride;
-  for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
-    const int l = idx % a.lpc, ix = idx / a.lpc;
-    const int row = blockIdx.x * a.lpc + l;
-    if (row < a.ps2) V[(int64_t)ix * a.ldV + row] = smem[(size_t)l * n + ix];
-  }
-}
-
 struct CsColArgs {
   FftPlan pl;
   int lpc;
@@ -160,6 +88,7 @@ struct CsColArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
+template <bool TWS>
 __global__ void __launch_bounds__(512, 1) cs_col_kernel(const CsColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
@@ -170,11 +99,11 @@ __global__ void __launch_bounds__(512, 1) cs_col_kernel(const CsColArgs a) {
   const int ix = blockIdx.x * a.lpc + line;
   double2* buf = smem + (size_t)line * n;
   const double2* V = a.V + (int64_t)b * a.V_bstride + (int64_t)ix * a.ldV;
-  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
   pdl_wait();   // V is the predecessor's output
   for (int y = tl; y < n; y += nthr) buf[y] = ix < a.ncols ? V[y] : make_double2(0.0, 0.0);
   __syncthreads();
-  fft_line<true, true>(buf, pls, tl);
+  fft_line<true, TWS>(buf, pls, tl);
   double* g = a.g + (int64_t)b * a.g_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, y = idx / a.lpc;
@@ -371,6 +300,7 @@ struct CsFftArgs {
   int tw_off;
 };
 
+template <bool TWS>
 __global__ void __launch_bounds__(512, 1) cs_rowfft_kernel(const CsFftArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
@@ -380,7 +310,7 @@ __global__ void __launch_bounds__(512, 1) cs_rowfft_kernel(const CsFftArgs a) {
   const int b = blockIdx.y;
   double2* buf = smem + (size_t)line * n;
   uint64_t* bar = (uint64_t*)(smem + (size_t)a.lpc * n);
-  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
   if (threadIdx.x == 0) mbar_init(bar, 1);
   __syncthreads();
   pdl_wait();   // Z is the predecessor's output
@@ -398,7 +328,7 @@ __global__ void __launch_bounds__(512, 1) cs_rowfft_kernel(const CsFftArgs a) {
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
-  fft_line<true, true>(buf, pls, tl);
+  fft_line<true, TWS>(buf, pls, tl);
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, ix = idx / a.lpc;
@@ -445,9 +375,12 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     fa.V_bstride = (int64_t)s->M1 * ldV;
     const dim3 grid((unsigned)ceil_div(e.ps2, fa.lpc), (unsigned)batch);
     fa.tw_off = (int)(fa.lpc * (size_t)e.ps1) + 1;
-    const size_t smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1 + e.pl1.ntw);
-    RK_TRY(set_smem_attr((const void*)cs_rowfft_kernel, smem));
-    RK_CUDA_TRY(launch_pdl(cs_rowfft_kernel, grid, dim3(fa.lpc * e.pl1.nthr), smem, st, fa));
+    size_t smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1 + e.pl1.ntw);
+    const bool tws = smem <= 227 * 1024;   // else twiddles are read through L1/L2
+    if (!tws) smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1);
+    auto kern = tws ? cs_rowfft_kernel<true> : cs_rowfft_kernel<false>;
+    RK_TRY(set_smem_attr((const void*)kern, smem));
+    RK_CUDA_TRY(launch_pdl(kern, grid, dim3(fa.lpc * e.pl1.nthr), smem, st, fa));
     count_launch();
     Zs = Z;
   }
@@ -464,9 +397,12 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   {
     const dim3 grid((unsigned)ceil_div(s->M1, ca.lpc), (unsigned)batch);
     ca.tw_off = (int)(ca.lpc * (size_t)e.ps2);
-    const size_t smem = sizeof(double2) * (e.ps2 * (size_t)ca.lpc + e.pl2.ntw);
-    RK_TRY(set_smem_attr((const void*)cs_col_kernel, smem));
-    RK_CUDA_TRY(launch_pdl(cs_col_kernel, grid, dim3(ca.lpc * e.pl2.nthr), smem, st, ca));
+    size_t smem = sizeof(double2) * (e.ps2 * (size_t)ca.lpc + e.pl2.ntw);
+    const bool tws = smem <= 227 * 1024;
+    if (!tws) smem = sizeof(double2) * e.ps2 * (size_t)ca.lpc;
+    auto kern = tws ? cs_col_kernel<true> : cs_col_kernel<false>;
+    RK_TRY(set_smem_attr((const void*)kern, smem));
+    RK_CUDA_TRY(launch_pdl(kern, grid, dim3(ca.lpc * e.pl2.nthr), smem, st, ca));
     count_launch();
   }
   scratch_free(Zs, st);
@@ -717,6 +653,57 @@ static Status fit_prepare_x(rk_fit* f, const double* X_host) {
 }
 
 // U^-1 (= L^-T) by blocked triangular inversion (cuSOLVER trtri), once per fit
+// In-place inverse of the upper-triangular column-major block U (n x n, leading dim ld).
+// cuSOLVER's trtri rejects very large n (INVALID_VALUE at n = 50000), so big blocks recurse:
+// inv([A B; 0 D]) = [inv(A), -inv(A) B inv(D); 0, inv(D)] with two TRMMs through scratch T.
+static int64_t trtri_block() {   // RK_TRTRI_BLOCK overrides (tests exercise the recursion)
+  static const int64_t b = getenv("RK_TRTRI_BLOCK") ? atoll(getenv("RK_TRTRI_BLOCK")) : 16384;
+  return std::max<int64_t>(b, 256);
+}
+
+static Status inv_upper(cusolverDnHandle_t sh, cublasHandle_t bh, double* U, int64_t n, int64_t ld, double* T,
+                        cudaStream_t st) {
+  if (n <= trtri_block()) {
+    size_t dbytes = 0, hbytes = 0;
+    cusolverStatus_t cs = cusolverDnXtrtri_bufferSize(sh, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, n,
+                                                      CUDA_R_64F, U, ld, &dbytes, &hbytes);
+    if (cs != CUSOLVER_STATUS_SUCCESS)
+      return Status::err(RK_CUDA, "cusolverDnXtrtri_bufferSize failed (status " + std::to_string((int)cs) + ")");
+    void* dwork = nullptr;
+    std::vector<char> hwork(hbytes + 1);
+    int* info = nullptr;
+    RK_CUDA_TRY(cudaMalloc(&dwork, dbytes + 16));
+    RK_CUDA_TRY(cudaMalloc(&info, sizeof(int)));
+    cs = cusolverDnXtrtri(sh, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, U, ld, dwork, dbytes,
+                          hwork.data(), hbytes, info);
+    int hinfo = 0;
+    RK_CUDA_TRY(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RK_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(dwork);
+    cudaFree(info);
+    if (cs != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+      char b[160];
+      snprintf(b, sizeof b, "triangular inverse of the Cholesky factor failed (cusolver status %d, info %d, n %lld)",
+               (int)cs, hinfo, (long long)n);
+      return Status::err(RK_NUMERIC, b);
+    }
+    return Status::ok();
+  }
+  const int64_t n1 = (n / 2 + 255) / 256 * 256, n2 = n - n1;
+  double* A = U;
+  double* B = U + n1 * ld;
+  double* D = B + n1;
+  RK_TRY(inv_upper(sh, bh, A, n1, ld, T, st));
+  RK_TRY(inv_upper(sh, bh, D, n2, ld, T, st));
+  const double one = 1.0, mone = -1.0;
+  RK_CUBLAS_TRY(cublasSetStream(bh, st));
+  RK_CUBLAS_TRY(cublasDtrmm_64(bh, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n1,
+                               n2, &one, A, ld, B, ld, T, n1));                 // T = inv(A) B
+  RK_CUBLAS_TRY(cublasDtrmm_64(bh, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, n1,
+                               n2, &mone, D, ld, T, n1, B, ld));                // B = -T inv(D)
+  return Status::ok();
+}
+
 static Status ensure_uinv(rk_fit* f, cudaStream_t st) {
   if (f->Uinv) return Status::ok();
   const int64_t n = f->n;
@@ -724,31 +711,27 @@ static Status ensure_uinv(rk_fit* f, cudaStream_t st) {
   RK_CUDA_TRY(cudaMalloc(&Ui, sizeof(double) * (size_t)n * n));
   RK_CUDA_TRY(cudaMemcpyAsync(Ui, f->U, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToDevice, st));
   cusolverDnHandle_t sh;
-  if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) return Status::err(RK_CUDA, "cusolverDnCreate failed");
-  cusolverDnSetStream(sh, st);
-  size_t dbytes = 0, hbytes = 0;
-  if (cusolverDnXtrtri_bufferSize(sh, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, Ui, n,
-                                  &dbytes, &hbytes) != CUSOLVER_STATUS_SUCCESS) {
-    cusolverDnDestroy(sh);
+  if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) {
     cudaFree(Ui);
-    return Status::err(RK_CUDA, "cusolverDnXtrtri_bufferSize failed");
+    return Status::err(RK_CUDA, "cusolverDnCreate failed");
   }
-  void* dwork = nullptr;
-  std::vector<char> hwork(hbytes + 1);
-  int* info = nullptr;
-  RK_CUDA_TRY(cudaMalloc(&dwork, dbytes + 16));
-  RK_CUDA_TRY(cudaMalloc(&info, sizeof(int)));
-  const cusolverStatus_t cs = cusolverDnXtrtri(sh, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F,
-                                               Ui, n, dwork, dbytes, hwork.data(), hbytes, info);
-  int hinfo = 0;
-  RK_CUDA_TRY(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, st));
-  RK_CUDA_TRY(cudaStreamSynchronize(st));
-  cudaFree(dwork);
-  cudaFree(info);
+  cusolverDnSetStream(sh, st);
+  double* T = nullptr;
+  Status r = Status::ok();
+  if (n > trtri_block()) {
+    const int64_t n1 = (n / 2 + 255) / 256 * 256;
+    r = scratch_alloc((void**)&T, sizeof(double) * (size_t)n1 * (n - n1), st);
+  }
+  if (r.good()) r = inv_upper(sh, (cublasHandle_t)f->cublas, Ui, n, n, T, st);
+  if (T) scratch_free(T, st);
+  if (r.good()) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) r = Status::err(RK_CUDA, std::string("inverse factor: ") + cudaGetErrorString(e));
+  }
   cusolverDnDestroy(sh);
-  if (cs != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+  if (!r.good()) {
     cudaFree(Ui);
-    return Status::err(RK_NUMERIC, "triangular inverse of the Cholesky factor failed");
+    return r;
   }
   f->Uinv = Ui;
   return Status::ok();
@@ -957,37 +940,48 @@ rk_status rk_ensemble_accumulate(rk_setup* s, const rk_fit* f, uint64_t seed, in
     if (!xg_dev && f->p != 1)
       return Status::err(RK_DOMAIN, "grid covariates are required when beta_hat has more than one entry");
     RK_TRY(ensure_embedding(s, st));
-    // realizations per device pass, capped so the per-pass scratch (Z, V, T, U, g, e) stays
-    // within ~8 GB (a 8748^2 torus needs ~1.2 GB of Z per realization)
+    // Realizations per field pass (B) are capped so the per-pass FFT scratch (Z, V, T, U, e)
+    // stays within ~8 GB (a 8748^2 torus needs ~1.2 GB of Z per realization).  The refit,
+    // whose cost is reading the n x n inverse factor twice, runs once per super-batch of up to
+    // `count` realizations: their unconditional fields are kept (up to ~16 GB) between the
+    // simulation passes and the prediction passes.
     const double per_real = 16.0 * ((double)s->emb.ps1 * s->emb.ps2 + (double)s->M1 * s->emb.ps2 +
-                                    2.0 * s->H1 * s->M2) + 16.0 * (double)s->M1 * s->M2;
+                                    2.0 * s->H1 * s->M2) + 8.0 * (double)s->m1 * s->m2;
     const int B = std::max(1, std::min((int)batch, (int)(8.0e9 / per_real)));
+    const int64_t gsz = (int64_t)s->M1 * s->M2;
+    const int64_t S = std::max<int64_t>(B, std::min<int64_t>(count, (int64_t)(16.0e9 / (8.0 * gsz))));
     const int64_t npix = (int64_t)s->m1 * s->m2;
     double *G = nullptr, *Z = nullptr, *C = nullptr, *BT = nullptr, *E = nullptr;
-    RK_TRY(scratch_alloc((void**)&G, sizeof(double) * (size_t)s->M1 * s->M2 * B, st));
-    RK_TRY(scratch_alloc((void**)&Z, sizeof(double) * (size_t)s->n * B, st));
-    RK_TRY(scratch_alloc((void**)&C, sizeof(double) * (size_t)s->n * B, st));
-    RK_TRY(scratch_alloc((void**)&BT, sizeof(double) * (size_t)f->p * B, st));
+    RK_TRY(scratch_alloc((void**)&G, sizeof(double) * (size_t)gsz * S, st));
+    RK_TRY(scratch_alloc((void**)&Z, sizeof(double) * (size_t)s->n * S, st));
+    RK_TRY(scratch_alloc((void**)&C, sizeof(double) * (size_t)s->n * S, st));
+    RK_TRY(scratch_alloc((void**)&BT, sizeof(double) * (size_t)f->p * S, st));
     RK_TRY(scratch_alloc((void**)&E, sizeof(double) * (size_t)npix * B, st));
-    for (int64_t j = j0; j < j0 + count; j += B) {
-      const int bc = (int)std::min<int64_t>(B, j0 + count - j);
-      RK_TRY(uncond_fields(s, seed, j, 0, bc, G, st));
-      RK_TRY(obs_local(s, f->model.tau2, G, seed, j, 0, bc, Z, st));
-      RK_TRY(gls_batch(f, Z, bc, BT, C, st));
-      PredictBatch pb;
-      pb.batch = bc;
-      pb.c = C;
-      pb.c_stride = s->n;
-      pb.beta = BT;
-      pb.p = f->p;
-      pb.xg = xg_dev;
-      pb.g = G;
-      pb.out = E;
-      RK_TRY(predict_batch(s, pb, st));
-      accumulate_kernel<<<(int)std::min<int64_t>(ceil_div(npix, 256), 148 * 16), 256, 0, st>>>(
-          E, bc, npix, data_pred_dev, s1_dev, s2_dev, draws_dev ? draws_dev + (j - j0) * npix : nullptr);
-      count_launch();
-      RK_LAUNCH_CHECK();
+    for (int64_t js = j0; js < j0 + count; js += S) {
+      const int64_t sc = std::min<int64_t>(S, j0 + count - js);
+      for (int64_t k = 0; k < sc; k += B) {   // unconditional fields + simulated observations
+        const int bc = (int)std::min<int64_t>(B, sc - k);
+        RK_TRY(uncond_fields(s, seed, js + k, 0, bc, G + k * gsz, st));
+        RK_TRY(obs_local(s, f->model.tau2, G + k * gsz, seed, js + k, 0, bc, Z + k * s->n, st));
+      }
+      RK_TRY(gls_batch(f, Z, sc, BT, C, st));
+      for (int64_t k = 0; k < sc; k += B) {   // e = interior(g) - predict(c_sim, beta_sim)
+        const int bc = (int)std::min<int64_t>(B, sc - k);
+        PredictBatch pb;
+        pb.batch = bc;
+        pb.c = C + k * s->n;
+        pb.c_stride = s->n;
+        pb.beta = BT + k * f->p;
+        pb.p = f->p;
+        pb.xg = xg_dev;
+        pb.g = G + k * gsz;
+        pb.out = E;
+        RK_TRY(predict_batch(s, pb, st));
+        accumulate_kernel<<<(int)std::min<int64_t>(ceil_div(npix, 256), 148 * 16), 256, 0, st>>>(
+            E, bc, npix, data_pred_dev, s1_dev, s2_dev, draws_dev ? draws_dev + (js + k - j0) * npix : nullptr);
+        count_launch();
+        RK_LAUNCH_CHECK();
+      }
     }
     scratch_free(G, st);
     scratch_free(Z, st);

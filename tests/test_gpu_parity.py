@@ -306,3 +306,38 @@ def test_ensemble_determinism_batch_independence(pk):
     assert rel_err(e1.draws, draws) < FIELD_TOL
     assert rel_err(e1.empirical_se, se) < FIELD_TOL
     assert rel_err(e1.mean_field, mean) < FIELD_TOL
+
+
+_RECURSIVE_INV_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import paper_2605_29284_b200 as pk
+from oracle import rk_oracle as ro
+from rk_testutil import rel_err
+rng = np.random.default_rng(8)
+obs = rng.uniform(0, 1, size=(1100, 2))
+z = rng.normal(size=1100)
+model = pk.CovarianceModel(1.0, 8.0, 1.5, 0.05)
+f = pk.fit(model, obs, z)
+st = pk.build_setup(model, pk.build_padded_grid((0.0, 1.0, 0.0, 1.0), (30, 26), 2, obs), 2, obs)
+e = pk.generate_ensemble(f, st, 4, 5)
+ofit = ro.exact_fit(ro.Model(1.0, 8.0, 1.5, 0.05), obs, z)
+ost = ro.rapid_setup(ofit.model, ro.make_grid((0.0, 1.0, 0.0, 1.0), (30, 26), 2, obs), 2, obs)
+draws, mean, se = ro.ensemble(ofit, ost, 4, 5)
+print(rel_err(e.draws, draws), rel_err(e.empirical_se, se))
+"""
+
+
+def test_recursive_factor_inverse_matches_oracle():
+    """Batched refit through the blocked (recursive) inverse of the Cholesky factor, forced
+    at n=1100 with RK_TRTRI_BLOCK=256 (the path n > 16384 takes, e.g. cfg5's n=50000)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RK_TRTRI_BLOCK="256")
+    r = subprocess.run([sys.executable, "-c", _RECURSIVE_INV_SCRIPT, root], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d, s = (float(v) for v in r.stdout.split()[-2:])
+    assert d < FIELD_TOL and s < FIELD_TOL, (d, s)
