@@ -258,7 +258,7 @@ def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind):
     M1, M2 = st.grid.total_dims
     flops = [0.0, (M2 + 1) // 2 * fft_flops(p1), H1 * 2 * fft_flops(p2), (m2 + 1) // 2 * fft_flops(p1)]
     dom = int(np.argmax(pass_ms))
-    names = ["gather_cstar", "pass1_rowfft", "pass2_column_filter", "pass3_rowifft_epilogue"]
+    names = ["gather_cstar", "pass1_gather_rowfft", "pass2_column_filter", "pass3_rowifft_epilogue"]
     ach = pass_bytes[dom] / (pass_ms[dom] * 1e-3) / 1e9
     peak = float(peaks.get("hbm_gbs", 6650.0))
     fl = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
@@ -269,7 +269,8 @@ def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind):
         "fp64_tflops": round(fl, 3), "fp64_peak_tflops": FP64_TFLOPS_MEASURED,
         "fp64_frac": round(fl / FP64_TFLOPS_MEASURED, 4),
         "passes": {names[i]: {"ms": round(float(pass_ms[i]), 5), "GB/s": round(pass_bytes[i] / (pass_ms[i] * 1e-3) / 1e9, 1),
-                              "fp64_TF/s": round(flops[i] / (pass_ms[i] * 1e-3) / 1e12, 3)} for i in range(4)},
+                              "fp64_TF/s": round(flops[i] / (pass_ms[i] * 1e-3) / 1e12, 3)}
+                   for i in range(4) if pass_bytes[i] > 0},   # the scatter is fused into pass 1
     }
 
 

@@ -133,7 +133,8 @@ rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const doubl
                              int32_t p, const double* xg_dev, double* out_dev, void* stream,
                              float* ms_out);
 /* algorithmic bytes per kernel of rk_predict_* for this setup:
- * bytes_out[0..3] as in rk_predict_profile, for p covariates (0 = no fixed part) */
+ * bytes_out[0..3] as in rk_predict_profile, for p covariates (0 = no fixed part).
+ * The scatter is fused into pass 1, so entry 0 (and ms_out[0]) is 0. */
 rk_status rk_predict_traffic(const rk_setup* s, int32_t p, double* bytes_out);
 
 /* ---- L2: exact fit / refit (exact.py:71-113) ---------------------------- */

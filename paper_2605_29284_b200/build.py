@@ -24,6 +24,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-ffp-contract=off", "-I" + os.path.join(ROOT, "include")]
+if os.environ.get("RK_PHASE_TIMING") == "1":   # diagnostics build (tools/phase_probe.py); use force=True
+    FLAGS.append("-DRK_PHASE_TIMING")
 SOURCES = ["rk_core.cu", "rk_predict.cu", "rk_sim.cu"]
 
 

@@ -44,22 +44,22 @@ static int finish(const Status& s) {
 // ------------------------------------------------------------------- plans
 namespace {
 std::mutex g_plan_mu;
-std::map<std::pair<int, int>, FftPlan> g_plans;
+std::map<std::pair<int, int>, FftPlan> g_plans;   // (device, n or -n for wide plans)
 std::map<std::pair<int, const void*>, bool> g_smem_set;
 }  // namespace
 
-Status plan_for(int n, FftPlan* out) {
+Status plan_for(int n, FftPlan* out, bool wide) {
   int dev = 0;
   RK_CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  auto key = std::make_pair(dev, n);
+  auto key = std::make_pair(dev, wide ? -n : n);
   auto it = g_plans.find(key);
   if (it != g_plans.end()) {
     *out = it->second;
     return Status::ok();
   }
   FftPlan pl{};
-  if (!fft_factor(n, &pl))
+  if (!fft_factor(n, &pl, wide))
     return Status::err(RK_INTERNAL, "FFT length " + std::to_string(n) + " is not 2^a 3^b");
   if (pl.nthr > 512)
     return Status::err(RK_DOMAIN, "FFT length " + std::to_string(n) + " too large for one CTA");
@@ -74,6 +74,15 @@ Status plan_for(int n, FftPlan* out) {
   g_plans[key] = pl;
   *out = pl;
   return Status::ok();
+}
+
+const FftPlan& plan_pick(const FftPlan& normal, const FftPlan& wide, int64_t lines) {
+  static const int mode = getenv("RK_WIDE") ? atoi(getenv("RK_WIDE")) : 1;   // 0 never, 1 auto, 2 always
+  if (wide.n == 0 || mode == 0) return normal;
+  if (mode == 2) return wide;
+  // wide while every line of the launch stays resident at once (148 SMs x 512 threads of a
+  // 128-register kernel); beyond that the extra threads only add waves
+  return wide.nthr > normal.nthr && lines * wide.nthr <= 148LL * 512 ? wide : normal;
 }
 
 // FFT kernels run at 128 registers/thread (__launch_bounds__(512, 1)), so an SM holds at
@@ -491,6 +500,13 @@ __global__ void row_node_kernel(const int32_t* __restrict__ node_q, int64_t nnod
   }
 }
 
+__global__ void ent_value_kernel(const int32_t* __restrict__ ent_w, const double* __restrict__ wsort, int64_t tot,
+                                 double* ent_wv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x)
+    ent_wv[i] = wsort[ent_w[i]];
+}
+
 static Status build_sparse_gather(rk_setup* s) {
   const int64_t tot = s->n * s->M;
   if (tot >= ((int64_t)1 << 31)) return Status::err(RK_DOMAIN, "n * M too large for the gather plan");
@@ -539,6 +555,28 @@ static Status build_sparse_gather(rk_setup* s) {
   count_launch();
   RK_LAUNCH_CHECK();
   RK_CUDA_TRY(cudaDeviceSynchronize());
+  {  // largest contribution count of a row pair (2k, 2k+1): sizes pass 1's product staging
+    std::vector<int32_t> rn(s->M2 + 1), no(s->nnodes + 1);
+    RK_CUDA_TRY(cudaMemcpy(rn.data(), s->row_node, sizeof(int32_t) * rn.size(), cudaMemcpyDeviceToHost));
+    RK_CUDA_TRY(cudaMemcpy(no.data(), s->node_off, sizeof(int32_t) * no.size(), cudaMemcpyDeviceToHost));
+    s->max_pair_ent = 0;
+    for (int y = 0; y < s->M2; y += 2)
+      s->max_pair_ent = std::max<int64_t>(s->max_pair_ent, no[rn[std::min(y + 2, s->M2)]] - no[rn[y]]);
+    // per row pair p: {first node, first node of row 2p+1, first contribution}; entry
+    // npairs is the end sentinel, so a pair reads two adjacent records in one round trip
+    const int npairs = (s->M2 + 1) / 2;
+    std::vector<int4> pi(npairs + 1);
+    for (int q = 0; q <= npairs; ++q) {
+      const int y = std::min(2 * q, s->M2);
+      pi[q] = make_int4(rn[y], rn[std::min(y + 1, s->M2)], no[rn[y]], 0);
+    }
+    RK_CUDA_TRY(cudaMalloc(&s->pair_info, sizeof(int4) * pi.size()));
+    RK_CUDA_TRY(cudaMemcpy(s->pair_info, pi.data(), sizeof(int4) * pi.size(), cudaMemcpyHostToDevice));
+  }
+  RK_CUDA_TRY(cudaMalloc(&s->ent_wv, sizeof(double) * std::max<int64_t>(tot, 1)));
+  ent_value_kernel<<<grid, 256>>>(s->ent_w, s->wsort, tot, s->ent_wv);
+  count_launch();
+  RK_LAUNCH_CHECK();
   cudaFree(tmp);
   cudaFree(key);
   cudaFree(key2);
@@ -565,6 +603,8 @@ static void free_setup(rk_setup* s) {
   cudaFree(s->row_node);
   cudaFree(s->ent_w);
   cudaFree(s->ent_c);
+  cudaFree(s->ent_wv);
+  cudaFree(s->pair_info);
   cudaFree(s->spec_q);
   cudaFree(s->kn_chol_dev);
   cudaFree(s->emb.root_q);
@@ -745,6 +785,8 @@ spectrum:
   s->Q2 = quarter_ld(s->p2);
   RK_TRY(plan_for(s->p1, &s->pl1));
   RK_TRY(plan_for(s->p2, &s->pl2));
+  if (!plan_for(s->p1, &s->pl1w, true).good()) s->pl1w = FftPlan{};   // n / 3 > 512 threads: none
+  if (!plan_for(s->p2, &s->pl2w, true).good()) s->pl2w = FftPlan{};
   RK_CUDA_TRY(cudaMalloc(&s->spec_q, sizeof(double) * (size_t)s->H1 * s->Q2));
   RK_TRY(spectrum_quarter(s->mat, grid->hx, grid->hy, s->p1, s->p2,
                           1.0 / ((double)s->p1 * (double)s->p2), s->spec_q, s->Q2, 0));

@@ -328,8 +328,13 @@ inline int fft_stage_list(const FftPlan& pl, int* rad) {
 }
 
 // n = 2^a 3^b -> 9^(b/2) * r3 * 8^(a'/3) * r2 with r3 = 3 or 6 (b odd; 6 absorbs one
-// factor 2 when a >= 1) and r2 = 2^(a' % 3)
-inline bool fft_factor(int n, FftPlan* pl) {
+// factor 2 when a >= 1) and r2 = 2^(a' % 3).
+// wide: for latency-bound launches with few lines, the same stages with one thread per
+// butterfly (nthr = max n/R, at most 512): measured on B200, a radix-9 stage of a 729-point
+// line takes ~1190 cycles with 2 butterflies per thread and ~700 with 1 (tools/fft_stage_lat),
+// and the line's gather / epilogue phases get more memory-level parallelism.  Splitting the
+// 9s into radix-3 stages instead was slower (6 stages x ~1100 cycles).
+inline bool fft_factor(int n, FftPlan* pl, bool wide = false) {
   int a = 0, b = 0, m = n;
   if (n < 1) return false;
   while (m % 2 == 0) { m /= 2; ++a; }
@@ -350,6 +355,11 @@ inline bool fft_factor(int n, FftPlan* pl) {
     const int nb = n / rad[i];
     const int k = fft_kmax(rad[i]);
     need = need > (nb + k - 1) / k ? need : (nb + k - 1) / k;
+  }
+  if (wide) {   // one butterfly per thread where 512 threads allow it
+    int mx = 1;
+    for (int i = 0; i < pl->nstages; ++i) mx = mx > n / rad[i] ? mx : n / rad[i];
+    need = need > (mx < 512 ? mx : 512) ? need : (mx < 512 ? mx : 512);
   }
   pl->nthr = (need + 31) / 32 * 32;
   if (pl->nthr < 32) pl->nthr = 32;

@@ -13,7 +13,10 @@ namespace rk {
 
 // --------------------------------------------------------------- bookkeeping
 void count_launch(int k = 1);
-Status plan_for(int n, FftPlan* out);            // cached per (device, n)
+Status plan_for(int n, FftPlan* out, bool wide = false);   // cached per (device, n, wide)
+// the wide plan of n when a launch of `lines` lines cannot fill the GPU with the normal
+// plan's threads (latency-bound small grids), else the normal plan
+const FftPlan& plan_pick(const FftPlan& normal, const FftPlan& wide, int64_t lines);
 // lines per CTA for a kernel: pack up to max_lines, but only while the launch still has
 // >= 2 CTAs per SM for `total_lines` lines (small grids are latency bound, not occupancy)
 int pick_lpc(const FftPlan& pl, int max_lines, int64_t total_lines = (int64_t)1 << 40);
@@ -48,7 +51,6 @@ struct GraphKey {
 };
 
 struct Workspace {
-  double* cstar = nullptr;      // (M2, ldc)
   double2* T = nullptr;         // (H1, ldT)
   double2* U = nullptr;         // (H1, ldU)
   double* c_in = nullptr;       // host-path staging
@@ -93,6 +95,7 @@ struct rk_setup {
   double px0 = 0, py0 = 0;
   int p1 = 0, p2 = 0, H1 = 0, Q2 = 0;
   rk::FftPlan pl1{}, pl2{};
+  rk::FftPlan pl1w{}, pl2w{};   // wide variants (n == 0 if none), see plan_pick
   // device arrays
   double* obs = nullptr;        // (n, 2)
   int32_t* base = nullptr;      // (n) flat padded index of block entry 0
@@ -110,6 +113,9 @@ struct rk_setup {
   int32_t* row_node = nullptr;    // (M2 + 1) first active node of each padded row
   int32_t* ent_w = nullptr;       // (n M) index into wsort
   int32_t* ent_c = nullptr;       // (n M) original observation index (into c)
+  int64_t max_pair_ent = 0;       // most contributions of one row pair (2k, 2k+1)
+  double* ent_wv = nullptr;       // (n M) weight of each contribution (wsort[ent_w])
+  int4* pair_info = nullptr;      // (ceil(M2/2) + 1) {node0, node of row 2p+1, contribution0, 0}
   double* spec_q = nullptr;     // (H1, Q2): Re fft2(filter)[ky, kx] / (p1 p2), ky <= p2/2
   double* kn_chol_dev = nullptr;  // (M, M) row-major lower
   std::vector<double> kn_chol, kn_inv;

@@ -1,10 +1,11 @@
 // rapidkrig B200: rapid predict = deterministic scatter + circulant FFT convolution.
 //
 // Reference mapping (/root/reference/pkg/src/rapidkrig/rapid.py):
-//   coefficients_to_grid 164-174 (np.add.at)  -> cstar_kernel: per-node GATHER over the
-//       cell-sorted observations (fixed order, no atomics), one thread per padded node
+//   coefficients_to_grid 164-174 (np.add.at)  -> per-node GATHER from a sparse plan built at
+//       setup (fixed order, no atomics): fused into pass 1 for predict, cstar_rows_kernel
+//       for the standalone coefficients_to_grid
 //   convolve_filter 89-100 (fft2 * spectrum, ifft2, crop) -> 3 passes:
-//       pass 1 row_fwd_kernel : two real padded rows (TMA bulk-staged) per complex FFT of
+//       pass 1 row_fwd_kernel : two real padded rows (gathered in smem, or TMA bulk-staged) per complex FFT of
 //                               length p1, split into two half spectra, written transposed
 //                               T[kx][y] (only the M2 nonzero rows exist)
 //       pass 2 col_kernel     : column kx (TMA bulk load) -> FFT(p2) -> x real-even spectrum
@@ -23,73 +24,64 @@
 #include "rk_internal.cuh"
 
 namespace rk {
+// Per-CTA phase timestamps (%globaltimer, ns) for the three predict kernels, compiled in with
+// RK_PHASE_TIMING=1 at build time and read back with rk_phase_timestamps (tools/phase_probe.py).
+#ifdef RK_PHASE_TIMING
+__device__ unsigned long long g_phase_ts[3 * 4096 * 8];
+#define RK_PHASE(k, ph)                                                                       \
+  do {                                                                                        \
+    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 4096) {                           \
+      unsigned long long t_;                                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                  \
+      g_phase_ts[((k) * 4096 + blockIdx.x) * 8 + (ph)] = t_;                                  \
+    }                                                                                         \
+  } while (0)
+#else
+#define RK_PHASE(k, ph) \
+  do {                  \
+  } while (0)
+#endif
 
 // ----------------------------------------------------------------- gather
-struct GatherSrc {
-  const int32_t* cell_start;
-  const int32_t* bsort;
-  const int32_t* perm;
+// Sparse gather plan (built at setup): per padded row, its active nodes in ascending
+// order, each with its contributions (index into wsort, original observation index) in the
+// fixed order dy asc, sorted j asc -> bitwise reproducible, identical for every batch / stream.
+struct SparseSrc {
+  const int32_t* node_q;
+  const int32_t* node_off;
+  const int32_t* row_node;
+  const int32_t* ent_w;
+  const int32_t* ent_c;
   const double* wsort;
+  const double* ent_wv;      // weight per contribution (pass 1: no wsort indirection)
+  const int4* pair_info;     // per row pair {node0, node of the odd row, contribution0, 0}
   const double* c;
   int64_t c_stride;
-  int M1, M2, bs, M;
+  int M1;
 };
 
-// c*[y, x] = sum over observations whose 2L x 2L block covers (y, x) of w * c,
-// visiting base rows by = y .. y-2L+1 and, inside each, the contiguous sorted
-// range of bases bx in [x-2L+1, x].  BS = 2L as a template (0 = runtime) so the
-// 2 x 2L cell-range loads are independent and issued together.
-template <int BS>
-__device__ __forceinline__ double cstar_at(const GatherSrc& g, const double* __restrict__ c, int y,
-                                           int x) {
-  const int bs = BS ? BS : g.bs;
-  const int xlo = max(0, x - bs + 1);
-  const int xhi = min(x, g.M1 - bs);
-  if (xlo > xhi) return 0.0;
-  double acc = 0.0;
-  constexpr int U = BS ? BS : 1;
-  for (int d0 = 0; d0 < bs; d0 += U) {
-    int j0[U], j1[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int by = y - (d0 + u);
-      j0[u] = j1[u] = 0;
-      if (by >= 0 && by <= g.M2 - bs) {
-        j0[u] = __ldg(&g.cell_start[by * g.M1 + xlo]);
-        j1[u] = __ldg(&g.cell_start[by * g.M1 + xhi + 1]);
-      }
+// c*[y, x] for the active nodes of padded row y, written through put(x, value)
+template <class Put>
+__device__ __forceinline__ void gather_row(const SparseSrc& g, const double* __restrict__ c, int y, int t,
+                                           int nt, Put put) {
+  const int a0 = __ldg(&g.row_node[y]), a1 = __ldg(&g.row_node[y + 1]);
+  const int rowq = y * g.M1;
+  for (int a = a0 + t; a < a1; a += nt) {
+    const int e0 = __ldg(&g.node_off[a]), e1 = __ldg(&g.node_off[a + 1]);
+    double acc = 0.0;
+    for (int e = e0; e < e1; ++e) {
+      const double w = __ldg(&g.wsort[__ldg(&g.ent_w[e])]);
+      const double cj = __ldg(&c[__ldg(&g.ent_c[e])]);
+      acc = __dadd_rn(acc, __dmul_rn(w, cj));   // (w * c) then add, as np.add.at
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int dy = d0 + u;
-      const int rowb = (y - dy) * g.M1;
-      for (int j = j0[u]; j < j1[u]; ++j) {
-        const int bx = __ldg(&g.bsort[j]) - rowb;
-        const double w = __ldg(&g.wsort[(int64_t)j * g.M + dy * bs + (x - bx)]);
-        const double cj = __ldg(&c[__ldg(&g.perm[j])]);
-        acc = __dadd_rn(acc, __dmul_rn(w, cj));   // (w * c) then add, as np.add.at
-      }
-    }
-  }
-  return acc;
-}
-
-template <int BS>
-__global__ void __launch_bounds__(256) cstar_kernel(GatherSrc g, double* __restrict__ out, int64_t ldo,
-                                                    int64_t out_bstride) {
-  const int b = blockIdx.y;
-  const double* c = g.c + (int64_t)b * g.c_stride;
-  double* o = out + (int64_t)b * out_bstride;
-  const int64_t tot = (int64_t)g.M1 * g.M2;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int y = (int)(e / g.M1), x = (int)(e % g.M1);
-    o[(int64_t)y * ldo + x] = cstar_at<BS>(g, c, y, x);
+    put(__ldg(&g.node_q[a]) - rowq, acc);
   }
 }
 
 // ----------------------------------------------------------------- pass 1
-enum RowSrc { SRC_ROWS = 1, SRC_LAG = 2 };
+// SRC_SPARSE: the scatter c* = A'c is formed in shared memory from the sparse plan (no c*
+// round trip through HBM); SRC_ROWS: dense input rows; SRC_LAG: the quarter lag table.
+enum RowSrc { SRC_ROWS = 1, SRC_LAG = 2, SRC_SPARSE = 3 };
 
 struct RowFwdArgs {
   FftPlan pl;
@@ -103,6 +95,9 @@ struct RowFwdArgs {
   int tma;                   // SRC_ROWS: rows are 16-byte aligned -> TMA bulk staging
   const double* lagq;        // SRC_LAG: quarter lag table (p2/2+1, p1/2+1)
   int lag_ld, p2;
+  SparseSrc sp;              // SRC_SPARSE: gather plan + coefficients
+  int prod_off, prod_cap;    // SRC_SPARSE: smem offset (double2 units) / per-line size (doubles)
+                             // of the staged products w * c of the line's row pair
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
@@ -118,6 +113,7 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
   const int ya = 2 * (blockIdx.x * a.lpc + line);
   const int yb = ya + 1;
   const bool va = ya < a.nrows, vb = yb < a.nrows;
+  RK_PHASE(0, 0);
   const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
   pdl_wait();   // everything below reads the predecessor's output
   if (SRC == SRC_ROWS) {
@@ -170,6 +166,60 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
         buf[x] = make_double2(u, v);
       }
     }
+  } else if (SRC == SRC_SPARSE) {
+    // the row pair's contributions are contiguous in the plan.  Three dependent global
+    // round trips: the pair record; the node records and contribution (weight, observation)
+    // pairs, all in flight together; the coefficients.  Products w * c and node records
+    // are staged in shared memory, then each active node adds its own products in the
+    // fixed plan order.
+    const SparseSrc& g = a.sp;
+    const double* __restrict__ cb = g.c + (int64_t)b * g.c_stride;
+    double* __restrict__ prod = (double*)(smem + a.prod_off) + (size_t)line * 2 * a.prod_cap;
+    int2* __restrict__ nrec = (int2*)(prod + a.prod_cap);
+    const int pidx = blockIdx.x * a.lpc + line;
+    int4 P0 = make_int4(0, 0, 0, 0), P1 = P0;
+    if (va) {
+      P0 = __ldg(&g.pair_info[pidx]);
+      P1 = __ldg(&g.pair_info[pidx + 1]);
+    }
+    const int n0 = P0.x, n1 = P0.y, e0 = P0.z;
+    const int nn = P1.x - n0, cnt = P1.z - e0;
+    for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
+    const int rowq = ya * g.M1;
+    for (int k = tl; k < nn; k += nthr) {   // node k: end of its products, its x | odd-row bit
+      const int q = __ldg(&g.node_q[n0 + k]) - rowq;
+      const int odd = n0 + k >= n1;
+      nrec[k] = make_int2(__ldg(&g.node_off[n0 + k + 1]) - e0, 2 * (q - odd * g.M1) + odd);
+    }
+    constexpr int U = 4;
+    for (int i0 = tl; i0 < cnt; i0 += U * nthr) {
+      double w[U];
+      int ci[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nthr;
+        w[u] = i < cnt ? __ldg(&g.ent_wv[e0 + i]) : 0.0;
+        ci[u] = i < cnt ? __ldg(&g.ent_c[e0 + i]) : 0;
+      }
+      double cv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cv[u] = i0 + u * nthr < cnt ? __ldg(&cb[ci[u]]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * nthr;
+        if (i < cnt) prod[i] = __dmul_rn(w[u], cv[u]);
+      }
+    }
+    __syncthreads();
+    RK_PHASE(0, 1);
+    double* bd = (double*)buf;
+    for (int k = tl; k < nn; k += nthr) {
+      const int s0 = k ? nrec[k - 1].x : 0;
+      const int2 r = nrec[k];
+      double acc = 0.0;
+      for (int i = s0; i < r.x; ++i) acc = __dadd_rn(acc, prod[i]);   // (w * c) then add, as np.add.at
+      bd[r.y] = acc;
+    }
   } else {
     for (int x = tl; x < n; x += nthr) {
       const int bx = min(x, n - x);
@@ -179,7 +229,9 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
     }
   }
   __syncthreads();
+  RK_PHASE(0, 2);
   fft_line<false, TWS>(buf, pls, tl);
+  RK_PHASE(0, 3);
   pdl_trigger();   // the column pass may start staging while the split rows are stored
   // split Z = FFT(u + i v) into U = (Z + conj Z[-k]) / 2, V = (Z - conj Z[-k]) / 2i
   const int nr = 2 * a.lpc;
@@ -198,6 +250,7 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
     else o = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
     T[(int64_t)kx * a.ldT + row] = o;
   }
+  RK_PHASE(0, 4);
 }
 
 // ----------------------------------------------------------------- pass 2
@@ -232,6 +285,7 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
   double* specs = (double*)(smem + (size_t)a.lpc * n);          // lpc x ldq (filter mode)
   uint64_t* bar = (uint64_t*)(specs + (MODE == 0 ? (size_t)a.lpc * a.ldq : 0));
   const double2* Tb = a.T + (int64_t)b * a.T_bstride;
+  RK_PHASE(1, 0);
   if (threadIdx.x == 0) mbar_init(bar, 1);
   __syncthreads();
   const uint32_t colb = (uint32_t)a.nin * 16u;
@@ -258,12 +312,15 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
     for (int y = tl; y < a.nin; y += nthr) buf[y] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
+  RK_PHASE(1, 1);
   fft_line<false, TWS>(buf, pls, tl);
+  RK_PHASE(1, 2);
   if (MODE == 0) {
     const double* S = specs + (size_t)line * a.ldq;
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     __syncthreads();
     fft_line<true, TWS>(buf, pls, tl);
+    RK_PHASE(1, 3);
     pdl_trigger();
     // TMA bulk store of the kept rows
     fence_async_smem();
@@ -279,6 +336,7 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
       bulk_wait_read0();
     }
     __syncthreads();
+    RK_PHASE(1, 4);
   } else {
     if (valid)
       for (int ky = tl; ky <= n / 2; ky += nthr) a.out_q[(int64_t)kx * a.ldq + ky] = buf[ky].x * a.scale;
@@ -305,6 +363,7 @@ struct RowInvArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
   int ep_off;                // smem offset (double2 units) of the prefetched epilogue operands
   int ep_smem;               // 1: epilogue operands prefetched to smem, 0: read from global
+  int xg_bulk;               // X_g is 16-byte aligned: one TMA bulk copy per CTA
 };
 
 template <bool TWS>
@@ -317,22 +376,42 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   const int b = blockIdx.y;
   const int H = n / 2 + 1;
   const double2* U = a.U + (int64_t)b * a.U_bstride;
+  RK_PHASE(2, 0);
   const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
-  // prefetch the epilogue operands of every line's two rows (covariates X_g, CS field g)
-  // with async copies; they land while the U rows are gathered and transformed
+  // prefetch the epilogue operands of the CTA's rows (covariates X_g: one contiguous block,
+  // a TMA bulk copy; CS field g: strided rows, 8-byte async copies); they land while the U
+  // rows are gathered and transformed
   const int pc = a.epi == EPI_COV ? a.p : 0;
   const int hasg = a.g ? 1 : 0;
-  double* ep = (double*)(smem + a.ep_off);
+  const int y0 = 2 * blockIdx.x * a.lpc;
+  const int nr = min(2 * a.lpc, a.nrows - y0);
+  double* epx = (double*)(smem + a.ep_off);                    // (2 lpc, ncols, pc)
+  double* epg = epx + (size_t)2 * a.lpc * a.ncols * pc;        // (2 lpc, ncols)
+  uint64_t* bar = (uint64_t*)(epg + (size_t)2 * a.lpc * a.ncols * hasg);
   const double* gb = a.g ? a.g + (int64_t)b * a.g_bstride : nullptr;
-  if (a.ep_smem && pc + hasg) {
-    const int per_row = a.ncols * (pc + hasg);
-    for (int e = threadIdx.x; e < a.lpc * 2 * per_row; e += blockDim.x) {
-      const int lr = e / per_row, r = e - lr * per_row;     // lr = 2 l + which
-      const int y = 2 * blockIdx.x * a.lpc + lr;
-      if (y >= a.nrows) continue;
-      const double* src = r < a.ncols * pc ? a.xg + (int64_t)y * a.ncols * pc + r
-                                           : gb + (int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + (r - a.ncols * pc);
-      cp_async8(ep + e, src);
+  bool xwait = false;
+  if (a.ep_smem && pc) {
+    const double* src = a.xg + (int64_t)y0 * a.ncols * pc;
+    const int cnt = nr * a.ncols * pc;
+    if (a.xg_bulk) {
+      const uint32_t b16 = (uint32_t)(cnt * 8) & ~15u;
+      xwait = b16 > 0;
+      if (threadIdx.x == 0) {
+        if (xwait) {
+          mbar_init(bar, 1);
+          mbar_expect_tx(bar, b16);
+          bulk_g2s(epx, src, b16, bar);
+        }
+        if (b16 != (uint32_t)cnt * 8) epx[cnt - 1] = __ldg(&src[cnt - 1]);   // odd tail
+      }
+    } else {
+      for (int e = threadIdx.x; e < cnt; e += blockDim.x) cp_async8(epx + e, src + e);
+    }
+  }
+  if (a.ep_smem && hasg) {
+    for (int e = threadIdx.x; e < nr * a.ncols; e += blockDim.x) {
+      const int r = e / a.ncols, x = e - r * a.ncols;
+      cp_async8(epg + e, gb + (int64_t)(a.g_row0 + y0 + r) * a.g_ld + a.g_col0 + x);
     }
   }
   pdl_wait();   // U is the predecessor's output
@@ -365,14 +444,17 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
       }
     }
   }
+  RK_PHASE(2, 1);
   cp_async_wait_all();
   __syncthreads();
+  RK_PHASE(2, 2);
   double2* buf = smem + (size_t)line * n;
   fft_line<true, TWS>(buf, pls, tl);
+  if (xwait) mbar_wait(bar, 0);   // init is ordered by the barrier above
+  RK_PHASE(2, 3);
   const int ya = 2 * (blockIdx.x * a.lpc + line);
   const double* beta = a.beta ? a.beta + (int64_t)b * a.p : nullptr;
   double* out = a.out + (int64_t)b * a.out_bstride;
-  const int per_row = a.ncols * (pc + hasg);
   for (int e = tl; e < 2 * a.ncols; e += nthr) {
     const int which = e >= a.ncols;
     const int x = e - which * a.ncols;
@@ -380,18 +462,19 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
     if (y >= a.nrows) continue;
     const double2 z = buf[a.col0 + x];
     double v = which ? z.y : z.x;
-    const double* er = ep + (2 * line + which) * per_row;
+    const int lr = 2 * line + which;
     if (a.epi == EPI_SCALAR) {
       v = v + beta[0];
     } else if (a.epi == EPI_COV) {
-      const double* xr = a.ep_smem ? er + x * pc : a.xg + ((int64_t)y * a.ncols + x) * pc;
+      const double* xr = a.ep_smem ? epx + ((size_t)lr * a.ncols + x) * pc : a.xg + ((int64_t)y * a.ncols + x) * pc;
       double fx = 0.0;
       for (int q = 0; q < pc; ++q) fx = fma(xr[q], beta[q], fx);
       v = v + fx;
     }
-    if (gb) v = (a.ep_smem ? er[a.ncols * pc + x] : gb[(int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + x]) - v;
+    if (gb) v = (a.ep_smem ? epg[lr * a.ncols + x] : gb[(int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + x]) - v;
     out[(int64_t)y * a.ldo + x] = v;
   }
+  RK_PHASE(2, 4);
 }
 
 // ----------------------------------------------------------------- launches
@@ -411,11 +494,16 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStrea
   size_t smem = sizeof(double2) * a.pl.n * a.lpc;
   const int threads = a.lpc * a.pl.nthr;
   if (src == SRC_ROWS) smem += (a.tma == 2 ? 0 : (size_t)a.lpc * 2 * a.ld_in * sizeof(double)) + 16;
+  if (src == SRC_SPARSE) {
+    a.prod_off = tw_slot(smem);
+    smem = (size_t)a.prod_off * 16 + sizeof(double) * (size_t)a.lpc * 2 * a.prod_cap;
+  }
   a.tw_off = tw_slot(smem);
   const bool tws = tw_fits(smem, a.pl);
   if (tws) smem = with_tw(smem, a.pl);
-  auto kern = src == SRC_ROWS ? (tws ? row_fwd_kernel<SRC_ROWS, true> : row_fwd_kernel<SRC_ROWS, false>)
-                              : (tws ? row_fwd_kernel<SRC_LAG, true> : row_fwd_kernel<SRC_LAG, false>);
+  auto kern = src == SRC_ROWS   ? (tws ? row_fwd_kernel<SRC_ROWS, true> : row_fwd_kernel<SRC_ROWS, false>)
+              : src == SRC_LAG ? (tws ? row_fwd_kernel<SRC_LAG, true> : row_fwd_kernel<SRC_LAG, false>)
+                               : (tws ? row_fwd_kernel<SRC_SPARSE, true> : row_fwd_kernel<SRC_SPARSE, false>);
   RK_TRY(set_smem_attr((const void*)kern, smem));
   RK_CUDA_TRY(launch_pdl(kern, grid, dim3(threads), smem, st, a));
   count_launch();
@@ -448,7 +536,8 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
   size_t smem = sizeof(double2) * a.pl.n * a.lpc;
   a.ep_off = tw_slot(smem);
   const int pc = a.epi == EPI_COV ? a.p : 0;
-  const size_t ep_bytes = sizeof(double) * (size_t)a.lpc * 2 * a.ncols * (pc + (a.g ? 1 : 0));
+  const size_t ep_bytes = sizeof(double) * (size_t)a.lpc * 2 * a.ncols * (pc + (a.g ? 1 : 0)) + 16;
+  a.xg_bulk = a.xg && (reinterpret_cast<uintptr_t>(a.xg) & 15) == 0;
   // prefetching the epilogue operands must not cost the twiddle table or occupancy: only
   // when both fit (large rows read them from global in the epilogue instead)
   a.ep_smem = (size_t)a.ep_off * 16 + ep_bytes + (size_t)a.pl.ntw * 16 + 16 <= kSmemMax;
@@ -529,91 +618,8 @@ Status spectrum_quarter(const MaternDev& P, double hx, double hy, int p1, int p2
   return Status::ok();
 }
 
-static GatherSrc gather_src(const rk_setup* s, const double* c, int64_t c_stride) {
-  GatherSrc g;
-  g.cell_start = s->cell_start;
-  g.bsort = s->bsort;
-  g.perm = s->perm;
-  g.wsort = s->wsort;
-  g.c = c;
-  g.c_stride = c_stride;
-  g.M1 = s->M1;
-  g.M2 = s->M2;
-  g.bs = s->bs;
-  g.M = s->M;
-  return g;
-}
-
-// Tiled gather: a CTA owns TY x TX nodes (one warp per row, 4 columns per lane) and first
-// stages the tile's window of cell_start (base rows y0-BS+1 .. y0+TY-1, base columns
-// x0-BS+1 .. x0+TX) in shared memory, so each node's 2 BS range lookups are smem reads.
-// Accumulation order per node is the same as cstar_at (dy ascending, sorted j ascending).
-constexpr int CS_TY = 8, CS_TX = 128;
-
-template <int BS>
-__global__ void __launch_bounds__(256) cstar_tile_kernel(GatherSrc g, double* __restrict__ out,
-                                                         int64_t ldo, int64_t out_bstride) {
-  constexpr int RW = CS_TY + BS - 1, CW = CS_TX + BS;
-  __shared__ int cs[RW][CW];
-  const int b = blockIdx.z;
-  const double* c = g.c + (int64_t)b * g.c_stride;
-  double* o = out + (int64_t)b * out_bstride;
-  const int x0 = blockIdx.x * CS_TX, y0 = blockIdx.y * CS_TY;
-  const int by_lo = y0 - BS + 1, bx_lo = x0 - BS + 1;
-  const int nbase = g.M1 * g.M2;
-  for (int e = threadIdx.x; e < RW * CW; e += blockDim.x) {
-    const int r = e / CW, q = e % CW;
-    const int by = by_lo + r, bx = bx_lo + q;
-    int v = 0;
-    if (by >= 0 && by <= g.M2 - BS && bx >= 0)
-      v = __ldg(&g.cell_start[min(by * g.M1 + min(bx, g.M1), nbase)]);
-    cs[r][q] = v;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int y = y0 + warp;
-  if (y >= g.M2) return;
-#pragma unroll
-  for (int k = 0; k < CS_TX / 32; ++k) {
-    const int x = x0 + lane + 32 * k;
-    if (x >= g.M1) continue;
-    const int xlo = max(0, x - BS + 1), xhi = min(x, g.M1 - BS);
-    double acc = 0.0;
-    if (xlo <= xhi) {
-#pragma unroll
-      for (int dy = 0; dy < BS; ++dy) {
-        const int by = y - dy;
-        if (by < 0 || by > g.M2 - BS) continue;
-        const int r = by - by_lo;
-        const int j0 = cs[r][xlo - bx_lo], j1 = cs[r][xhi + 1 - bx_lo];
-        const int rowb = by * g.M1;
-        for (int j = j0; j < j1; ++j) {
-          const int bx = __ldg(&g.bsort[j]) - rowb;
-          const double w = __ldg(&g.wsort[(int64_t)j * g.M + dy * BS + (x - bx)]);
-          const double cj = __ldg(&c[__ldg(&g.perm[j])]);
-          acc = __dadd_rn(acc, __dmul_rn(w, cj));
-        }
-      }
-    }
-    o[(int64_t)y * ldo + x] = acc;
-  }
-}
-
-// Sparse gather: one CTA per padded row; the row is zero-filled in smem, every active node of
-// the row sums its precomputed contributions (fixed order -> bitwise reproducible, identical
-// to cstar_at), then the row is written out coalesced.  Work ~ n M + G instead of G (2L)^2
-// range tests.
-struct SparseSrc {
-  const int32_t* node_q;
-  const int32_t* node_off;
-  const int32_t* row_node;
-  const int32_t* ent_w;
-  const int32_t* ent_c;
-  const double* wsort;
-  const double* c;
-  int64_t c_stride;
-  int M1;
-};
+// Standalone scatter (coefficients_to_grid): one CTA per padded row, zero-filled in smem,
+// gathered from the sparse plan, written out coalesced.  Work ~ n M + G.
 
 __global__ void __launch_bounds__(256) cstar_rows_kernel(SparseSrc g, double* __restrict__ out,
                                                          int64_t ldo, int64_t out_bstride) {
@@ -622,26 +628,14 @@ __global__ void __launch_bounds__(256) cstar_rows_kernel(SparseSrc g, double* __
   const double* c = g.c + (int64_t)b * g.c_stride;
   for (int x = threadIdx.x; x < g.M1; x += blockDim.x) rowbuf[x] = 0.0;
   __syncthreads();
-  const int a0 = __ldg(&g.row_node[y]), a1 = __ldg(&g.row_node[y + 1]);
-  const int rowq = y * g.M1;
-  for (int a = a0 + threadIdx.x; a < a1; a += blockDim.x) {
-    const int e0 = __ldg(&g.node_off[a]), e1 = __ldg(&g.node_off[a + 1]);
-    double acc = 0.0;
-    for (int e = e0; e < e1; ++e) {
-      const double w = __ldg(&g.wsort[__ldg(&g.ent_w[e])]);
-      const double cj = __ldg(&c[__ldg(&g.ent_c[e])]);
-      acc = __dadd_rn(acc, __dmul_rn(w, cj));   // (w * c) then add, as np.add.at
-    }
-    rowbuf[__ldg(&g.node_q[a]) - rowq] = acc;
-  }
+  gather_row(g, c, y, threadIdx.x, blockDim.x, [&](int x, double v) { rowbuf[x] = v; });
   pdl_trigger();   // the row-FFT pass may stage its twiddles while the rows are stored
   __syncthreads();
   double* o = out + (int64_t)b * out_bstride + (int64_t)y * ldo;
   for (int x = threadIdx.x; x < g.M1; x += blockDim.x) o[x] = rowbuf[x];
 }
 
-static Status launch_cstar(const rk_setup* s, const double* c, int64_t c_stride, double* out,
-                           int64_t ldo, int batch, cudaStream_t st) {
+static SparseSrc sparse_src(const rk_setup* s, const double* c, int64_t c_stride) {
   SparseSrc g;
   g.node_q = s->node_q;
   g.node_off = s->node_off;
@@ -649,9 +643,24 @@ static Status launch_cstar(const rk_setup* s, const double* c, int64_t c_stride,
   g.ent_w = s->ent_w;
   g.ent_c = s->ent_c;
   g.wsort = s->wsort;
+  g.ent_wv = s->ent_wv;
+  g.pair_info = s->pair_info;
   g.c = c;
   g.c_stride = c_stride;
   g.M1 = s->M1;
+  return g;
+}
+
+// pass 1 stages one row pair's products per line: fused while that stays small
+// (RK_FUSED_GATHER=0 forces the standalone scatter; tests compare both)
+static bool fused_gather(const rk_setup* s) {
+  static const bool allow = !(getenv("RK_FUSED_GATHER") && atoi(getenv("RK_FUSED_GATHER")) == 0);
+  return allow && s->max_pair_ent * 16 <= 64 * 1024;
+}
+
+static Status launch_cstar(const rk_setup* s, const double* c, int64_t c_stride, double* out,
+                           int64_t ldo, int batch, cudaStream_t st) {
+  const SparseSrc g = sparse_src(s, c, c_stride);
   const size_t smem = sizeof(double) * (size_t)s->M1;
   RK_TRY(set_smem_attr((const void*)cstar_rows_kernel, smem));
   cstar_rows_kernel<<<dim3((unsigned)s->M2, (unsigned)batch), 256, smem, st>>>(g, out, ldo, ldo * s->M2);
@@ -667,7 +676,7 @@ static inline int64_t round_even(int64_t v) { return (v + 1) & ~int64_t(1); }
 static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in, int64_t in_bstride,
                             int batch, int row0, int nout, int col0, int ncols, const RowInvArgs& epi,
                             cudaStream_t st, cudaEvent_t* ev = nullptr, Workspace* ws = nullptr,
-                            const HostIo* hio = nullptr) {
+                            const HostIo* hio = nullptr, const SparseSrc* sp = nullptr) {
   const int64_t ldT = round_even(s->M2);
   const int64_t ldU = round_even(nout);
   double2 *T = nullptr, *U = nullptr;
@@ -680,8 +689,8 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     U = ws->U;
   }
   RowFwdArgs ra{};
-  ra.pl = s->pl1;
-  ra.lpc = pick_lpc(s->pl1, 4, (int64_t)((s->M2 + 1) / 2) * batch);
+  ra.pl = plan_pick(s->pl1, s->pl1w, (int64_t)((s->M2 + 1) / 2) * batch);
+  ra.lpc = pick_lpc(ra.pl, 4, (int64_t)((s->M2 + 1) / 2) * batch);
   ra.nrows = s->M2;
   ra.ncols = s->M1;
   ra.T = T;
@@ -693,12 +702,17 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   ra.tma = ((ld_in * 8) % 16 == 0) && ((reinterpret_cast<uintptr_t>(rows) & 15) == 0) &&
            ((in_bstride * 8) % 16 == 0);
   if (ra.tma && s->pl1.n - ld_in >= s->M1) ra.tma = 2;   // stage inside the line's zero tail
+  if (sp) {
+    ra.sp = *sp;
+    ra.tma = 0;
+    ra.prod_cap = (int)((s->max_pair_ent + 1) & ~int64_t(1));
+  }
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[1], st));
-  RK_TRY(launch_row_fwd(SRC_ROWS, ra, batch, st));
+  RK_TRY(launch_row_fwd(sp ? SRC_SPARSE : SRC_ROWS, ra, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[2], st));
   ColArgs ca{};
-  ca.pl = s->pl2;
-  ca.lpc = pick_lpc(s->pl2, 4, (int64_t)s->H1 * batch);
+  ca.pl = plan_pick(s->pl2, s->pl2w, (int64_t)s->H1 * batch);
+  ca.lpc = pick_lpc(ca.pl, 4, (int64_t)s->H1 * batch);
   ca.ncols = s->H1;
   ca.nin = s->M2;
   ca.T = T;
@@ -714,8 +728,8 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   RK_TRY(launch_col(0, ca, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
   RowInvArgs ia = epi;
-  ia.pl = s->pl1;
-  ia.lpc = pick_lpc(s->pl1, 4, (int64_t)((nout + 1) / 2) * batch);
+  ia.pl = plan_pick(s->pl1, s->pl1w, (int64_t)((nout + 1) / 2) * batch);
+  ia.lpc = pick_lpc(ia.pl, 4, (int64_t)((nout + 1) / 2) * batch);
   ia.nrows = nout;
   ia.U = U;
   ia.ldU = ldU;
@@ -734,7 +748,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
       ck.out = ia.out + (int64_t)r0 * ia.ldo;
       if (ck.xg) ck.xg = ia.xg + (int64_t)r0 * ncols * ia.p;
       ck.g_row0 = ia.g_row0 + r0;
-      ck.lpc = pick_lpc(s->pl1, 4, (int64_t)((ck.nrows + 1) / 2));
+      ck.lpc = pick_lpc(ck.pl, 4, (int64_t)((ck.nrows + 1) / 2));
       if (hio->xev) RK_CUDA_TRY(cudaStreamWaitEvent(st, hio->xev[k], 0));
       RK_TRY(launch_row_inv(ck, 1, st));
       if (hio->out_host)
@@ -770,16 +784,20 @@ Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st,
   e.g_ld = s->M1;
   e.g_row0 = s->grid.pad[2];
   e.g_col0 = s->grid.pad[0];
+  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[0], st));
+  if (fused_gather(s)) {   // c* is formed in shared memory per row pair inside pass 1
+    const SparseSrc sp = sparse_src(s, pb.c, pb.c_stride);
+    return conv_pipeline(s, nullptr, s->M1, 0, pb.batch, s->grid.pad[2], s->m2, s->grid.pad[0], s->m1, e, st,
+                         ev, ws, hio, &sp);
+  }
+  // very dense row pairs: standalone scatter kernel, c* through HBM
   const int64_t ldc = round_even(s->M1);
   double* cstar = nullptr;
-  const bool own = !(ws && pb.batch == 1);
-  if (own) RK_TRY(scratch_alloc((void**)&cstar, sizeof(double) * (size_t)ldc * s->M2 * pb.batch, st));
-  else cstar = ws->cstar;
-  if (ev) RK_CUDA_TRY(cudaEventRecord(ev[0], st));
+  RK_TRY(scratch_alloc((void**)&cstar, sizeof(double) * (size_t)ldc * s->M2 * pb.batch, st));
   RK_TRY(launch_cstar(s, pb.c, pb.c_stride, cstar, ldc, pb.batch, st));
-  Status r = conv_pipeline(s, cstar, ldc, ldc * s->M2, pb.batch, s->grid.pad[2], s->m2,
-                           s->grid.pad[0], s->m1, e, st, ev, ws, hio);
-  if (own) scratch_free(cstar, st);
+  Status r = conv_pipeline(s, cstar, ldc, ldc * s->M2, pb.batch, s->grid.pad[2], s->m2, s->grid.pad[0], s->m1,
+                           e, st, ev, ws, hio);
+  scratch_free(cstar, st);
   return r;
 }
 
@@ -792,8 +810,7 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
     return Status::ok();
   }
   Workspace* w = new Workspace();
-  const int64_t ldc = round_even(s->M1), ldT = round_even(s->M2), ldU = round_even(s->m2);
-  RK_CUDA_TRY(cudaMalloc(&w->cstar, sizeof(double) * (size_t)ldc * s->M2));
+  const int64_t ldT = round_even(s->M2), ldU = round_even(s->m2);
   RK_CUDA_TRY(cudaMalloc(&w->T, sizeof(double2) * (size_t)s->H1 * ldT));
   RK_CUDA_TRY(cudaMalloc(&w->U, sizeof(double2) * (size_t)s->H1 * ldU));
   RK_CUDA_TRY(cudaMalloc(&w->c_in, sizeof(double) * std::max<int64_t>(s->n, 2)));
@@ -819,7 +836,6 @@ void free_workspaces(rk_setup* s) {
     for (auto& e : w->xev)
       if (e) cudaEventDestroy(e);
     cudaFreeHost(w->beta_h);
-    cudaFree(w->cstar);
     cudaFree(w->T);
     cudaFree(w->U);
     cudaFree(w->c_in);
@@ -835,6 +851,9 @@ void free_workspaces(rk_setup* s) {
 // Predict of one field through the workspace: direct launches the first time a pointer
 // set is seen, a CUDA graph (captured on the workspace's private stream, replayed on
 // `st`) from the second time on.
+// kernels in one graphed predict: gather + row FFT, column filter, row IFFT + epilogue
+static constexpr int kPredictKernels = 3;
+
 static Status predict_graphed(rk_setup* s, Workspace* w, const PredictBatch& pb, cudaStream_t st) {
   const GraphKey key{(uintptr_t)pb.c, (uintptr_t)pb.beta, (uintptr_t)pb.xg, (uintptr_t)pb.out, pb.p};
   cudaGraphExec_t exec = nullptr;
@@ -847,7 +866,7 @@ static Status predict_graphed(rk_setup* s, Workspace* w, const PredictBatch& pb,
   }
   if (exec) {
     RK_CUDA_TRY(cudaGraphLaunch(exec, st));
-    count_launch(4);
+    count_launch(kPredictKernels);
     return Status::ok();
   }
   if (!capture) return predict_batch(s, pb, st, nullptr, w);
@@ -855,7 +874,7 @@ static Status predict_graphed(rk_setup* s, Workspace* w, const PredictBatch& pb,
   RK_CUDA_TRY(cudaStreamBeginCapture(w->cap, cudaStreamCaptureModeThreadLocal));
   Status r = predict_batch(s, pb, w->cap, nullptr, w);
   const cudaError_t ec = cudaStreamEndCapture(w->cap, &g);
-  count_launch(-4);   // captured, not executed
+  count_launch(-kPredictKernels);   // captured, not executed
   if (!r.good()) {
     if (g) cudaGraphDestroy(g);
     return r;
@@ -868,7 +887,7 @@ static Status predict_graphed(rk_setup* s, Workspace* w, const PredictBatch& pb,
     w->graphs[key] = exec;
   }
   RK_CUDA_TRY(cudaGraphLaunch(exec, st));
-  count_launch(4);
+  count_launch(kPredictKernels);
   return Status::ok();
 }
 
@@ -891,6 +910,17 @@ static int finish_status(const Status& s) {
 }
 
 extern "C" {
+
+// diagnostics: copies the 3 x 4096 x 8 phase timestamps (RK_PHASE_TIMING builds only)
+rk_status rk_phase_timestamps(unsigned long long* out) {
+#ifdef RK_PHASE_TIMING
+  return cudaMemcpyFromSymbol(out, g_phase_ts, sizeof(g_phase_ts)) == cudaSuccess ? RK_OK : RK_CUDA;
+#else
+  (void)out;
+  rk::set_error(RK_INTERNAL, "library built without RK_PHASE_TIMING");
+  return RK_INTERNAL;
+#endif
+}
 
 rk_status rk_coefficients_to_grid(const rk_setup* s, const double* c_dev, double* cstar_dev,
                                   void* stream) {
@@ -988,13 +1018,14 @@ rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const doubl
 }
 
 rk_status rk_predict_traffic(const rk_setup* s, int32_t p, double* b) {
-  // gather: weights (n M), sorted base/perm (8 n), c (8 n), cell_start (4 (G + 1)), c* write (8 G)
-  // pass 1: c* read (8 G), T write (16 H1 M2); pass 2: T read, quarter spectrum (8 H1 (p2/2+1)),
-  // U write (16 H1 m2); pass 3: U read, covariates (8 N p), field write (8 N)
-  const double n = (double)s->n, M = (double)s->M, G = (double)s->M1 * s->M2;
+  // the scatter is fused into pass 1, so entry 0 is empty.  pass 1: weights (8 n M), plan
+  // indices (8 n M: wsort index + observation index), c (8 n), node lists (8 nnodes + 4 M2),
+  // T write (16 H1 M2); pass 2: T read, quarter spectrum (8 H1 (p2/2+1)), U write (16 H1 m2);
+  // pass 3: U read, covariates (8 N p), field write (8 N)
+  const double n = (double)s->n, M = (double)s->M;
   const double N = (double)s->m1 * s->m2, H = (double)s->H1;
-  b[0] = n * M * 8.0 + 16.0 * n + 4.0 * (G + 1.0) + 8.0 * G;
-  b[1] = 8.0 * G + 16.0 * H * s->M2;
+  b[0] = 0.0;
+  b[1] = n * M * 16.0 + 8.0 * n + 8.0 * (double)s->nnodes + 4.0 * s->M2 + 16.0 * H * s->M2;
   b[2] = 16.0 * H * s->M2 + 8.0 * H * (s->p2 / 2 + 1) + 16.0 * H * s->m2;
   b[3] = 16.0 * H * s->m2 + 8.0 * N * (double)p + 8.0 * N;
   return RK_OK;
@@ -1082,7 +1113,7 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
       if (it != w->hgraphs.end()) exec = it->second;
       else capture = graph_env && (++w->hseen[key] >= 2) && w->hgraphs.size() < 64;
     }
-    const int nk = 4 + (K - 1);
+    const int nk = kPredictKernels + (K - 1);
     if (!exec && !capture) {
       RK_TRY(enqueue(st));
     } else {

@@ -341,3 +341,35 @@ def test_recursive_factor_inverse_matches_oracle():
     assert r.returncode == 0, r.stderr[-2000:]
     d, s = (float(v) for v in r.stdout.split()[-2:])
     assert d < FIELD_TOL and s < FIELD_TOL, (d, s)
+
+
+_UNFUSED_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2605_29284_b200 as pk
+from paper_2605_29284_b200 import workloads
+wl = workloads.cfg2()
+model = pk.CovarianceModel(wl.sigma2, wl.alpha, wl.nu, wl.tau2)
+grid = pk.build_padded_grid(wl.domain, wl.dims, wl.L, wl.obs)
+st = pk.build_setup(model, grid, wl.L, wl.obs)
+xg = workloads.grid_covariates_for(grid.interior_nodes(), wl.grid_covariates)
+c = np.random.default_rng(2).normal(size=wl.obs.shape[0])
+np.save(sys.argv[2], pk.predict_rapid(st, c, [0.5, 1.0, -1.0], xg))
+"""
+
+
+def test_fused_and_standalone_scatter_identical(tmp_path):
+    """Pass 1 with the fused in-smem scatter and the standalone scatter kernel (forced with
+    RK_FUSED_GATHER=0) give bit-identical fields."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        f = str(tmp_path / f"f{flag}.npy")
+        r = subprocess.run([sys.executable, "-c", _UNFUSED_SCRIPT, root, f],
+                           env=dict(os.environ, RK_FUSED_GATHER=flag), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
