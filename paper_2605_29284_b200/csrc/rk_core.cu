@@ -80,9 +80,15 @@ const FftPlan& plan_pick(const FftPlan& normal, const FftPlan& wide, int64_t lin
   static const int mode = getenv("RK_WIDE") ? atoi(getenv("RK_WIDE")) : 1;   // 0 never, 1 auto, 2 always
   if (wide.n == 0 || mode == 0) return normal;
   if (mode == 2) return wide;
-  // wide while every line of the launch stays resident at once (148 SMs x 512 threads of a
-  // 128-register kernel); beyond that the extra threads only add waves
-  return wide.nthr > normal.nthr && lines * wide.nthr <= 148LL * 512 ? wide : normal;
+  // wide while every CTA of the launch is resident at once (a 128-register kernel holds 512
+  // threads per SM; shared memory as pick_lpc models it); beyond that it only adds waves
+  if (wide.nthr <= normal.nthr) return normal;
+  const int lpc = pick_lpc(wide, 4, lines);
+  const size_t line_bytes = (size_t)wide.n * sizeof(double2);
+  const int by_regs = 512 / (lpc * wide.nthr);
+  const int by_smem = (int)((227 * 1024) / (lpc * line_bytes + line_bytes / 8 + 64));
+  const int64_t resident = 148LL * std::min(by_regs, by_smem);
+  return ceil_div(lines, lpc) <= resident ? wide : normal;
 }
 
 // FFT kernels run at 128 registers/thread (__launch_bounds__(512, 1)), so an SM holds at

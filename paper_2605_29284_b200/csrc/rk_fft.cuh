@@ -35,7 +35,7 @@ struct FftPlan {
   int n;                       // transform length
   int nstages;
   int nthr;                    // threads cooperating on one line (multiple of 32)
-  int n9, r3, n8, r2;          // r3 in {1,3,6}, r2 in {1,2,4}
+  int n9, r3, n8, r2;          // r3 in {1,3,6}, r2 in {1,2,4,16}; 16 = two radix-4 stages
   int ntw;                     // entries of the stage twiddle table (sum of Ns > 1)
   const double2* tw;           // per-stage twiddles, see fft_stage_twiddles()
 };
@@ -313,8 +313,16 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
     if (Ns > 1) tw += Ns;
     Ns *= 8;
   }
-  if (pl.r2 == 2) fft_stage<2, INV, TWS>(buf, n, Ns, t, nthr, tw);
-  else if (pl.r2 == 4) fft_stage<4, INV, TWS>(buf, n, Ns, t, nthr, tw);
+  if (pl.r2 == 2) {
+    fft_stage<2, INV, TWS>(buf, n, Ns, t, nthr, tw);
+  } else if (pl.r2 >= 4) {
+#pragma unroll 1
+    for (int s = 0; s < (pl.r2 == 16 ? 2 : 1); ++s) {
+      fft_stage<4, INV, TWS>(buf, n, Ns, t, nthr, tw);
+      if (Ns > 1) tw += Ns;
+      Ns *= 4;
+    }
+  }
 }
 
 // ----------------------------------------------------------------- host planning
@@ -323,12 +331,17 @@ inline int fft_stage_list(const FftPlan& pl, int* rad) {
   for (int i = 0; i < pl.n9; ++i) rad[ns++] = 9;
   if (pl.r3 > 1) rad[ns++] = pl.r3;
   for (int i = 0; i < pl.n8; ++i) rad[ns++] = 8;
-  if (pl.r2 > 1) rad[ns++] = pl.r2;
+  if (pl.r2 == 16) {
+    rad[ns++] = 4;
+    rad[ns++] = 4;
+  } else if (pl.r2 > 1) {
+    rad[ns++] = pl.r2;
+  }
   return ns;
 }
 
 // n = 2^a 3^b -> 9^(b/2) * r3 * 8^(a'/3) * r2 with r3 = 3 or 6 (b odd; 6 absorbs one
-// factor 2 when a >= 1) and r2 = 2^(a' % 3).
+// factor 2 when a >= 1) and r2 = 2^(a' % 3), except that a trailing 8 * 2 becomes 4 * 4.
 // wide: for latency-bound launches with few lines, the same stages with one thread per
 // butterfly (nthr = max n/R, at most 512): measured on B200, a radix-9 stage of a 729-point
 // line takes ~1190 cycles with 2 butterflies per thread and ~700 with 1 (tools/fft_stage_lat),
@@ -348,6 +361,10 @@ inline bool fft_factor(int n, FftPlan* pl, bool wide = false) {
   }
   pl->n8 = a / 3;
   pl->r2 = 1 << (a % 3);
+  if (pl->r2 == 2 && pl->n8 >= 1) {   // 8 * 2 -> 4 * 4: a radix-2 stage has n/2 butterflies,
+    pl->n8 -= 1;                        // which caps the one-per-thread (wide) plans
+    pl->r2 = 16;
+  }
   int rad[FFT_MAX_STAGES];
   pl->nstages = fft_stage_list(*pl, rad);
   int need = 1;

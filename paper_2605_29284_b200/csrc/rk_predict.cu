@@ -186,20 +186,20 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
     const int nn = P1.x - n0, cnt = P1.z - e0;
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
     const int rowq = ya * g.M1;
-    for (int k = tl; k < nn; k += nthr) {   // node k: end of its products, its x | odd-row bit
-      const int q = __ldg(&g.node_q[n0 + k]) - rowq;
-      const int odd = n0 + k >= n1;
-      nrec[k] = make_int2(__ldg(&g.node_off[n0 + k + 1]) - e0, 2 * (q - odd * g.M1) + odd);
-    }
+    // one pass issues the contribution loads and the node-record loads together; only the
+    // coefficient loads depend on them
     constexpr int U = 4;
-    for (int i0 = tl; i0 < cnt; i0 += U * nthr) {
+    const int m = max(cnt, nn);
+    for (int i0 = tl; i0 < m; i0 += U * nthr) {
       double w[U];
-      int ci[U];
+      int ci[U], nq[U], ne[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i = i0 + u * nthr;
         w[u] = i < cnt ? __ldg(&g.ent_wv[e0 + i]) : 0.0;
         ci[u] = i < cnt ? __ldg(&g.ent_c[e0 + i]) : 0;
+        nq[u] = i < nn ? __ldg(&g.node_q[n0 + i]) : 0;
+        ne[u] = i < nn ? __ldg(&g.node_off[n0 + i + 1]) : 0;
       }
       double cv[U];
 #pragma unroll
@@ -208,6 +208,10 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
       for (int u = 0; u < U; ++u) {
         const int i = i0 + u * nthr;
         if (i < cnt) prod[i] = __dmul_rn(w[u], cv[u]);
+        if (i < nn) {   // node i: end of its products, its x | odd-row bit
+          const int odd = n0 + i >= n1;
+          nrec[i] = make_int2(ne[u] - e0, 2 * (nq[u] - rowq - odd * g.M1) + odd);
+        }
       }
     }
     __syncthreads();
@@ -914,7 +918,9 @@ extern "C" {
 // diagnostics: copies the 3 x 4096 x 8 phase timestamps (RK_PHASE_TIMING builds only)
 rk_status rk_phase_timestamps(unsigned long long* out) {
 #ifdef RK_PHASE_TIMING
-  return cudaMemcpyFromSymbol(out, g_phase_ts, sizeof(g_phase_ts)) == cudaSuccess ? RK_OK : RK_CUDA;
+  if (cudaMemcpyFromSymbol(out, g_phase_ts, sizeof(g_phase_ts)) != cudaSuccess) return RK_CUDA;
+  static const unsigned long long zero[3 * 4096 * 8] = {};   // next read shows only new launches
+  return cudaMemcpyToSymbol(g_phase_ts, zero, sizeof(zero)) == cudaSuccess ? RK_OK : RK_CUDA;
 #else
   (void)out;
   rk::set_error(RK_INTERNAL, "library built without RK_PHASE_TIMING");

@@ -19,6 +19,7 @@
 #include <cusolverDn.h>
 
 #include "rk_internal.cuh"
+#include "rk_ndtri.cuh"
 
 namespace rk {
 
@@ -60,10 +61,8 @@ __device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t stream, 
 }
 
 // integers(0, 2^53) == w >> 11 (Lemire, power-of-two range); u = (k + 0.5) / 2^53; ndtri(u)
-__device__ __forceinline__ double word_normal(uint64_t w) {
-  const double u = ((double)(w >> 11) + 0.5) * 0x1.0p-53;
-  return normcdfinv(u);
-}
+__device__ __forceinline__ double word_uniform(uint64_t w) { return ((double)(w >> 11) + 0.5) * 0x1.0p-53; }
+__device__ __forceinline__ double word_normal(uint64_t w) { return ndtri_b200(word_uniform(w)); }
 
 __global__ void philox_kernel(uint64_t seed, uint64_t stream, uint64_t start, int64_t count,
                               double* out_n, uint64_t* out_raw) {
@@ -257,29 +256,72 @@ struct CsRngArgs {
   int64_t Z_bstride;
 };
 
-__global__ void __launch_bounds__(256) cs_rng_kernel(const CsRngArgs a) {
+// Inverse normal with warp-level tail compaction: every lane evaluates the central rational
+// for its 8 normals; the ~8% tail values (log + sqrt + a second rational) are queued per warp
+// in shared memory and evaluated by all lanes together, so a warp pays one tail round per
+// iteration instead of running both branches for every lane.
+constexpr int kRngThreads = 256;
+
+__global__ void __launch_bounds__(kRngThreads) cs_rng_kernel(const CsRngArgs a) {
+  __shared__ double tq[kRngThreads / 32][8 * 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* wq = tq[wid];
   const int b = blockIdx.y;
   const uint64_t fs = a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
   const uint64_t Ps = (uint64_t)a.ps1 * (uint64_t)a.ps2;
   const uint64_t nblk = (Ps + 3) / 4;
   const int imoff = (int)(Ps & 3);
   double2* Z = a.Z + (int64_t)b * a.Z_bstride;
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nblk;
-       t += (uint64_t)gridDim.x * blockDim.x) {
+  // warp-uniform grid-stride loop (the compaction uses full-warp shuffles)
+  for (uint64_t t0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) - lane; t0 < nblk;
+       t0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = t0 + lane;
+    const bool valid = t < nblk;
     uint64_t re[4], im[8];
     philox4x64_10(t + 1, fs, 0, re);
     const uint64_t ib = (Ps + 4 * t) / 4;            // first block holding imaginary words
     philox4x64_10(ib + 1, fs, 0, im);
     if (imoff) philox4x64_10(ib + 2, fs, 0, im + 4);
+    double z[8];
+    unsigned tmask = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double u = word_uniform(q < 4 ? re[q] : im[imoff + q - 4]);
+      if (valid && ndtri_is_tail(u)) tmask |= 1u << q;
+      z[q] = tmask >> q & 1 ? u : ndtri_central(u);
+    }
+    // exclusive prefix of the tail counts across the warp
+    const int cnt = __popc(tmask);
+    int off = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;
+    if (total) {
+      int o = off;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) wq[o++] = z[q];
+      __syncwarp();
+      for (int k = lane; k < total; k += 32) wq[k] = ndtri_tail(wq[k]);
+      __syncwarp();
+      o = off;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) z[q] = wq[o++];
+      __syncwarp();
+    }
+    if (!valid) continue;
     uint64_t p = 4 * t;
     int iy = (int)(p / a.ps1), ix = (int)(p - (uint64_t)iy * a.ps1);
 #pragma unroll
     for (int q = 0; q < 4; ++q, ++p) {
       if (p < Ps) {
-        const double zr = word_normal(re[q]);
-        const double zi = word_normal(im[imoff + q]);
         const double r = __ldg(&a.root_q[(int64_t)min(iy, a.ps2 - iy) * a.rq_ld + min(ix, a.ps1 - ix)]);
-        Z[p] = make_double2(r * zr, r * zi);
+        Z[p] = make_double2(r * z[q], r * z[4 + q]);
       }
       if (++ix == a.ps1) { ix = 0; ++iy; }
     }
@@ -359,8 +401,8 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     ga.rq_ld = e.hs1;
     ga.Z = Z;
     ga.Z_bstride = Ps;
-    const dim3 rgrid((unsigned)std::min<int64_t>(ceil_div(ceil_div(Ps, 4), 256), 148 * 8), (unsigned)batch);
-    cs_rng_kernel<<<rgrid, 256, 0, st>>>(ga);
+    const dim3 rgrid((unsigned)std::min<int64_t>(ceil_div(ceil_div(Ps, 4), kRngThreads), 148 * 8), (unsigned)batch);
+    cs_rng_kernel<<<rgrid, kRngThreads, 0, st>>>(ga);
     count_launch();
     RK_LAUNCH_CHECK();
     CsFftArgs fa{};
