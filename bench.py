@@ -23,6 +23,7 @@ workload, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -250,7 +251,17 @@ def fft_flops(n):
     return n * sum(per_pt[r] for r in rad)
 
 
-def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind):
+def _ncu_traffic(cfg, kernel):
+    """dram read + write bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/round1_traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round1_traffic.json")) as f:
+            return json.load(f)["kernels"][cfg][kernel]["dram_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind, cfg=None):
     st = case["setup"]
     p1, p2 = st.embed_dims
     H1 = p1 // 2 + 1
@@ -264,7 +275,8 @@ def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind):
     fl = flops[dom] / (pass_ms[dom] * 1e-3) / 1e12
     return {
         "bound": "hbm", "kernel": names[dom], "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(ach / peak, 4), "traffic": None, "peak_source": peaks_kind,
+        "frac": round(ach / peak, 4), "traffic": _ncu_traffic(cfg, names[dom]), "peak_source": peaks_kind,
+        "traffic_source": "profiles/round1_traffic.json (ncu --set full, dram bytes per launch)",
         "algorithmic_bytes": float(pass_bytes[dom]), "kernel_ms": round(float(pass_ms[dom]), 5),
         "fp64_tflops": round(fl, 3), "fp64_peak_tflops": FP64_TFLOPS_MEASURED,
         "fp64_frac": round(fl / FP64_TFLOPS_MEASURED, 4),
@@ -287,12 +299,16 @@ def time_predict_e2e(pk, case, steps, warmup, flush):
     for k in range(max(warmup, 2 * len(ch) + 1)):
         pk.predict_rapid(st, ch[k % len(ch)], beta, xg, out=out)
     ms = []
-    for k in range(steps):
-        flush()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        pk.predict_rapid(st, ch[k % len(ch)], beta, xg, out=out)
-        ms.append((time.perf_counter() - t0) * 1e3)
+    gc.disable()   # host-side timing: keep collector pauses out of the per-call numbers
+    try:
+        for k in range(steps):
+            flush()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pk.predict_rapid(st, ch[k % len(ch)], beta, xg, out=out)
+            ms.append((time.perf_counter() - t0) * 1e3)
+    finally:
+        gc.enable()
     h2d = 8 * (ch[0].size + beta.size + (0 if xg is None else xg.size))
     return ms, h2d, 8 * m1 * m2
 
@@ -465,7 +481,7 @@ def main():
     N = wl.dims[0] * wl.dims[1]
     value = N * args.steps * world / (tot_ms * 1e-3)
     pass_ms, pass_bytes = profile_passes(pk, case, 10, flush)
-    e2e_ms, h2d, d2h = time_predict_e2e(pk, case, args.steps, args.warmup, flush)
+    e2e_ms, h2d, d2h = time_predict_e2e(pk, case, max(args.steps, 200), args.warmup, flush)   # host-timed: more samples
     e2e_tot = max_over_ranks(sum(e2e_ms), world)
     line = {
         "metric": "predicted grid points/s (fp64)", "value": round(value, 1), "unit": "points/s",
@@ -476,9 +492,9 @@ def main():
                    "embed": list(case["setup"].embed_dims), "padded": list(case["setup"].grid.total_dims),
                    "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}",
                    "setup_s": round(case["t_setup"], 4), "fit_s": round(case["t_fit"], 4)},
-        "e2e": {"value": round(N * args.steps * world / (e2e_tot * 1e-3), 1), "unit": "points/s",
+        "e2e": {"value": round(N * len(e2e_ms) * world / (e2e_tot * 1e-3), 1), "unit": "points/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "roofline": roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind),
+        "roofline": roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind, "cfg2"),
         "gpu_launches": int(launches),
         "clocks": {**clk.summary(), "window": "0.5 s soak of the same flushed predicts + the timed steps"},
     }
@@ -505,7 +521,7 @@ def main():
             "metric": "predicted grid points/s (fp64)", "value": round(N3 * len(ms3) * world / (t3 * 1e-3), 1),
             "unit": "points/s", "ms_per_predict": round(t3 / len(ms3), 4),
             "config": {"workload": "cfg3: n=20000, 2048x2048, L=4, nu=2.5", "embed": list(case3["setup"].embed_dims)},
-            "roofline": roofline_obj(case3, pm3, pb3, peaks, peaks_kind), "setup_s": round(case3["t_setup"], 3),
+            "roofline": roofline_obj(case3, pm3, pb3, peaks, peaks_kind, "cfg3"), "setup_s": round(case3["t_setup"], 3),
             "fit_s": round(case3["t_fit"], 3)}
         del case3
         torch.cuda.empty_cache()
