@@ -44,15 +44,15 @@ static int finish(const Status& s) {
 // ------------------------------------------------------------------- plans
 namespace {
 std::mutex g_plan_mu;
-std::map<std::pair<int, int>, FftPlan> g_plans;   // (device, n or -n for wide plans)
+std::map<std::pair<int, int>, FftPlan> g_plans;   // (device, 4 n + variant)
 std::map<std::pair<int, const void*>, bool> g_smem_set;
 }  // namespace
 
-Status plan_for(int n, FftPlan* out, bool wide) {
+Status plan_for(int n, FftPlan* out, int wide) {
   int dev = 0;
   RK_CUDA_TRY(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  auto key = std::make_pair(dev, wide ? -n : n);
+  auto key = std::make_pair(dev, n * 4 + wide);
   auto it = g_plans.find(key);
   if (it != g_plans.end()) {
     *out = it->second;
@@ -61,7 +61,7 @@ Status plan_for(int n, FftPlan* out, bool wide) {
   FftPlan pl{};
   if (!fft_factor(n, &pl, wide))
     return Status::err(RK_INTERNAL, "FFT length " + std::to_string(n) + " is not 2^a 3^b");
-  if (pl.nthr > 512)
+  if (pl.nthr > (wide == 2 ? 1024 : 512))
     return Status::err(RK_DOMAIN, "FFT length " + std::to_string(n) + " too large for one CTA");
   std::vector<double2> tw;
   fft_stage_twiddles(pl, tw, [](double c, double s) { return make_double2(c, s); });
@@ -76,23 +76,34 @@ Status plan_for(int n, FftPlan* out, bool wide) {
   return Status::ok();
 }
 
-const FftPlan& plan_pick(const FftPlan& normal, const FftPlan& wide, int64_t lines) {
-  static const int mode = getenv("RK_WIDE") ? atoi(getenv("RK_WIDE")) : 1;   // 0 never, 1 auto, 2 always
-  if (wide.n == 0 || mode == 0) return normal;
-  if (mode == 2) return wide;
-  // wide while every CTA of the launch is resident at once (a 128-register kernel holds 512
-  // threads per SM; shared memory as pick_lpc models it); beyond that it only adds waves
-  if (wide.nthr <= normal.nthr) return normal;
-  const int lpc = pick_lpc(wide, 4, lines);
-  const size_t line_bytes = (size_t)wide.n * sizeof(double2);
-  const int by_regs = 512 / (lpc * wide.nthr);
-  const int by_smem = (int)((227 * 1024) / (lpc * line_bytes + line_bytes / 8 + 64));
-  const int64_t resident = 148LL * std::min(by_regs, by_smem);
-  return ceil_div(lines, lpc) <= resident ? wide : normal;
+Status plan_set(int n, PlanSet* out) {
+  RK_TRY(plan_for(n, &out->v[0]));
+  // the variants keep the stage twiddle table in smem next to the line: n <= 4608
+  for (int w = 1; w <= 2; ++w)
+    if (n > 4608 || !plan_for(n, &out->v[w], w).good()) out->v[w] = FftPlan{};
+  return Status::ok();
+}
+
+const FftPlan& plan_pick(const PlanSet& ps, int64_t lines) {
+  // RK_WIDE: 0 normal only, 1 auto, 2 spread where available, 3 wide where available
+  static const int mode = getenv("RK_WIDE") ? atoi(getenv("RK_WIDE")) : 1;
+  const FftPlan& sp = ps.v[1];
+  const FftPlan& wd = ps.v[2];
+  if (mode == 0) return ps.v[0];
+  if (mode == 2) return sp.n ? sp : ps.v[0];
+  if (mode == 3) return wd.n ? wd : ps.v[0];
+  if (sp.n && sp.nthr > ps.v[0].nthr) {   // one wave with the spread plan?
+    const int lpc = pick_lpc(sp, 4, lines);
+    const size_t line_bytes = (size_t)sp.n * sizeof(double2);
+    const int by_regs = 512 / (lpc * sp.nthr);
+    const int by_smem = (int)((227 * 1024) / (lpc * line_bytes + line_bytes / 8 + 64));
+    if (ceil_div(lines, lpc) <= 148LL * std::min(by_regs, by_smem)) return sp;
+  }
+  return wd.n ? wd : ps.v[0];
 }
 
 // FFT kernels run at 128 registers/thread (__launch_bounds__(512, 1)), so an SM holds at
-// most 512 of their threads; pick the lines-per-CTA that maximises resident threads under
+// most 512 of their threads (1024 for the 64-register WIDE kernels); pick the lines-per-CTA that maximises resident threads under
 // that and the shared-memory limit (line buffers + ~1/8 for twiddles/staging), preferring
 // more lines per CTA on ties (wider coalesced transposed I/O), and never packing so much
 // that the launch has fewer than 2 CTAs per SM.
@@ -104,11 +115,12 @@ int pick_lpc(const FftPlan& pl, int max_lines, int64_t total_lines) {
   }();
   int best = 1;
   int64_t best_res = -1;
+  const int tmax = pl.wide == 2 ? 1024 : 512;   // resident FFT threads per SM (registers)
   for (int lpc = 1; lpc <= std::max(1, max_lines); ++lpc) {
     const int threads = lpc * pl.nthr;
     const size_t smem = lpc * line_bytes + line_bytes / 8 + 64;
-    if (threads > 512 || (lpc > 1 && (smem > cap || ceil_div(total_lines, lpc) < 2 * 148))) break;
-    const int by_regs = 512 / threads;
+    if (threads > tmax || (lpc > 1 && (smem > cap || ceil_div(total_lines, lpc) < 2 * 148))) break;
+    const int by_regs = tmax / threads;
     const int by_smem = (int)((227 * 1024) / smem);
     const int64_t res = (int64_t)std::min(by_regs, by_smem) * threads;
     if (res >= best_res) {
@@ -791,8 +803,8 @@ spectrum:
   s->Q2 = quarter_ld(s->p2);
   RK_TRY(plan_for(s->p1, &s->pl1));
   RK_TRY(plan_for(s->p2, &s->pl2));
-  if (!plan_for(s->p1, &s->pl1w, true).good()) s->pl1w = FftPlan{};   // n / 3 > 512 threads: none
-  if (!plan_for(s->p2, &s->pl2w, true).good()) s->pl2w = FftPlan{};
+  RK_TRY(plan_set(s->p1, &s->pl1v));
+  RK_TRY(plan_set(s->p2, &s->pl2v));
   RK_CUDA_TRY(cudaMalloc(&s->spec_q, sizeof(double) * (size_t)s->H1 * s->Q2));
   RK_TRY(spectrum_quarter(s->mat, grid->hx, grid->hy, s->p1, s->p2,
                           1.0 / ((double)s->p1 * (double)s->p2), s->spec_q, s->Q2, 0));

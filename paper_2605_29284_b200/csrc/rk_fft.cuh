@@ -37,6 +37,8 @@ struct FftPlan {
   int nthr;                    // threads cooperating on one line (multiple of 32)
   int n9, r3, n8, r2;          // r3 in {1,3,6}, r2 in {1,2,4,16}; 16 = two radix-4 stages
   int ntw;                     // entries of the stage twiddle table (sum of Ns > 1)
+  int wide;                    // 0 normal; 1 spread (one butterfly per thread, <= 512 threads);
+                               // 2 built for the WIDE kernels (fft_kmax_wide butterflies per thread)
   const double2* tw;           // per-stage twiddles, see fft_stage_twiddles()
 };
 
@@ -50,6 +52,10 @@ __device__ __forceinline__ FftPlan fft_twiddles_to_smem(const FftPlan& pl, doubl
 }
 
 // butterflies each thread keeps in registers for a stage of radix R
+// WIDE kernels (__launch_bounds__(1024): 64 registers) hold one radix-8/9 butterfly or two
+// smaller ones per thread, so a line spreads over up to 1024 threads and an SM keeps 32
+// FFT warps resident instead of 16
+__host__ __device__ constexpr int fft_kmax_wide(int r) { return r >= 8 ? 1 : 2; }
 __host__ __device__ constexpr int fft_kmax(int r) {
   return r == 2 ? 9 : r == 3 ? 6 : r == 4 ? 4 : r == 6 ? 3 : r == 8 ? 2 : r == 9 ? 2 : r == 12 ? 2 : 1;
 }
@@ -240,10 +246,10 @@ template <bool INV> struct Dft<36, INV> : DftPQ<4, 9, INV> {};
 // bandwidth the engine is bound by for FP64 work it has spare.  The whole table has
 // sum(Ns) entries (~n / R_last), small enough to stage in shared memory per CTA
 // (fft_twiddles_to_smem); warp loads are contiguous.  TWS: table in shared memory.
-template <int R, bool INV, bool TWS = false>
+template <int R, bool INV, bool TWS = false, bool WIDE = false>
 __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
                                           const double2* __restrict__ tw) {
-  constexpr int K = fft_kmax(R);
+  constexpr int K = WIDE ? fft_kmax_wide(R) : fft_kmax(R);
   const int nb = n / R;
   double2 a[K][R];
   int outb[K];
@@ -287,38 +293,38 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
 
 // Full transform of the line at `buf` by thread t (0 <= t < pl.nthr or idle beyond).
 // Must be called by every thread of the CTA (contains barriers).
-template <bool INV, bool TWS = false>
+template <bool INV, bool TWS = false, bool WIDE = false>
 __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t) {
   const int n = pl.n, nthr = pl.nthr;
   const double2* tw = pl.tw;   // stage 1 (Ns = 1) needs no twiddles and has no block
   int Ns = 1;
 #pragma unroll 1
   for (int s = 0; s < pl.n9; ++s) {
-    fft_stage<9, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
     if (Ns > 1) tw += Ns;
     Ns *= 9;
   }
   if (pl.r3 == 6) {
-    fft_stage<6, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
     if (Ns > 1) tw += Ns;
     Ns *= 6;
   } else if (pl.r3 == 3) {
-    fft_stage<3, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    fft_stage<3, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
     if (Ns > 1) tw += Ns;
     Ns *= 3;
   }
 #pragma unroll 1
   for (int s = 0; s < pl.n8; ++s) {
-    fft_stage<8, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    fft_stage<8, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
     if (Ns > 1) tw += Ns;
     Ns *= 8;
   }
   if (pl.r2 == 2) {
-    fft_stage<2, INV, TWS>(buf, n, Ns, t, nthr, tw);
+    fft_stage<2, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
   } else if (pl.r2 >= 4) {
 #pragma unroll 1
     for (int s = 0; s < (pl.r2 == 16 ? 2 : 1); ++s) {
-      fft_stage<4, INV, TWS>(buf, n, Ns, t, nthr, tw);
+      fft_stage<4, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
       if (Ns > 1) tw += Ns;
       Ns *= 4;
     }
@@ -342,12 +348,14 @@ inline int fft_stage_list(const FftPlan& pl, int* rad) {
 
 // n = 2^a 3^b -> 9^(b/2) * r3 * 8^(a'/3) * r2 with r3 = 3 or 6 (b odd; 6 absorbs one
 // factor 2 when a >= 1) and r2 = 2^(a' % 3), except that a trailing 8 * 2 becomes 4 * 4.
-// wide: for latency-bound launches with few lines, the same stages with one thread per
-// butterfly (nthr = max n/R, at most 512): measured on B200, a radix-9 stage of a 729-point
-// line takes ~1190 cycles with 2 butterflies per thread and ~700 with 1 (tools/fft_stage_lat),
-// and the line's gather / epilogue phases get more memory-level parallelism.  Splitting the
-// 9s into radix-3 stages instead was slower (6 stages x ~1100 cycles).
-inline bool fft_factor(int n, FftPlan* pl, bool wide = false) {
+// wide = 1 ("spread"): for latency-bound launches with few lines, the same stages with one
+// thread per butterfly (nthr = max n/R, at most 512) in the 128-register kernels: measured on
+// B200, a radix-9 stage of a 729-point line takes ~1190 cycles with 2 butterflies per thread
+// and ~700 with 1 (tools/fft_stage_lat), and the gather / epilogue phases get more
+// memory-level parallelism.  Splitting the 9s into radix-3 stages was slower (6 x ~1100).
+// wide = 2: for the 64-register WIDE kernels (fft_kmax_wide), up to 1024 threads per line
+// and 1024 resident FFT threads per SM, for launches that do not fit the GPU in one wave.
+inline bool fft_factor(int n, FftPlan* pl, int wide = 0) {
   int a = 0, b = 0, m = n;
   if (n < 1) return false;
   while (m % 2 == 0) { m /= 2; ++a; }
@@ -373,11 +381,19 @@ inline bool fft_factor(int n, FftPlan* pl, bool wide = false) {
     const int k = fft_kmax(rad[i]);
     need = need > (nb + k - 1) / k ? need : (nb + k - 1) / k;
   }
-  if (wide) {   // one butterfly per thread where 512 threads allow it
+  if (wide == 1) {   // one butterfly per thread where 512 threads allow it
     int mx = 1;
     for (int i = 0; i < pl->nstages; ++i) mx = mx > n / rad[i] ? mx : n / rad[i];
     need = need > (mx < 512 ? mx : 512) ? need : (mx < 512 ? mx : 512);
+  } else if (wide == 2) {   // fft_kmax_wide butterflies per thread, up to 1024 threads per line
+    need = 1;
+    for (int i = 0; i < pl->nstages; ++i) {
+      const int nb = n / rad[i];
+      const int k = fft_kmax_wide(rad[i]);
+      need = need > (nb + k - 1) / k ? need : (nb + k - 1) / k;
+    }
   }
+  pl->wide = wide;
   pl->nthr = (need + 31) / 32 * 32;
   if (pl->nthr < 32) pl->nthr = 32;
   return true;

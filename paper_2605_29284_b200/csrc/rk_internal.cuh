@@ -13,10 +13,15 @@ namespace rk {
 
 // --------------------------------------------------------------- bookkeeping
 void count_launch(int k = 1);
-Status plan_for(int n, FftPlan* out, bool wide = false);   // cached per (device, n, wide)
-// the wide plan of n when a launch of `lines` lines cannot fill the GPU with the normal
-// plan's threads (latency-bound small grids), else the normal plan
-const FftPlan& plan_pick(const FftPlan& normal, const FftPlan& wide, int64_t lines);
+Status plan_for(int n, FftPlan* out, int wide = 0);   // cached per (device, n, wide)
+// the plan variants of one length: v[0] normal, v[1] spread, v[2] wide (n == 0 if absent)
+struct PlanSet {
+  FftPlan v[3] = {};
+};
+Status plan_set(int n, PlanSet* out);
+// spread while the launch's CTAs are all resident at once (latency-bound small grids), else
+// wide (64-register kernels, twice the resident warps), else normal
+const FftPlan& plan_pick(const PlanSet& ps, int64_t lines);
 // lines per CTA for a kernel: pack up to max_lines, but only while the launch still has
 // >= 2 CTAs per SM for `total_lines` lines (small grids are latency bound, not occupancy)
 int pick_lpc(const FftPlan& pl, int max_lines, int64_t total_lines = (int64_t)1 << 40);
@@ -32,6 +37,7 @@ struct Embedding {
   int ps1 = 0, ps2 = 0, doubled = 0;
   int hs1 = 0, qs2 = 0;          // ps1/2+1, ps2/2+1
   FftPlan pl1{}, pl2{};
+  PlanSet ps1v, ps2v;            // all plan variants of ps1 / ps2
   double* root_q = nullptr;      // (qs2, hs1) row-major: sqrt(clip(lambda,0)) * sqrt(P)/P
 };
 
@@ -95,7 +101,7 @@ struct rk_setup {
   double px0 = 0, py0 = 0;
   int p1 = 0, p2 = 0, H1 = 0, Q2 = 0;
   rk::FftPlan pl1{}, pl2{};
-  rk::FftPlan pl1w{}, pl2w{};   // wide variants (n == 0 if none), see plan_pick
+  rk::PlanSet pl1v, pl2v;       // all plan variants of p1 / p2, see plan_pick
   // device arrays
   double* obs = nullptr;        // (n, 2)
   int32_t* base = nullptr;      // (n) flat padded index of block entry 0

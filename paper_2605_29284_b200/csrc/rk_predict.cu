@@ -101,8 +101,11 @@ struct RowFwdArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
-template <int SRC, bool TWS>
-__global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
+// FFT kernels: WIDE instantiations run 64-register threads (fft_kmax_wide butterflies each)
+#define RK_FFT_BOUNDS(WIDE) __launch_bounds__((WIDE) ? 1024 : 512, 1)
+
+template <int SRC, bool TWS, bool WIDE>
+__global__ void RK_FFT_BOUNDS(WIDE) row_fwd_kernel(const RowFwdArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(512, 1) row_fwd_kernel(const RowFwdArgs a) {
   }
   __syncthreads();
   RK_PHASE(0, 2);
-  fft_line<false, TWS>(buf, pls, tl);
+  fft_line<false, TWS, WIDE>(buf, pls, tl);
   RK_PHASE(0, 3);
   pdl_trigger();   // the column pass may start staging while the split rows are stored
   // split Z = FFT(u + i v) into U = (Z + conj Z[-k]) / 2, V = (Z - conj Z[-k]) / 2i
@@ -275,8 +278,8 @@ struct ColArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
-template <int MODE, bool TWS>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
-__global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
+template <int MODE, bool TWS, bool WIDE>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
+__global__ void RK_FFT_BOUNDS(WIDE) col_kernel(const ColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -317,13 +320,13 @@ __global__ void __launch_bounds__(512, 1) col_kernel(const ColArgs a) {
   mbar_wait(bar, 0);
   __syncthreads();
   RK_PHASE(1, 1);
-  fft_line<false, TWS>(buf, pls, tl);
+  fft_line<false, TWS, WIDE>(buf, pls, tl);
   RK_PHASE(1, 2);
   if (MODE == 0) {
     const double* S = specs + (size_t)line * a.ldq;
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     __syncthreads();
-    fft_line<true, TWS>(buf, pls, tl);
+    fft_line<true, TWS, WIDE>(buf, pls, tl);
     RK_PHASE(1, 3);
     pdl_trigger();
     // TMA bulk store of the kept rows
@@ -370,8 +373,8 @@ struct RowInvArgs {
   int xg_bulk;               // X_g is 16-byte aligned: one TMA bulk copy per CTA
 };
 
-template <bool TWS>
-__global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
+template <bool TWS, bool WIDE>
+__global__ void RK_FFT_BOUNDS(WIDE) row_inv_kernel(const RowInvArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(512, 1) row_inv_kernel(const RowInvArgs a) {
   __syncthreads();
   RK_PHASE(2, 2);
   double2* buf = smem + (size_t)line * n;
-  fft_line<true, TWS>(buf, pls, tl);
+  fft_line<true, TWS, WIDE>(buf, pls, tl);
   if (xwait) mbar_wait(bar, 0);   // init is ordered by the barrier above
   RK_PHASE(2, 3);
   const int ya = 2 * (blockIdx.x * a.lpc + line);
@@ -490,6 +493,11 @@ static inline size_t with_tw(size_t bytes_before, const FftPlan& pl) {
 // the table is staged in smem when it fits next to the lines (else read through L1/L2)
 static constexpr size_t kSmemMax = 227 * 1024;
 static inline bool tw_fits(size_t bytes_before, const FftPlan& pl) { return with_tw(bytes_before, pl) <= kSmemMax; }
+// WIDE kernels are only instantiated with the table in smem (wide plans exist for n <= 4608)
+static inline Status wide_needs_tws(const FftPlan& pl, bool tws) {
+  if (pl.wide == 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+  return Status::ok();
+}
 
 static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStream_t st) {
   RowFwdArgs a = a0;
@@ -505,9 +513,13 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStrea
   a.tw_off = tw_slot(smem);
   const bool tws = tw_fits(smem, a.pl);
   if (tws) smem = with_tw(smem, a.pl);
-  auto kern = src == SRC_ROWS   ? (tws ? row_fwd_kernel<SRC_ROWS, true> : row_fwd_kernel<SRC_ROWS, false>)
-              : src == SRC_LAG ? (tws ? row_fwd_kernel<SRC_LAG, true> : row_fwd_kernel<SRC_LAG, false>)
-                               : (tws ? row_fwd_kernel<SRC_SPARSE, true> : row_fwd_kernel<SRC_SPARSE, false>);
+  RK_TRY(wide_needs_tws(a.pl, tws));
+  auto kern = a.pl.wide == 2 ? (src == SRC_ROWS ? row_fwd_kernel<SRC_ROWS, true, true>
+                           : src == SRC_LAG ? row_fwd_kernel<SRC_LAG, true, true>
+                                            : row_fwd_kernel<SRC_SPARSE, true, true>)
+              : src == SRC_ROWS ? (tws ? row_fwd_kernel<SRC_ROWS, true, false> : row_fwd_kernel<SRC_ROWS, false, false>)
+              : src == SRC_LAG  ? (tws ? row_fwd_kernel<SRC_LAG, true, false> : row_fwd_kernel<SRC_LAG, false, false>)
+                                : (tws ? row_fwd_kernel<SRC_SPARSE, true, false> : row_fwd_kernel<SRC_SPARSE, false, false>);
   RK_TRY(set_smem_attr((const void*)kern, smem));
   RK_CUDA_TRY(launch_pdl(kern, grid, dim3(threads), smem, st, a));
   count_launch();
@@ -524,8 +536,10 @@ static Status launch_col(int mode, const ColArgs& a0, int batch, cudaStream_t st
   a.tw_off = tw_slot(smem);
   const bool tws = tw_fits(smem, a.pl);
   if (tws) smem = with_tw(smem, a.pl);
-  auto kern = mode == 0 ? (tws ? col_kernel<0, true> : col_kernel<0, false>)
-                        : (tws ? col_kernel<1, true> : col_kernel<1, false>);
+  RK_TRY(wide_needs_tws(a.pl, tws));
+  auto kern = a.pl.wide == 2 ? (mode == 0 ? col_kernel<0, true, true> : col_kernel<1, true, true>)
+              : mode == 0 ? (tws ? col_kernel<0, true, false> : col_kernel<0, false, false>)
+                          : (tws ? col_kernel<1, true, false> : col_kernel<1, false, false>);
   RK_TRY(set_smem_attr((const void*)kern, smem));
   RK_CUDA_TRY(launch_pdl(kern, grid, dim3(threads), smem, st, a));
   count_launch();
@@ -549,7 +563,8 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
   a.tw_off = tw_slot(smem);
   const bool tws = tw_fits(smem, a.pl);
   if (tws) smem = with_tw(smem, a.pl);
-  auto kern = tws ? row_inv_kernel<true> : row_inv_kernel<false>;
+  RK_TRY(wide_needs_tws(a.pl, tws));
+  auto kern = a.pl.wide == 2 ? row_inv_kernel<true, true> : tws ? row_inv_kernel<true, false> : row_inv_kernel<false, false>;
   RK_TRY(set_smem_attr((const void*)kern, smem));
   RK_CUDA_TRY(launch_pdl(kern, grid, dim3(a.lpc * a.pl.nthr), smem, st, a));
   count_launch();
@@ -693,7 +708,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     U = ws->U;
   }
   RowFwdArgs ra{};
-  ra.pl = plan_pick(s->pl1, s->pl1w, (int64_t)((s->M2 + 1) / 2) * batch);
+  ra.pl = plan_pick(s->pl1v, (int64_t)((s->M2 + 1) / 2) * batch);
   ra.lpc = pick_lpc(ra.pl, 4, (int64_t)((s->M2 + 1) / 2) * batch);
   ra.nrows = s->M2;
   ra.ncols = s->M1;
@@ -715,7 +730,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   RK_TRY(launch_row_fwd(sp ? SRC_SPARSE : SRC_ROWS, ra, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[2], st));
   ColArgs ca{};
-  ca.pl = plan_pick(s->pl2, s->pl2w, (int64_t)s->H1 * batch);
+  ca.pl = plan_pick(s->pl2v, (int64_t)s->H1 * batch);
   ca.lpc = pick_lpc(ca.pl, 4, (int64_t)s->H1 * batch);
   ca.ncols = s->H1;
   ca.nin = s->M2;
@@ -732,7 +747,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   RK_TRY(launch_col(0, ca, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
   RowInvArgs ia = epi;
-  ia.pl = plan_pick(s->pl1, s->pl1w, (int64_t)((nout + 1) / 2) * batch);
+  ia.pl = plan_pick(s->pl1v, (int64_t)((nout + 1) / 2) * batch);
   ia.lpc = pick_lpc(ia.pl, 4, (int64_t)((nout + 1) / 2) * batch);
   ia.nrows = nout;
   ia.U = U;
@@ -963,6 +978,8 @@ rk_status rk_convolve_spectrum(const double* spec_q_dev, int32_t p1, int32_t p2,
     t.spec_q = const_cast<double*>(spec_q_dev);
     RK_TRY(plan_for(p1, &t.pl1));
     RK_TRY(plan_for(p2, &t.pl2));
+    RK_TRY(plan_set(p1, &t.pl1v));
+    RK_TRY(plan_set(p2, &t.pl2v));
     RowInvArgs e{};
     e.out = out_dev;
     e.ldo = M1;

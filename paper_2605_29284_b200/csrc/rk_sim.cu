@@ -87,8 +87,8 @@ struct CsColArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
-template <bool TWS>
-__global__ void __launch_bounds__(512, 1) cs_col_kernel(const CsColArgs a) {
+template <bool TWS, bool WIDE>
+__global__ void __launch_bounds__(WIDE ? 1024 : 512, 1) cs_col_kernel(const CsColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(512, 1) cs_col_kernel(const CsColArgs a) {
   pdl_wait();   // V is the predecessor's output
   for (int y = tl; y < n; y += nthr) buf[y] = ix < a.ncols ? V[y] : make_double2(0.0, 0.0);
   __syncthreads();
-  fft_line<true, TWS>(buf, pls, tl);
+  fft_line<true, TWS, WIDE>(buf, pls, tl);
   double* g = a.g + (int64_t)b * a.g_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, y = idx / a.lpc;
@@ -219,6 +219,8 @@ Status ensure_embedding(rk_setup* s, cudaStream_t st) {
       e.qs2 = qs2;
       RK_TRY(plan_for(e.ps1, &e.pl1));
       RK_TRY(plan_for(e.ps2, &e.pl2));
+      RK_TRY(plan_set(e.ps1, &e.ps1v));
+      RK_TRY(plan_set(e.ps2, &e.ps2v));
       RK_CUDA_TRY(cudaMalloc(&e.root_q, sizeof(double) * (size_t)hs1 * qs2));
       const double P = (double)p1 * (double)p2;
       root_q_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)hs1 * qs2, 256), 148 * 32), 256, 0, st>>>(
@@ -342,8 +344,8 @@ struct CsFftArgs {
   int tw_off;
 };
 
-template <bool TWS>
-__global__ void __launch_bounds__(512, 1) cs_rowfft_kernel(const CsFftArgs a) {
+template <bool TWS, bool WIDE>
+__global__ void __launch_bounds__(WIDE ? 1024 : 512, 1) cs_rowfft_kernel(const CsFftArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(512, 1) cs_rowfft_kernel(const CsFftArgs a) {
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
-  fft_line<true, TWS>(buf, pls, tl);
+  fft_line<true, TWS, WIDE>(buf, pls, tl);
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, ix = idx / a.lpc;
@@ -406,8 +408,8 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     count_launch();
     RK_LAUNCH_CHECK();
     CsFftArgs fa{};
-    fa.pl = e.pl1;
-    fa.lpc = pick_lpc(e.pl1, 4, (int64_t)e.ps2 * batch);
+    fa.pl = plan_pick(e.ps1v, (int64_t)e.ps2 * batch);
+    fa.lpc = pick_lpc(fa.pl, 4, (int64_t)e.ps2 * batch);
     fa.ps2 = e.ps2;
     fa.keep = s->M1;
     fa.Z = Z;
@@ -417,18 +419,19 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     fa.V_bstride = (int64_t)s->M1 * ldV;
     const dim3 grid((unsigned)ceil_div(e.ps2, fa.lpc), (unsigned)batch);
     fa.tw_off = (int)(fa.lpc * (size_t)e.ps1) + 1;
-    size_t smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1 + e.pl1.ntw);
+    size_t smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1 + fa.pl.ntw);
     const bool tws = smem <= 227 * 1024;   // else twiddles are read through L1/L2
     if (!tws) smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1);
-    auto kern = tws ? cs_rowfft_kernel<true> : cs_rowfft_kernel<false>;
+    if (fa.pl.wide == 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+    auto kern = fa.pl.wide == 2 ? cs_rowfft_kernel<true, true> : tws ? cs_rowfft_kernel<true, false> : cs_rowfft_kernel<false, false>;
     RK_TRY(set_smem_attr((const void*)kern, smem));
-    RK_CUDA_TRY(launch_pdl(kern, grid, dim3(fa.lpc * e.pl1.nthr), smem, st, fa));
+    RK_CUDA_TRY(launch_pdl(kern, grid, dim3(fa.lpc * fa.pl.nthr), smem, st, fa));
     count_launch();
     Zs = Z;
   }
   CsColArgs ca{};
-  ca.pl = e.pl2;
-  ca.lpc = pick_lpc(e.pl2, 4, (int64_t)s->M1 * batch);
+  ca.pl = plan_pick(e.ps2v, (int64_t)s->M1 * batch);
+  ca.lpc = pick_lpc(ca.pl, 4, (int64_t)s->M1 * batch);
   ca.ncols = s->M1;
   ca.keep = s->M2;
   ca.V = V;
@@ -439,12 +442,13 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   {
     const dim3 grid((unsigned)ceil_div(s->M1, ca.lpc), (unsigned)batch);
     ca.tw_off = (int)(ca.lpc * (size_t)e.ps2);
-    size_t smem = sizeof(double2) * (e.ps2 * (size_t)ca.lpc + e.pl2.ntw);
+    size_t smem = sizeof(double2) * (e.ps2 * (size_t)ca.lpc + ca.pl.ntw);
     const bool tws = smem <= 227 * 1024;
     if (!tws) smem = sizeof(double2) * e.ps2 * (size_t)ca.lpc;
-    auto kern = tws ? cs_col_kernel<true> : cs_col_kernel<false>;
+    if (ca.pl.wide == 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+    auto kern = ca.pl.wide == 2 ? cs_col_kernel<true, true> : tws ? cs_col_kernel<true, false> : cs_col_kernel<false, false>;
     RK_TRY(set_smem_attr((const void*)kern, smem));
-    RK_CUDA_TRY(launch_pdl(kern, grid, dim3(ca.lpc * e.pl2.nthr), smem, st, ca));
+    RK_CUDA_TRY(launch_pdl(kern, grid, dim3(ca.lpc * ca.pl.nthr), smem, st, ca));
     count_launch();
   }
   scratch_free(Zs, st);
