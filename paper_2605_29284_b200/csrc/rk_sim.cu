@@ -270,28 +270,40 @@ __global__ void __launch_bounds__(kRngThreads) cs_rng_kernel(const CsRngArgs a) 
   double* wq = tq[wid];
   const int b = blockIdx.y;
   const uint64_t fs = a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
-  const uint64_t Ps = (uint64_t)a.ps1 * (uint64_t)a.ps2;
-  const uint64_t nblk = (Ps + 3) / 4;
+  // 32-bit indexing (the host checks Ps < 2^31); (iy, ix) of word 4t advance incrementally
+  const uint32_t Ps = (uint32_t)a.ps1 * (uint32_t)a.ps2;
+  const uint32_t nblk = (Ps + 3) / 4, ps4 = Ps / 4;
   const int imoff = (int)(Ps & 3);
   double2* Z = a.Z + (int64_t)b * a.Z_bstride;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t dstep = 4 * stride;
+  const int dy = (int)(dstep / (uint32_t)a.ps1), dx = (int)(dstep % (uint32_t)a.ps1);
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  int iy = (int)(4 * t / (uint32_t)a.ps1), ix = (int)(4 * t - (uint32_t)iy * a.ps1);
   // warp-uniform grid-stride loop (the compaction uses full-warp shuffles)
-  for (uint64_t t0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) - lane; t0 < nblk;
-       t0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t t = t0 + lane;
+  for (uint32_t t0 = t - lane; t0 < nblk; t0 += stride, t += stride) {
     const bool valid = t < nblk;
     uint64_t re[4], im[8];
-    philox4x64_10(t + 1, fs, 0, re);
-    const uint64_t ib = (Ps + 4 * t) / 4;            // first block holding imaginary words
+    philox4x64_10((uint64_t)t + 1, fs, 0, re);
+    const uint64_t ib = (uint64_t)ps4 + t;          // first block holding imaginary words
     philox4x64_10(ib + 1, fs, 0, im);
     if (imoff) philox4x64_10(ib + 2, fs, 0, im + 4);
-    double z[8];
+    double uu[8], z[8];
     unsigned tmask = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const double u = word_uniform(q < 4 ? re[q] : im[imoff + q - 4]);
-      if (valid && ndtri_is_tail(u)) tmask |= 1u << q;
-      z[q] = tmask >> q & 1 ? u : ndtri_central(u);
+      // im[imoff + q - 4] with compile-time indices only (a runtime index would put im in
+      // local memory)
+      const int k = q - 4;
+      const uint64_t w = q < 4 ? re[q]
+                       : imoff == 0 ? im[k] : imoff == 1 ? im[k + 1] : imoff == 2 ? im[k + 2] : im[k + 3];
+      uu[q] = word_uniform(w);
+      if (valid && ndtri_is_tail(uu[q])) tmask |= 1u << q;
     }
+    ndtri_central_n<8>(uu, z);   // tails are replaced below
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (tmask >> q & 1) z[q] = uu[q];
     // exclusive prefix of the tail counts across the warp
     const int cnt = __popc(tmask);
     int off = cnt;
@@ -316,16 +328,26 @@ __global__ void __launch_bounds__(kRngThreads) cs_rng_kernel(const CsRngArgs a) 
         if (tmask >> q & 1) z[q] = wq[o++];
       __syncwarp();
     }
-    if (!valid) continue;
-    uint64_t p = 4 * t;
-    int iy = (int)(p / a.ps1), ix = (int)(p - (uint64_t)iy * a.ps1);
+    if (valid) {
+      uint32_t p = 4 * t;
+      int jy = iy, jx = ix;
 #pragma unroll
-    for (int q = 0; q < 4; ++q, ++p) {
-      if (p < Ps) {
-        const double r = __ldg(&a.root_q[(int64_t)min(iy, a.ps2 - iy) * a.rq_ld + min(ix, a.ps1 - ix)]);
-        Z[p] = make_double2(r * z[q], r * z[4 + q]);
+      for (int q = 0; q < 4; ++q, ++p) {
+        if (p < Ps) {
+          const double r = __ldg(&a.root_q[min(jy, a.ps2 - jy) * a.rq_ld + min(jx, a.ps1 - jx)]);
+          Z[p] = make_double2(r * z[q], r * z[4 + q]);
+        }
+        if (++jx == a.ps1) {
+          jx = 0;
+          ++jy;
+        }
       }
-      if (++ix == a.ps1) { ix = 0; ++iy; }
+    }
+    ix += dx;
+    iy += dy;
+    if (ix >= a.ps1) {
+      ix -= a.ps1;
+      ++iy;
     }
   }
 }
@@ -391,6 +413,7 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   double2* Zs = nullptr;   // freed after the column pass so the two FFT kernels stay adjacent
   {
     const int64_t Ps = (int64_t)e.ps1 * e.ps2;
+    if (Ps >= (int64_t)1 << 31) return Status::err(RK_DOMAIN, "simulation torus larger than 2^31 nodes");
     double2* Z = nullptr;
     RK_TRY(scratch_alloc((void**)&Z, sizeof(double2) * (size_t)Ps * batch, st));
     CsRngArgs ga{};

@@ -16,7 +16,7 @@ def _consts():
     scal = {m.group(1): float.fromhex(m.group(2))
             for m in re.finditer(r"constexpr double (\w+) = (\S+);", src)}
     arrs = {}
-    for m in re.finditer(r"const double (\w+)\[\d+\] = \{(.*?)\};", src, re.S):
+    for m in re.finditer(r"__constant__ (?:const )?double (\w+)\[\d+\] = \{(.*?)\};", src, re.S):
         arrs[m.group(1)] = [float.fromhex(t.split("/*")[0].strip()) for t in m.group(2).split(",")]
     return scal, arrs
 
