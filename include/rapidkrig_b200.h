@@ -157,6 +157,17 @@ rk_status rk_fit_info(const rk_fit* f, int64_t* n, int32_t* p);
 rk_status rk_refit_dev(const rk_fit* f, const double* z_dev, int64_t batch, double* beta_dev,
                        double* c_dev, void* stream);
 
+/* predict_exact (exact.py:132-147): out[t] = x_t . beta + sum_i cov(|t - obs_i|) c_i for
+ * targets_dev (nt, 2); xt_dev (nt, p) row-major, or NULL for an intercept-only fit, whose
+ * target covariate is x00 = X[0, 0] (exact.py:116-121).  Fixed summation order (index order). */
+rk_status rk_predict_exact(const rk_fit* f, const double* targets_dev, int64_t nt, const double* xt_dev,
+                           double x00, double* out_dev, void* stream);
+/* kriging_se_exact (exact.py:150-175): sqrt(sigma2 - k'M^-1 k + h'(X'M^-1X)^-1 h) per target,
+ * h = x_t - k'M^-1 X; processed `chunk` targets at a time (<= 0: 4000); RK_NUMERIC
+ * "negative prediction variance ..." below -1e-10, values in [-1e-10, 0) clamp to 0. */
+rk_status rk_kriging_se_exact(rk_fit* f, const double* targets_dev, int64_t nt, const double* xt_dev,
+                              double x00, int64_t chunk, double* out_dev, void* stream);
+
 /* ---- L3: conditional simulation (simulate.py:52-192) -------------------- */
 /* seed ^ splitmix64(j)  (simulate.py:52-62) */
 uint64_t rk_draw_seed(uint64_t seed, uint64_t j);

@@ -192,6 +192,29 @@ def gen_cs():
          embed=np.array([p1, p2]), g=g)
 
 
+def gen_exact_targets():
+    """predict_exact / kriging_se_exact (exact.py:132-175) at scattered targets, for a fit with
+    covariates [1, x, y] (nu = 1.0, Bessel path) and an intercept-only fit (nu = 2.5); targets
+    include observation locations themselves and points outside the data hull."""
+    rng = np.random.default_rng(77)
+    out = {}
+    for tag, nu, p in (("cov", 1.0, 3), ("icpt", 2.5, 1)):
+        obs = rng.uniform(0, 1, size=(160, 2))
+        X = np.column_stack([np.ones(160), obs]) if p == 3 else None
+        model = rk.CovarianceModel(sigma2=1.3, alpha=6.0, nu=nu, tau2=0.04)
+        z = 0.5 + np.sin(5 * obs[:, 0]) * np.cos(3 * obs[:, 1]) + rng.normal(0, 0.2, 160)
+        krig = rk.fit(model, obs, z, X)
+        tg = np.vstack([rng.uniform(-0.1, 1.1, size=(400, 2)), obs[:20]])
+        xt = np.column_stack([np.ones(len(tg)), tg]) if p == 3 else None
+        out.update({f"{tag}_obs": obs, f"{tag}_z": z, f"{tag}_nu": nu, f"{tag}_targets": tg,
+                    f"{tag}_xt": xt if xt is not None else np.zeros((0, 0)),
+                    f"{tag}_X": X if X is not None else np.zeros((0, 0)),
+                    f"{tag}_chol": krig.chol_M, f"{tag}_beta": krig.beta_hat, f"{tag}_c": krig.c,
+                    f"{tag}_pred": rk.predict_exact(krig, tg, xt),
+                    f"{tag}_se": rk.kriging_se_exact(krig, tg, xt)})
+    save("exact_targets", sigma2=1.3, alpha=6.0, tau2=0.04, **out)
+
+
 def gen_misc():
     ks = np.arange(1, 1200)
     save("fft_len", n=ks, p=np.array([rapid.next_fft_len(int(k)) for k in ks]))
@@ -205,5 +228,6 @@ if __name__ == "__main__":
     gen_rng()
     gen_cs()
     gen_misc()
+    gen_exact_targets()
     gen_config("cfg1")
     gen_config("cfg2")

@@ -536,6 +536,38 @@ def refit(fit: Fit, z):
     return gls(fit.chol_M, fit.X, z)
 
 
+def target_covariates(fit: Fit, targets, xt):
+    """exact.py:116-129."""
+    if xt is None:
+        if not (fit.X.shape[1] == 1 and np.all(fit.X == fit.X[0, 0])):
+            raise OracleDomainError("fit uses nontrivial covariates")
+        return np.full((targets.shape[0], 1), fit.X[0, 0])
+    xt = np.asarray(xt, dtype=float)
+    return xt[:, None] if xt.ndim == 1 else xt
+
+
+def predict_exact(fit: Fit, targets, xt=None):
+    """exact.py:132-147: X_t beta + k_t c (one block; the reference chunks only for memory)."""
+    targets = np.asarray(targets, dtype=float).reshape(-1, 2)
+    xt = target_covariates(fit, targets, xt)
+    return cov_dense(fit.model, targets, fit.obs) @ fit.c + xt @ fit.beta
+
+
+def kriging_se_exact(fit: Fit, targets, xt=None):
+    """exact.py:150-175: sqrt(sigma2 - k'M^-1 k + h'(B'B)^-1 h), h = x_t - u'B, u = L^-1 k."""
+    targets = np.asarray(targets, dtype=float).reshape(-1, 2)
+    xt = target_covariates(fit, targets, xt)
+    b = scipy.linalg.solve_triangular(fit.chol_M, fit.X, lower=True)
+    g = scipy.linalg.cho_factor(b.T @ b, lower=True)
+    u = scipy.linalg.solve_triangular(fit.chol_M, cov_dense(fit.model, targets, fit.obs).T, lower=True)
+    var = fit.model.sigma2 - np.einsum("ij,ij->j", u, u)
+    h = xt - u.T @ b
+    var += np.einsum("ij,ji->i", h, scipy.linalg.cho_solve(g, h.T))
+    if np.any(var < -1.0e-10):
+        raise OracleNumericError(f"negative prediction variance {var.min():.3e}")
+    return np.sqrt(np.clip(var, 0.0, None))
+
+
 # --------------------------------------------------------------------------
 # randomness  (simulate.py:52-74)
 # --------------------------------------------------------------------------

@@ -9,7 +9,7 @@ C ABI, include/rapidkrig_b200.h); there is no CPU fallback.
 
 from .covariance import CovarianceModel, cov, cov_matrix, matern_phi
 from .errors import DomainError, InternalError, NumericError, RapidKrigError
-from .exact import KrigingFit, as_device_fit, fit, refit_coefficients
+from .exact import KrigingFit, as_device_fit, fit, kriging_se_exact, predict_exact, refit_coefficients
 from .gridding import (NODE_SNAP_TOL, Neighborhood, PaddedGrid, build_padded_grid,
                        fill_distance, neighborhood)
 from .rapid import (RapidSetup, build_filter_spectrum, build_setup, convolve_filter,
@@ -23,7 +23,7 @@ __version__ = "0.1.0"
 __all__ = [
     "CovarianceModel", "cov", "cov_matrix", "matern_phi",
     "RapidKrigError", "DomainError", "NumericError", "InternalError",
-    "KrigingFit", "fit", "refit_coefficients", "as_device_fit",
+    "KrigingFit", "fit", "refit_coefficients", "predict_exact", "kriging_se_exact", "as_device_fit",
     "PaddedGrid", "Neighborhood", "build_padded_grid", "neighborhood", "fill_distance",
     "NODE_SNAP_TOL",
     "RapidSetup", "build_setup", "predict_rapid", "next_fft_len", "build_filter_spectrum",

@@ -72,6 +72,8 @@ _PROTOS = {
     "rk_fit_copy_out": (_i32, [_vp, _dp, _dp, _dp]),
     "rk_fit_info": (_i32, [_vp, C.POINTER(_i64), C.POINTER(_i32)]),
     "rk_refit_dev": (_i32, [_vp, _dp, _i64, _dp, _dp, _vp]),
+    "rk_predict_exact": (_i32, [_vp, _dp, _i64, _dp, C.c_double, _dp, _vp]),
+    "rk_kriging_se_exact": (_i32, [_vp, _dp, _i64, _dp, C.c_double, _i64, _dp, _vp]),
     "rk_draw_seed": (_u64, [_u64, _u64]),
     "rk_philox_normals": (_i32, [_u64, _u64, _u64, _i64, _dp, _vp]),
     "rk_philox_raw": (_i32, [_u64, _u64, _u64, _i64, _dp, _vp]),

@@ -142,6 +142,8 @@ struct rk_fit {
   double* Uinv = nullptr;       // U^-1 = L^-T (n, n) column-major upper, built on first batched refit
   double* beta = nullptr;       // (p)
   double* c = nullptr;          // (n)
+  double* obs = nullptr;        // (n, 2) observation locations (exact prediction at targets)
+  rk::MaternDev mat{};
   std::vector<double> gram_lu;  // (p, p) LU of B'B with partial pivoting (row-major)
   std::vector<int> gram_piv;
   void* cublas = nullptr;

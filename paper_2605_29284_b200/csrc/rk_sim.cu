@@ -12,6 +12,7 @@
 //   fit / _cholesky_with_ridge exact.py:25-37,71-105 -> rk_fit_create
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <memory>
 #include <vector>
 
@@ -679,6 +680,7 @@ static Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double*
 static void free_fit(rk_fit* f) {
   if (!f) return;
   cudaFree(f->Uinv);
+  cudaFree(f->obs);
   cudaFree(f->U);
   cudaFree(f->X);
   cudaFree(f->B);
@@ -880,6 +882,7 @@ rk_status rk_fit_create(const rk_model* model, const double* obs_host, int64_t n
     double* dobs = nullptr;
     int* bad = nullptr;
     RK_CUDA_TRY(cudaMalloc(&dobs, sizeof(double) * 2 * n));
+    f->obs = dobs;   // owned by the fit: kept for predict_exact / kriging_se_exact
     RK_CUDA_TRY(cudaMalloc(&bad, sizeof(int)));
     RK_CUDA_TRY(cudaMemset(bad, 0, sizeof(int)));
     RK_CUDA_TRY(cudaMemcpy(dobs, obs_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
@@ -921,7 +924,7 @@ rk_status rk_fit_create(const rk_model* model, const double* obs_host, int64_t n
     int hb = 0;
     RK_CUDA_TRY(cudaMemcpy(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost));
     cudaFree(bad);
-    cudaFree(dobs);
+    f->mat = P;
     if (hb) return Status::err(RK_NUMERIC, "Temme series / continued fraction for K_nu failed to converge");
     if (hinfo != 0)
       return Status::err(RK_NUMERIC, "Cholesky of the observation covariance M failed even with ridge");
@@ -948,7 +951,6 @@ rk_status rk_fit_import(const rk_model* model, const double* obs_host, int64_t n
                         int32_t p, const double* chol_host, const double* beta_host,
                         const double* c_host, rk_fit** out) {
   auto run = [&]() -> Status {
-    (void)obs_host;
     if (n < 1 || p < 1 || p > 8) return Status::err(RK_DOMAIN, "need n >= p >= 1 (p <= 8)");
     rk_fit* f = new rk_fit();
     std::unique_ptr<rk_fit, void (*)(rk_fit*)> guard(f, free_fit);
@@ -967,6 +969,9 @@ rk_status rk_fit_import(const rk_model* model, const double* obs_host, int64_t n
     RK_CUDA_TRY(cudaMalloc(&f->c, sizeof(double) * n));
     RK_CUDA_TRY(cudaMemcpy(f->beta, beta_host, sizeof(double) * p, cudaMemcpyHostToDevice));
     RK_CUDA_TRY(cudaMemcpy(f->c, c_host, sizeof(double) * n, cudaMemcpyHostToDevice));
+    RK_CUDA_TRY(cudaMalloc(&f->obs, sizeof(double) * 2 * n));
+    RK_CUDA_TRY(cudaMemcpy(f->obs, obs_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+    f->mat = make_matern_dev(*model);
     *out = guard.release();
     return Status::ok();
   };
@@ -1072,6 +1077,240 @@ rk_status rk_ensemble_finalize(int64_t n_pix, int64_t n_draws, const double* dat
                                               mean_dev, se_dev);
     count_launch();
     RK_LAUNCH_CHECK();
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+}  // extern "C"
+
+// ===================================================== exact prediction at targets
+// predict_exact (exact.py:132-147): X_t beta + k_t c, k_t the cross covariance of the targets
+// with the observations, never formed: every thread owns one target and runs over the
+// observations in index order (staged through shared memory), so the sum order is fixed.
+// kriging_se_exact (exact.py:150-175): the k_t block IS formed (n x chunk, column-major),
+// u = L^-1 k_t as one FP64 tensor-core GEMM with the fit's U^-1, var = sigma2 - |u|^2 +
+// h'(B'B)^-1 h with h = x_t - u'B, clamp at -1e-10, sqrt.
+namespace rk {
+
+constexpr int kExactThreads = 256;
+
+struct ExactArgs {
+  MaternDev mat;
+  const double* obs;       // (n, 2)
+  const double* c;         // (n)
+  int64_t n;
+  const double* tgt;       // (nt, 2)
+  int64_t nt;
+  const double* xt;        // (nt, p) row-major, or null: intercept-only fit, x00 * beta[0]
+  double x00;
+  const double* beta;      // (p)
+  int p;
+  double* out;             // (nt)
+  int* bad;
+};
+
+__global__ void __launch_bounds__(kExactThreads) predict_exact_kernel(const ExactArgs a) {
+  __shared__ double so[3][kExactThreads];
+  const int64_t t = blockIdx.x * (int64_t)kExactThreads + threadIdx.x;
+  const bool valid = t < a.nt;
+  const double tx = valid ? a.tgt[2 * t] : 0.0, ty = valid ? a.tgt[2 * t + 1] : 0.0;
+  double acc = 0.0;
+  for (int64_t i0 = 0; i0 < a.n; i0 += kExactThreads) {
+    const int m = a.n - i0 < kExactThreads ? (int)(a.n - i0) : kExactThreads;
+    __syncthreads();
+    if (threadIdx.x < m) {
+      so[0][threadIdx.x] = a.obs[2 * (i0 + threadIdx.x)];
+      so[1][threadIdx.x] = a.obs[2 * (i0 + threadIdx.x) + 1];
+      so[2][threadIdx.x] = a.c[i0 + threadIdx.x];
+    }
+    __syncthreads();
+    if (valid)
+      for (int k = 0; k < m; ++k) {
+        const double dx = tx - so[0][k], dy = ty - so[1][k];
+        acc = fma(matern_cov(a.mat, sqrt(dx * dx + dy * dy), a.bad), so[2][k], acc);
+      }
+  }
+  if (!valid) return;
+  double fx = 0.0;
+  if (a.xt)
+    for (int q = 0; q < a.p; ++q) fx = fma(a.xt[t * a.p + q], a.beta[q], fx);
+  else
+    fx = a.x00 * a.beta[0];
+  a.out[t] = acc + fx;
+}
+
+// K (n x tc, column-major): K[i + j n] = cov(|obs_i - tgt_j|)
+__global__ void cross_cov_kernel(MaternDev P, const double* __restrict__ obs, int64_t n,
+                                 const double* __restrict__ tgt, int64_t tc, double* __restrict__ K, int* bad) {
+  const int64_t tot = n * tc;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / n, i = e - j * n;
+    const double dx = tgt[2 * j] - obs[2 * i], dy = tgt[2 * j + 1] - obs[2 * i + 1];
+    K[e] = matern_cov(P, sqrt(dx * dx + dy * dy), bad);
+  }
+}
+
+// one warp per target column: var = sigma2 - sum_i u_i^2 (fixed lane-strided order + tree)
+__global__ void colsq_kernel(const double* __restrict__ u, int64_t n, int64_t tc, double sigma2, double* var) {
+  const int64_t j = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (j >= tc) return;
+  const double* col = u + j * n;
+  double s = 0.0;
+  for (int64_t i = lane; i < n; i += 32) s = fma(col[i], col[i], s);
+#pragma unroll
+  for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+  if (lane == 0) var[j] = sigma2 - s;
+}
+
+// h = x_t - (B'u)' (p x tc, column-major) in place over BtU; then hg = gram^-1 h; var += h.hg;
+// clamp / sqrt into out; the most negative variance is tracked for the error message
+__global__ void se_finish_kernel(GramLU g, double* __restrict__ BtU, const double* __restrict__ xt, double x00,
+                                 int64_t tc, const double* __restrict__ var, double* __restrict__ out,
+                                 unsigned long long* minvar_bits) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= tc) return;
+  const int p = g.p;
+  double h[8], x[8];
+  for (int q = 0; q < p; ++q) {
+    const double xq = xt ? xt[j * p + q] : x00;
+    h[q] = xq - BtU[j * p + q];
+    x[q] = h[q];
+  }
+  for (int i = 0; i < p; ++i) {
+    const int pi = g.piv[i];
+    if (pi != i) { const double tt = x[i]; x[i] = x[pi]; x[pi] = tt; }
+  }
+  for (int i = 0; i < p; ++i)
+    for (int k = 0; k < i; ++k) x[i] -= g.lu[i * p + k] * x[k];
+  for (int i = p - 1; i >= 0; --i) {
+    for (int k = i + 1; k < p; ++k) x[i] -= g.lu[i * p + k] * x[k];
+    x[i] /= g.lu[i * p + i];
+  }
+  double v = var[j];
+  for (int q = 0; q < p; ++q) v = fma(h[q], x[q], v);
+  if (v < -1.0e-10) {   // exact.py:171-173: keep the most negative for the message
+    unsigned long long old = *minvar_bits, assumed;
+    do {
+      assumed = old;
+      if (__longlong_as_double((long long)assumed) <= v) break;
+      old = atomicCAS(minvar_bits, assumed, (unsigned long long)__double_as_longlong(v));
+    } while (old != assumed);
+  }
+  out[j] = sqrt(fmax(v, 0.0));
+}
+
+static Status exact_targets_check(const rk_fit* f, const double* xt, int64_t nt) {
+  if (nt < 0) return Status::err(RK_DOMAIN, "negative target count");
+  if (!f->obs) return Status::err(RK_INTERNAL, "fit has no observation locations");
+  (void)xt;
+  return Status::ok();
+}
+
+}  // namespace rk
+
+extern "C" {
+
+rk_status rk_predict_exact(const rk_fit* f, const double* targets_dev, int64_t nt, const double* xt_dev,
+                           double x00, double* out_dev, void* stream) {
+  auto run = [&]() -> Status {
+    RK_TRY(exact_targets_check(f, xt_dev, nt));
+    if (nt == 0) return Status::ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    int* bad = nullptr;
+    RK_TRY(scratch_alloc((void**)&bad, sizeof(int), st));
+    RK_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    ExactArgs a{};
+    a.mat = f->mat;
+    a.obs = f->obs;
+    a.c = f->c;
+    a.n = f->n;
+    a.tgt = targets_dev;
+    a.nt = nt;
+    a.xt = xt_dev;
+    a.x00 = x00;
+    a.beta = f->beta;
+    a.p = f->p;
+    a.out = out_dev;
+    a.bad = bad;
+    predict_exact_kernel<<<(unsigned)ceil_div(nt, kExactThreads), kExactThreads, 0, st>>>(a);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    int hb = 0;
+    RK_CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    scratch_free(bad, st);
+    RK_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hb) return Status::err(RK_NUMERIC, "Temme series / continued fraction for K_nu failed to converge");
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_kriging_se_exact(rk_fit* f, const double* targets_dev, int64_t nt, const double* xt_dev,
+                              double x00, int64_t chunk, double* out_dev, void* stream) {
+  auto run = [&]() -> Status {
+    RK_TRY(exact_targets_check(f, xt_dev, nt));
+    if (nt == 0) return Status::ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    RK_TRY(ensure_uinv(f, st));
+    const int64_t n = f->n;
+    const int p = f->p;
+    // chunk of targets per pass: the caller's, capped so K and u stay within ~4 GB
+    int64_t tc = std::max<int64_t>(1, std::min<int64_t>(chunk > 0 ? chunk : 4000, nt));
+    tc = std::max<int64_t>(1, std::min<int64_t>(tc, (int64_t)(4.0e9 / (16.0 * (double)n))));
+    double *K = nullptr, *U = nullptr, *var = nullptr, *BtU = nullptr;
+    int* bad = nullptr;
+    unsigned long long* minv = nullptr;
+    RK_TRY(scratch_alloc((void**)&K, sizeof(double) * (size_t)n * tc, st));
+    RK_TRY(scratch_alloc((void**)&U, sizeof(double) * (size_t)n * tc, st));
+    RK_TRY(scratch_alloc((void**)&var, sizeof(double) * (size_t)tc, st));
+    RK_TRY(scratch_alloc((void**)&BtU, sizeof(double) * (size_t)p * tc, st));
+    RK_TRY(scratch_alloc((void**)&bad, sizeof(int), st));
+    RK_TRY(scratch_alloc((void**)&minv, sizeof(unsigned long long), st));
+    RK_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    const double zero_d = 0.0;
+    unsigned long long zero_bits;
+    memcpy(&zero_bits, &zero_d, sizeof zero_bits);
+    RK_CUDA_TRY(cudaMemcpyAsync(minv, &zero_bits, sizeof zero_bits, cudaMemcpyHostToDevice, st));
+    cublasHandle_t h = (cublasHandle_t)f->cublas;
+    RK_CUBLAS_TRY(cublasSetStream(h, st));
+    const double one = 1.0, zer = 0.0;
+    const GramLU g = gram_args(f);
+    for (int64_t j0 = 0; j0 < nt; j0 += tc) {
+      const int64_t m = std::min<int64_t>(tc, nt - j0);
+      cross_cov_kernel<<<(int)std::min<int64_t>(ceil_div(n * m, 256), 148 * 64), 256, 0, st>>>(
+          f->mat, f->obs, n, targets_dev + 2 * j0, m, K, bad);
+      count_launch();
+      RK_LAUNCH_CHECK();
+      // u = L^-1 K = (U^-1)' K
+      RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)m, (int)n, &one, f->Uinv, (int)n, K,
+                                (int)n, &zer, U, (int)n));
+      colsq_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(U, n, m, f->model.sigma2, var);
+      count_launch();
+      // B'u (p x m)
+      RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, (int)m, (int)n, &one, f->B, (int)n, U, (int)n,
+                                &zer, BtU, p));
+      se_finish_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(g, BtU, xt_dev ? xt_dev + j0 * p : nullptr, x00,
+                                                                   m, var, out_dev + j0, minv);
+      count_launch();
+      RK_LAUNCH_CHECK();
+    }
+    int hb = 0;
+    unsigned long long mb = 0;
+    RK_CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RK_CUDA_TRY(cudaMemcpyAsync(&mb, minv, sizeof mb, cudaMemcpyDeviceToHost, st));
+    for (void* q : {(void*)K, (void*)U, (void*)var, (void*)BtU, (void*)bad, (void*)minv}) scratch_free(q, st);
+    RK_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hb) return Status::err(RK_NUMERIC, "Temme series / continued fraction for K_nu failed to converge");
+    double mv;
+    memcpy(&mv, &mb, sizeof mv);
+    if (mv < -1.0e-10) {
+      char b[128];
+      snprintf(b, sizeof b, "negative prediction variance %.3e beyond clamp tolerance", mv);
+      return Status::err(RK_NUMERIC, b);
+    }
     return Status::ok();
   };
   return (rk_status)finish_sim(run());

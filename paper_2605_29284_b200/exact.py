@@ -1,8 +1,10 @@
-"""Exact universal-Kriging fit and batched GLS refit on the GPU.
+"""Exact universal Kriging on the GPU: fit, batched GLS refit, prediction and its SE.
 
-Interface of reference exact.py:40-113: ``KrigingFit`` (model, obs_locs, X,
-chol_M, beta_hat, c), ``fit(model, obs_locs, z, X=None)`` (71-105) and
-``refit_coefficients(krig, z_new)`` (108-113).  The n x n factor stays on the
+Interface of reference exact.py:40-175: ``KrigingFit`` (model, obs_locs, X,
+chol_M, beta_hat, c), ``fit(model, obs_locs, z, X=None)`` (71-105),
+``refit_coefficients(krig, z_new)`` (108-113), ``predict_exact(krig, targets,
+target_covariates=None, chunk=20000)`` (132-147) and ``kriging_se_exact(krig, targets,
+target_covariates=None, chunk=4000)`` (150-175).  The n x n factor stays on the
 device; ``chol_M`` (lower, row-major like scipy) is copied out on first access.
 ``as_device_fit`` adopts a reference-built KrigingFit so ensembles can run on
 the identical (chol_M, beta_hat, c).
@@ -19,7 +21,7 @@ from . import _native as N
 from .covariance import CovarianceModel
 from .errors import DomainError
 
-__all__ = ["KrigingFit", "fit", "refit_coefficients", "as_device_fit"]
+__all__ = ["KrigingFit", "fit", "refit_coefficients", "predict_exact", "kriging_se_exact", "as_device_fit"]
 
 
 class _FitHandle:
@@ -148,3 +150,56 @@ def refit_coefficients(krig, z_new):
     if dev:
         return beta, c
     return beta.cpu().numpy(), c.cpu().numpy()
+
+
+def _target_covariates(f: KrigingFit, targets: np.ndarray, target_covariates):
+    """exact.py:116-129: None -> intercept-only fits use X[0, 0]; else (nt, p)."""
+    if target_covariates is None:
+        if not f.is_intercept_only():
+            raise DomainError("fit uses nontrivial covariates; pass target_covariates for prediction")
+        return None
+    if D.is_device_tensor(target_covariates):
+        xt = target_covariates.to(dtype=D.torch().float64)
+        if xt.ndim == 1:
+            xt = xt[:, None]
+        shape = tuple(xt.shape)
+    else:
+        xt = np.asarray(target_covariates, dtype=float)
+        if xt.ndim == 1:
+            xt = xt[:, None]
+        shape = xt.shape
+    if shape != (targets.shape[0], f.X.shape[1]):
+        raise DomainError(f"target covariates shape {shape} does not match "
+                          f"({targets.shape[0]}, {f.X.shape[1]})")
+    return D.to_device(xt).contiguous()
+
+
+def _targets(targets):
+    if D.is_device_tensor(targets):
+        return targets.to(dtype=D.torch().float64).reshape(-1, 2).contiguous()
+    return D.to_device(np.asarray(targets, dtype=float).reshape(-1, 2)).contiguous()
+
+
+def predict_exact(krig, targets, target_covariates=None, chunk: int = 20000):
+    """Exact Kriging prediction X_t beta_hat + k_t c at arbitrary targets (exact.py:132-147).
+    ``chunk`` is accepted for signature compatibility: the cross covariance is never formed."""
+    f = as_device_fit(krig)
+    dev = D.is_device_tensor(targets)
+    t = _targets(targets)
+    xt = _target_covariates(f, t, target_covariates)
+    out = D.empty((t.shape[0],))
+    N.call("rk_predict_exact", f.handle, N.ptr(t), t.shape[0], N.ptr(xt), float(f.X[0, 0]), N.ptr(out),
+           N.stream_ptr())
+    return out if dev else out.cpu().numpy()
+
+
+def kriging_se_exact(krig, targets, target_covariates=None, chunk: int = 4000):
+    """Prediction standard error of the smooth field at each target (exact.py:150-175)."""
+    f = as_device_fit(krig)
+    dev = D.is_device_tensor(targets)
+    t = _targets(targets)
+    xt = _target_covariates(f, t, target_covariates)
+    out = D.empty((t.shape[0],))
+    N.call("rk_kriging_se_exact", f.handle, N.ptr(t), t.shape[0], N.ptr(xt), float(f.X[0, 0]), int(chunk),
+           N.ptr(out), N.stream_ptr())
+    return out if dev else out.cpu().numpy()

@@ -373,3 +373,30 @@ def test_fused_and_standalone_scatter_identical(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("tag", ["cov", "icpt"])
+def test_predict_exact_and_se_against_reference(pk, tag):
+    """GPU predict_exact / kriging_se_exact (exact.py:132-175) against the reference, on our GPU
+    fit and on the reference's own fit adopted through as_device_fit; device targets stay on
+    the device; intercept-only fits take target_covariates=None; bad covariates raise."""
+    import torch
+    g = load_golden("exact_targets")
+    model = pk.CovarianceModel(float(g["sigma2"]), float(g["alpha"]), float(g[f"{tag}_nu"]), float(g["tau2"]))
+    X = g[f"{tag}_X"] if g[f"{tag}_X"].size else None
+    xt = g[f"{tag}_xt"] if g[f"{tag}_xt"].size else None
+    f = pk.fit(model, g[f"{tag}_obs"], g[f"{tag}_z"], X)
+    tg = g[f"{tag}_targets"]
+    assert rel_err(pk.predict_exact(f, tg, xt), g[f"{tag}_pred"]) < FIELD_TOL
+    assert rel_err(pk.kriging_se_exact(f, tg, xt, chunk=97), g[f"{tag}_se"]) < FIELD_TOL
+    from types import SimpleNamespace   # the reference KrigingFit's attribute names (exact.py:40-56)
+    ofit = SimpleNamespace(model=model, obs_locs=g[f"{tag}_obs"],
+                           X=X if X is not None else np.ones((len(g[f"{tag}_obs"]), 1)),
+                           chol_M=g[f"{tag}_chol"], beta_hat=g[f"{tag}_beta"], c=g[f"{tag}_c"])
+    pd = pk.predict_exact(ofit, torch.as_tensor(tg, device="cuda"), None if xt is None else torch.as_tensor(xt, device="cuda"))
+    assert pd.is_cuda and rel_err(pd.cpu().numpy(), g[f"{tag}_pred"]) < FIELD_TOL
+    if tag == "cov":
+        with pytest.raises(pk.DomainError):
+            pk.predict_exact(f, tg)
+        with pytest.raises(pk.DomainError):
+            pk.kriging_se_exact(f, tg, xt[:, :2])

@@ -137,3 +137,19 @@ def test_embedding_failure_raises():
     grid = ro.make_grid((0.0, 1.0, 0.0, 1.0), (24, 24), 2, [])
     with pytest.raises(ro.OracleNumericError, match="eigenvalue"):
         ro.embedding_root(model, grid)
+
+
+@pytest.mark.parametrize("tag", ["cov", "icpt"])
+def test_exact_targets_match_reference(tag):
+    """predict_exact / kriging_se_exact (exact.py:132-175) restated in the oracle, on the
+    reference's own fit (chol_M, beta_hat, c)."""
+    g = load_golden("exact_targets")
+    model = ro.Model(float(g["sigma2"]), float(g["alpha"]), float(g[f"{tag}_nu"]), float(g["tau2"]))
+    X = g[f"{tag}_X"] if g[f"{tag}_X"].size else np.ones((g[f"{tag}_obs"].shape[0], 1))
+    fit = ro.Fit(model, g[f"{tag}_obs"], X, g[f"{tag}_chol"], g[f"{tag}_beta"], g[f"{tag}_c"])
+    xt = g[f"{tag}_xt"] if g[f"{tag}_xt"].size else None
+    assert rel_err(ro.predict_exact(fit, g[f"{tag}_targets"], xt), g[f"{tag}_pred"]) < 1e-13
+    assert rel_err(ro.kriging_se_exact(fit, g[f"{tag}_targets"], xt), g[f"{tag}_se"]) < 1e-13
+    # and the oracle's own fit reproduces the reference's
+    fit2 = ro.exact_fit(model, g[f"{tag}_obs"], g[f"{tag}_z"], None if tag == "icpt" else X)
+    assert rel_err(fit2.c, g[f"{tag}_c"]) < 1e-10
