@@ -215,6 +215,35 @@ def gen_exact_targets():
     save("exact_targets", sigma2=1.3, alpha=6.0, tau2=0.04, **out)
 
 
+CLI_RUNS = {
+    "predict_rapid": ["predict", "--grid", "32x24", "--L", "3", "--covariates", "1+x+y"],
+    "predict_exact": ["predict", "--grid", "32x24", "--method", "exact", "--domain", "0,1,0,1"],
+    "simulate": ["simulate", "--grid", "32x32", "--draws", "10", "--seed", "7", "--save-draws"],
+}
+CLI_MODEL = ["--sigma2", "1.0", "--alpha", "5.0", "--nu", "1.0", "--tau2", "0.05"]
+
+
+def gen_cli():
+    """The reference CLI (cli.py) on a 60-point file (test_acceptance.py:246-266 style):
+    RKGRID1 outputs of predict (rapid with covariates, exact) and simulate."""
+    from rapidkrig.cli import cli_main
+    rng = np.random.default_rng(6)
+    n = 60
+    x, y = rng.uniform(0, 1, n), rng.uniform(0, 1, n)
+    z = np.sin(3 * x) + np.cos(2 * y) + 0.1 * rng.normal(size=n)
+    d = os.path.join(OUT, "cli")
+    os.makedirs(d, exist_ok=True)
+    obs = os.path.join(d, "obs.csv")
+    with open(obs, "w", encoding="utf-8") as fh:
+        fh.write("x,y,z\n")
+        for row in zip(x, y, z):
+            fh.write(",".join(f"{v:.17g}" for v in row) + "\n")
+    for name, args in CLI_RUNS.items():
+        out = os.path.join(d, name + ".rkg")
+        assert cli_main([*args, "--obs", obs, "--out", out, *CLI_MODEL]) == 0
+        print("wrote", out, os.path.getsize(out))
+
+
 def gen_misc():
     ks = np.arange(1, 1200)
     save("fft_len", n=ks, p=np.array([rapid.next_fft_len(int(k)) for k in ks]))
@@ -229,5 +258,6 @@ if __name__ == "__main__":
     gen_cs()
     gen_misc()
     gen_exact_targets()
+    gen_cli()
     gen_config("cfg1")
     gen_config("cfg2")
