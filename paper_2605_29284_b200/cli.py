@@ -4,14 +4,15 @@ Same flags, output files and exit status as cli.py:60-263: 0 success, 1 domain /
 error, 2 numeric error; ``RAPIDKRIG_SEED`` overrides ``--seed``.  ``predict`` fits on the GPU
 and writes the ``prediction`` field by the rapid path (``--method rapid``, default) or exact
 Kriging at every interior node (``--method exact``); ``simulate`` writes ``mean`` / ``se``
-(and ``drawNNNN`` with ``--save-draws``) of a conditional-simulation ensemble.  The study
-subcommands (bench-error / bench-converge / bench-time: studies.py) are outside this
-build's scope and exit 1 with a message.
+(and ``drawNNNN`` with ``--save-draws``) of a conditional-simulation ensemble;
+``bench-time`` runs the timing study (studies.run_timing) and writes its CSV.  The error and
+convergence studies (bench-error / bench-converge) are outside this build's scope and exit 1.
 """
 
 from __future__ import annotations
 
 import argparse
+import csv
 import os
 import sys
 
@@ -22,6 +23,7 @@ from .gridding import build_padded_grid
 from .io import build_covariates, load_observations, parse_formula, write_grid_output
 from .rapid import build_setup, predict_rapid
 from .simulate import RNG_ALGORITHM, generate_ensemble
+from .studies import run_timing
 
 __all__ = ["cli_main", "main"]
 
@@ -73,7 +75,15 @@ def _parser():
     ps.add_argument("--draws", type=int, default=100)
     ps.add_argument("--seed", type=int, default=0)
     ps.add_argument("--save-draws", action="store_true")
-    for name in ("bench-error", "bench-converge", "bench-time"):
+    pt = sub.add_parser("bench-time", help="timing comparison (GPU path)")
+    pt.add_argument("--out", required=True)
+    pt.add_argument("--ns", type=lambda t: tuple(int(p) for p in t.split(",") if p.strip()), default=(200, 1500))
+    pt.add_argument("--grids", default="60x60,100x100,140x140")
+    pt.add_argument("--methods", default="exact,rapid-L4")
+    pt.add_argument("--reps", type=int, default=3)
+    pt.add_argument("--timeout", type=float, default=60.0)
+    pt.add_argument("--seed", type=int, default=1)
+    for name in ("bench-error", "bench-converge"):
         sub.add_parser(name, help="study harness (not in this build)").add_argument("rest", nargs="*")
     return ap
 
@@ -124,12 +134,26 @@ def _simulate(a):
     return 0
 
 
+def _bench_time(a):
+    env = os.environ.get("RAPIDKRIG_SEED")
+    rows = run_timing(ns=a.ns, grid_ladder=tuple(_dims(g) for g in a.grids.split(",")),
+                      methods=tuple(m.strip() for m in a.methods.split(",")), reps=a.reps,
+                      timeout_seconds=a.timeout, seed=int(env) if env else a.seed)
+    with open(a.out, "w", newline="", encoding="utf-8") as fh:
+        w = csv.writer(fh)
+        w.writerow(("method", "n", "grid", "setup_seconds", "predict_seconds", "reps", "censored"))
+        w.writerows((r.method, r.n, f"{r.grid[0]}x{r.grid[1]}", f"{r.setup_seconds:.6f}",
+                     f"{r.predict_seconds:.6f}", r.reps, int(r.censored)) for r in rows)
+    print(f"wrote {a.out} ({len(rows)} rows)")
+    return 0
+
+
 def _out_of_scope(a):
     raise DomainError(f"'{a.command}' (studies.py) is not provided by this build")
 
 
-_COMMANDS = {"predict": _predict, "simulate": _simulate, "bench-error": _out_of_scope,
-             "bench-converge": _out_of_scope, "bench-time": _out_of_scope}
+_COMMANDS = {"predict": _predict, "simulate": _simulate, "bench-time": _bench_time,
+             "bench-error": _out_of_scope, "bench-converge": _out_of_scope}
 
 
 def cli_main(argv=None) -> int:

@@ -26,7 +26,7 @@ from .errors import DomainError
 from .exact import as_device_fit, refit_coefficients
 from .rapid import GRID_SETUPS, _fixed_inputs, predict_rapid
 
-__all__ = ["Ensemble", "RNG_ALGORITHM", "draw_seed", "sim_unconditional_grid", "sim_obs_local",
+__all__ = ["Ensemble", "RNG_ALGORITHM", "draw_seed", "std_normals", "sim_unconditional_grid", "sim_obs_local",
            "conditional_draw", "generate_ensemble", "ensemble_chunks", "ENSEMBLE_CHUNKS"]
 
 RNG_ALGORITHM = "philox4x64-10"
@@ -54,6 +54,16 @@ class Ensemble:
     mean_field: np.ndarray
     empirical_se: np.ndarray
     rng_algorithm: str = RNG_ALGORITHM
+
+
+def std_normals(seed: int, stream: int, count: int, start: int = 0, device: bool = False):
+    """``_std_normals(_rng(seed, stream), count)`` (simulate.py:65-74) on the GPU: Philox4x64-10
+    words ``start .. start + count - 1`` of the (seed, stream) key, bit-exact, through ndtri."""
+    out = D.empty((int(count),))
+    if count:
+        N.call("rk_philox_normals", int(seed) & _M64, int(stream) & _M64, int(start), int(count), N.ptr(out),
+               N.stream_ptr())
+    return out if device else out.cpu().numpy()
 
 
 def _embedding_handle(model, setup_or_grid):

@@ -58,3 +58,25 @@ def test_seed_env_exit_codes(cli, tmp_path, monkeypatch, capsys):
                    "--seed", "1", "--sigma2", "1.0", "--alpha", "1.0", "--nu", "1.5", "--tau2", "0.05"])
     assert rc == 2
     assert "numeric error" in capsys.readouterr().err
+
+
+def test_timing_study_and_its_data(tmp_path):
+    """studies.run_timing rows (studies.py:289-390) and its data: the (seed, n) Philox stream's
+    uniforms then normals, identical to numpy Philox + scipy ndtri."""
+    import scipy.special as sp
+    from paper_2605_29284_b200 import studies
+    from paper_2605_29284_b200.cli import cli_main
+    from paper_2605_29284_b200.simulate import std_normals
+    n, seed = 70, 3
+    rng = np.random.Generator(np.random.Philox(key=seed + (n << 64)))
+    rng.uniform(0, 1, n), rng.uniform(0, 1, n)
+    ref = sp.ndtri((rng.integers(0, 1 << 53, size=n).astype(float) + 0.5) / float(1 << 53))
+    assert rel_err(std_normals(seed, n, n, start=2 * n), ref) < 1e-14
+    rows = studies.run_timing(ns=(60,), grid_ladder=((20, 16),), methods=("exact", "rapid-L2", "cs-fast"), reps=1)
+    assert [r.method for r in rows] == ["exact", "rapid-L2", "cs-fast"]
+    assert all(r.grid == (20, 16) and r.predict_seconds > 0 and not r.censored for r in rows)
+    out = str(tmp_path / "t.csv")
+    assert cli_main(["bench-time", "--out", out, "--ns", "40", "--grids", "16x16", "--methods", "rapid-L4",
+                     "--reps", "1"]) == 0
+    assert open(out).read().splitlines()[0] == "method,n,grid,setup_seconds,predict_seconds,reps,censored"
+    assert cli_main(["bench-error", "--out", out]) == 1
