@@ -61,7 +61,7 @@ Status plan_for(int n, FftPlan* out, int wide) {
   FftPlan pl{};
   if (!fft_factor(n, &pl, wide))
     return Status::err(RK_INTERNAL, "FFT length " + std::to_string(n) + " is not 2^a 3^b");
-  if (pl.nthr > (wide == 2 ? 1024 : 512))
+  if (pl.nthr > (wide == 2 ? kFftWideThreads : 512))
     return Status::err(RK_DOMAIN, "FFT length " + std::to_string(n) + " too large for one CTA");
   std::vector<double2> tw;
   fft_stage_twiddles(pl, tw, [](double c, double s) { return make_double2(c, s); });
@@ -115,7 +115,7 @@ int pick_lpc(const FftPlan& pl, int max_lines, int64_t total_lines) {
   }();
   int best = 1;
   int64_t best_res = -1;
-  const int tmax = pl.wide == 2 ? 1024 : 512;   // resident FFT threads per SM (registers)
+  const int tmax = pl.wide == 2 ? kFftWideThreads : 512;   // resident FFT threads per SM (registers)
   for (int lpc = 1; lpc <= std::max(1, max_lines); ++lpc) {
     const int threads = lpc * pl.nthr;
     const size_t smem = lpc * line_bytes + line_bytes / 8 + 64;

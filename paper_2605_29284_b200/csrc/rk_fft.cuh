@@ -56,6 +56,8 @@ __device__ __forceinline__ FftPlan fft_twiddles_to_smem(const FftPlan& pl, doubl
 // smaller ones per thread, so a line spreads over up to 1024 threads and an SM keeps 32
 // FFT warps resident instead of 16
 __host__ __device__ constexpr int fft_kmax_wide(int r) { return r >= 8 ? 1 : 2; }
+// threads per SM (and at most per line) of the WIDE kernels' launch bound
+constexpr int kFftWideThreads = 1024;
 __host__ __device__ constexpr int fft_kmax(int r) {
   return r == 2 ? 9 : r == 3 ? 6 : r == 4 ? 4 : r == 6 ? 3 : r == 8 ? 2 : r == 9 ? 2 : r == 12 ? 2 : 1;
 }
@@ -389,7 +391,7 @@ inline bool fft_factor(int n, FftPlan* pl, int wide = 0) {
     need = 1;
     for (int i = 0; i < pl->nstages; ++i) {
       const int nb = n / rad[i];
-      const int k = fft_kmax_wide(rad[i]);
+      const int k = fft_kmax_wide(rad[i]);   // nthr must stay <= kFftWideThreads (plan_for checks)
       need = need > (nb + k - 1) / k ? need : (nb + k - 1) / k;
     }
   }

@@ -102,7 +102,7 @@ struct RowFwdArgs {
 };
 
 // FFT kernels: WIDE instantiations run 64-register threads (fft_kmax_wide butterflies each)
-#define RK_FFT_BOUNDS(WIDE) __launch_bounds__((WIDE) ? 1024 : 512, 1)
+#define RK_FFT_BOUNDS(WIDE) __launch_bounds__((WIDE) ? kFftWideThreads : 512, 1)
 
 template <int SRC, bool TWS, bool WIDE>
 __global__ void RK_FFT_BOUNDS(WIDE) row_fwd_kernel(const RowFwdArgs a) {

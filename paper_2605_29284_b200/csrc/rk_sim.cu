@@ -89,7 +89,7 @@ struct CsColArgs {
 };
 
 template <bool TWS, bool WIDE>
-__global__ void __launch_bounds__(WIDE ? 1024 : 512, 1) cs_col_kernel(const CsColArgs a) {
+__global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_col_kernel(const CsColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -368,7 +368,7 @@ struct CsFftArgs {
 };
 
 template <bool TWS, bool WIDE>
-__global__ void __launch_bounds__(WIDE ? 1024 : 512, 1) cs_rowfft_kernel(const CsFftArgs a) {
+__global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_rowfft_kernel(const CsFftArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
