@@ -7,21 +7,22 @@
 // are coalesced), runs a register DFT_R codelet, then — after one barrier —
 // scatters the outputs to y[(j - j mod Ns) R + j mod Ns + k Ns] (autosort).
 //
-// Throughput note (measured, tools/fft_bench.cu + ncu): an fp64 complex element is 16
-// bytes and every stage moves it through shared memory twice, so a radix-9 stage does
-// only ~0.55 flop per smem byte while an SM balances 128 B/clk of smem against 128
-// flop/clk of FP64 -- the engine is shared-memory-bandwidth bound.  Larger radices
-// (composite P x Q codelets, DftPQ below) cut smem round trips, but every schedule that
-// mixes several large-radix arms in one kernel made ptxas spill; the shipped schedule is
-// 9^a * {3,6} * 8^b * {2,4}.  Radix-3 family first, so the first (Ns = 1) stage writes
-// with an odd stride (bank-conflict free for 16-byte elements).
+// Throughput note (measured, tools/fft_bench.cu, tools/fft_stage_lat.cu + ncu): an fp64
+// complex element is 16 bytes and every stage moves it through shared memory twice, and a
+// radix-9 butterfly costs 88 FP64 instructions of codelet plus 60 of twiddles; on the cfg3
+// column pass ncu shows the smem pipe ~57 % and the FP64 pipe ~43 % busy with barrier and
+// short-scoreboard (smem) stalls on top -- no single unit saturated.  Larger radices
+// (composite P x Q register codelets, radix 12-36, tried in an earlier revision) cut smem
+// round trips, but every schedule that mixed several large-radix arms in one kernel made
+// ptxas spill (as did a full power-table option: every extra code path costs registers);
+// the shipped schedule is 9^a * {3,6} * 8^b * {2,4,4x4}.  Radix-3 family first, so the
+// first (Ns = 1) stage writes with an odd stride (bank-conflict free for 16-byte elements).
 //
 // Several lines can share a CTA: every thread calls every stage (barriers are CTA
 // wide); threads whose butterfly index runs past n/R just idle.
 #pragma once
 
 #include "rk_common.cuh"
-#include "rk_fft_consts.cuh"
 
 namespace rk {
 
@@ -191,56 +192,6 @@ struct Dft<9, INV> {
     }
   }
 };
-
-// x * W_R^e (e a compile-time constant after unrolling); trivial powers are free
-template <int R, bool INV>
-__device__ __forceinline__ double2 tw_mul(double2 x, int e) {
-  e %= R;
-  if (e == 0) return x;
-  if (2 * e == R) return make_double2(-x.x, -x.y);
-  if (4 * e == R) return mul_mi<INV>(x);
-  if (4 * e == 3 * R) return mul_mi<!INV>(x);
-  const double c = TwC<R>::c(e);
-  const double s = INV ? TwC<R>::s(e) : -TwC<R>::s(e);
-  return make_double2(fma(x.x, c, -x.y * s), fma(x.x, s, x.y * c));
-}
-
-// Composite R = P x Q in registers: inputs a[r + Q j] (r < Q, j < P); inner DFT_P over j,
-// twiddle W_R^{r k1}, outer DFT_Q over r; output index k1 + P k2.
-template <int P, int Q, bool INV>
-struct DftPQ {
-  static __device__ __forceinline__ void run(double2* a) {
-    constexpr int R = P * Q;
-    double2 u[Q][P];
-#pragma unroll
-    for (int r = 0; r < Q; ++r) {
-#pragma unroll
-      for (int j = 0; j < P; ++j) u[r][j] = a[r + Q * j];
-      Dft<P, INV>::run(u[r]);
-      if (r > 0) {
-#pragma unroll
-        for (int k1 = 1; k1 < P; ++k1) u[r][k1] = tw_mul<R, INV>(u[r][k1], r * k1);
-      }
-    }
-#pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) {
-      double2 v[Q];
-#pragma unroll
-      for (int r = 0; r < Q; ++r) v[r] = u[r][k1];
-      Dft<Q, INV>::run(v);
-#pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) a[k1 + P * k2] = v[k2];
-    }
-  }
-};
-
-template <bool INV> struct Dft<12, INV> : DftPQ<4, 3, INV> {};
-template <bool INV> struct Dft<16, INV> : DftPQ<4, 4, INV> {};
-template <bool INV> struct Dft<18, INV> : DftPQ<2, 9, INV> {};
-template <bool INV> struct Dft<24, INV> : DftPQ<8, 3, INV> {};
-template <bool INV> struct Dft<27, INV> : DftPQ<3, 9, INV> {};
-template <bool INV> struct Dft<32, INV> : DftPQ<4, 8, INV> {};
-template <bool INV> struct Dft<36, INV> : DftPQ<4, 9, INV> {};
 
 // ----------------------------------------------------------------- one stage
 // Stage twiddles: each stage with Ns > 1 owns a block tw[jm] = W_{Ns R}^{jm}, jm < Ns (the
