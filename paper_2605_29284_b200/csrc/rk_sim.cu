@@ -264,8 +264,11 @@ struct CsRngArgs {
 // in shared memory and evaluated by all lanes together, so a warp pays one tail round per
 // iteration instead of running both branches for every lane.
 constexpr int kRngThreads = 256;
+#ifndef RK_RNG_MINB
+#define RK_RNG_MINB 4
+#endif
 
-__global__ void __launch_bounds__(kRngThreads) cs_rng_kernel(const CsRngArgs a) {
+__global__ void __launch_bounds__(kRngThreads, RK_RNG_MINB) cs_rng_kernel(const CsRngArgs a) {
   __shared__ double tq[kRngThreads / 32][8 * 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double* wq = tq[wid];

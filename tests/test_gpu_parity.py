@@ -400,3 +400,26 @@ def test_predict_exact_and_se_against_reference(pk, tag):
             pk.predict_exact(f, tg)
         with pytest.raises(pk.DomainError):
             pk.kriging_se_exact(f, tg, xt[:, :2])
+
+
+def test_concurrent_streams_share_one_setup(pk):
+    """A setup is immutable and shareable across concurrent predicts: two CUDA
+    streams, each with its own workspace / captured graph, give the sequential results."""
+    import torch
+    rng = np.random.default_rng(12)
+    obs = rng.uniform(0, 1, size=(300, 2))
+    model = pk.CovarianceModel(1.0, 7.0, 1.5, 0.02)
+    grid = pk.build_padded_grid(UNIT, (90, 70), 3, obs)
+    st = pk.build_setup(model, grid, 3, obs)
+    cs = [torch.as_tensor(rng.normal(size=300), device="cuda") for _ in range(4)]
+    beta = torch.as_tensor([0.7], device="cuda")
+    want = [pk.predict_rapid(st, c, beta).cpu().numpy() for c in cs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty((70, 90), dtype=torch.float64, device="cuda") for _ in range(4)]
+    for rep in range(3):   # first use eager, second captures, third replays
+        for k in range(4):
+            with torch.cuda.stream(streams[k % 2]):
+                pk.predict_rapid(st, cs[k], beta, out=outs[k])
+        torch.cuda.synchronize()
+        for k in range(4):
+            assert np.array_equal(outs[k].cpu().numpy(), want[k]), (rep, k)
