@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(kRngThreads, RK_RNG_MINB) cs_rng_kernel(const 
   const int dy = (int)(dstep / (uint32_t)a.ps1), dx = (int)(dstep % (uint32_t)a.ps1);
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   int iy = (int)(4 * t / (uint32_t)a.ps1), ix = (int)(4 * t - (uint32_t)iy * a.ps1);
+  const bool quad_rows = (a.ps1 & 3) == 0;
   // warp-uniform grid-stride loop (the compaction uses full-warp shuffles)
   for (uint32_t t0 = t - lane; t0 < nblk; t0 += stride, t += stride) {
     const bool valid = t < nblk;
@@ -332,7 +333,15 @@ __global__ void __launch_bounds__(kRngThreads, RK_RNG_MINB) cs_rng_kernel(const 
         if (tmask >> q & 1) z[q] = wq[o++];
       __syncwarp();
     }
-    if (valid) {
+    if (valid && quad_rows) {   // the 4 words lie in one row, all in range (ps1 % 4 == 0)
+      const double* rq = a.root_q + min(iy, a.ps2 - iy) * a.rq_ld;
+      double2* zp = Z + 4 * t;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double r = __ldg(&rq[min(ix + q, a.ps1 - ix - q)]);
+        zp[q] = make_double2(r * z[q], r * z[4 + q]);
+      }
+    } else if (valid) {
       uint32_t p = 4 * t;
       int jy = iy, jx = ix;
 #pragma unroll
