@@ -416,6 +416,129 @@ __global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_rowfft_ker
   }
 }
 
+// Fused CS pass A: each line's threads generate its row of Z = sqrt(lambda) (re + i im) straight
+// into shared memory (Philox words, inverse normals with warp-level tail compaction), then run
+// the inverse row FFT and store the kept columns transposed.  No Z round trip through HBM, and
+// CTAs of one SM in different phases overlap integer (Philox) and FP64 / smem (FFT) work.
+struct CsGenArgs {
+  FftPlan pl;
+  int lpc;
+  uint64_t seed;
+  int64_t j0;
+  int direct;
+  int ps1, ps2;
+  const double* root_q;
+  int rq_ld;
+  int keep;                  // M1
+  double2* V;
+  int64_t ldV, V_bstride;
+  int tw_off, q_off;         // smem offsets (double2 units): twiddles, tail queues
+};
+
+// words w .. w+3 of the (fs, 0) Philox stream; two blocks when w is not block aligned
+__device__ __forceinline__ void philox_words4(uint64_t w, uint64_t fs, uint64_t o[4]) {
+  uint64_t a[4], c[4];
+  const uint64_t blk = w >> 2;
+  const int off = (int)(w & 3);
+  philox4x64_10(blk + 1, fs, 0, a);
+  if (off == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) o[q] = a[q];
+    return;
+  }
+  philox4x64_10(blk + 2, fs, 0, c);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {   // compile-time indices only
+    const uint64_t x1 = q + 1 < 4 ? a[q + 1] : c[q - 3];
+    const uint64_t x2 = q + 2 < 4 ? a[q + 2] : c[q - 2];
+    const uint64_t x3 = q + 3 < 4 ? a[q + 3] : c[q - 1];
+    o[q] = off == 1 ? x1 : off == 2 ? x2 : x3;
+  }
+}
+
+template <bool TWS, bool WIDE>
+__global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_rowgen_kernel(const CsGenArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int n = a.pl.n;
+  const int nthr = a.pl.nthr;
+  const int line = threadIdx.x / nthr;
+  const int tl = threadIdx.x - line * nthr;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const int iy = blockIdx.x * a.lpc + line;
+  double2* buf = smem + (size_t)line * n;
+  double* wq = (double*)(smem + a.q_off) + (size_t)(threadIdx.x >> 5) * 256;
+  const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
+  const uint64_t fs = a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
+  if (iy < a.ps2) {
+    const uint64_t Ps = (uint64_t)a.ps1 * (uint64_t)a.ps2;
+    const uint64_t wre = (uint64_t)iy * a.ps1, wim = Ps + wre;   // simulate.py:114-115
+    const double* rq = a.root_q + (int64_t)min(iy, a.ps2 - iy) * a.rq_ld;
+    const int ng = (a.ps1 + 3) / 4;
+    for (int g0 = tl - lane; g0 < ng; g0 += nthr) {   // warp-uniform (nthr % 32 == 0)
+      const int g = g0 + lane;
+      const int x0 = 4 * g;
+      uint64_t re[4], im[4];
+      philox_words4(wre + x0, fs, re);
+      philox_words4(wim + x0, fs, im);
+      double uu[8], z[8];
+      unsigned tmask = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uu[q] = word_uniform(q < 4 ? re[q] : im[q - 4]);
+        if (g < ng && x0 + (q & 3) < a.ps1 && ndtri_is_tail(uu[q])) tmask |= 1u << q;
+      }
+      ndtri_central_n<8>(uu, z);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) z[q] = uu[q];
+      const int cnt = __popc(tmask);
+      int off = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, off, d);
+        if (lane >= d) off += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, off, 31);
+      off -= cnt;
+      if (total) {
+        int o = off;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (tmask >> q & 1) wq[o++] = z[q];
+        __syncwarp();
+        for (int k = lane; k < total; k += 32) wq[k] = ndtri_tail(wq[k]);
+        __syncwarp();
+        o = off;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (tmask >> q & 1) z[q] = wq[o++];
+        __syncwarp();
+      }
+      if (g < ng) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int x = x0 + q;
+          if (x < a.ps1) {
+            const double r = __ldg(&rq[min(x, a.ps1 - x)]);
+            buf[x] = make_double2(r * z[q], r * z[4 + q]);
+          }
+        }
+      }
+    }
+  } else {
+    for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_line<true, TWS, WIDE>(buf, pls, tl);
+  double2* V = a.V + (int64_t)b * a.V_bstride;
+  for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
+    const int l = idx % a.lpc, ix = idx / a.lpc;
+    const int row = blockIdx.x * a.lpc + l;
+    if (row < a.ps2) V[(int64_t)ix * a.ldV + row] = smem[(size_t)l * n + ix];
+  }
+}
+
 static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, int batch,
                             double* g, cudaStream_t st) {
   RK_TRY(ensure_embedding(s, st));
@@ -424,7 +547,37 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   double2* V = nullptr;
   RK_TRY(scratch_alloc((void**)&V, sizeof(double2) * (size_t)s->M1 * ldV * batch, st));
   double2* Zs = nullptr;   // freed after the column pass so the two FFT kernels stay adjacent
-  {
+  static const bool fused = !(getenv("RK_CS_FUSED") && atoi(getenv("RK_CS_FUSED")) == 0);
+  if (fused) {
+    CsGenArgs ga{};
+    ga.pl = plan_pick(e.ps1v, (int64_t)e.ps2 * batch);
+    ga.lpc = pick_lpc(ga.pl, 4, (int64_t)e.ps2 * batch);
+    ga.seed = seed;
+    ga.j0 = j0;
+    ga.direct = direct;
+    ga.ps1 = e.ps1;
+    ga.ps2 = e.ps2;
+    ga.root_q = e.root_q;
+    ga.rq_ld = e.hs1;
+    ga.keep = s->M1;
+    ga.V = V;
+    ga.ldV = ldV;
+    ga.V_bstride = (int64_t)s->M1 * ldV;
+    const int warps = ga.lpc * ga.pl.nthr / 32;
+    ga.q_off = (int)(ga.lpc * (size_t)e.ps1);
+    ga.tw_off = ga.q_off + warps * 128;   // 256 doubles per warp
+    size_t smem = sizeof(double2) * ((size_t)ga.tw_off + ga.pl.ntw);
+    const bool tws = smem <= 227 * 1024;
+    if (!tws) smem = sizeof(double2) * (size_t)ga.tw_off;
+    if (ga.pl.wide == 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+    auto kern = ga.pl.wide == 2 ? cs_rowgen_kernel<true, true> : tws ? cs_rowgen_kernel<true, false>
+                                                                     : cs_rowgen_kernel<false, false>;
+    RK_TRY(set_smem_attr((const void*)kern, smem));
+    const dim3 grid((unsigned)ceil_div(e.ps2, ga.lpc), (unsigned)batch);
+    kern<<<grid, ga.lpc * ga.pl.nthr, smem, st>>>(ga);
+    count_launch();
+    RK_LAUNCH_CHECK();
+  } else {
     const int64_t Ps = (int64_t)e.ps1 * e.ps2;
     if (Ps >= (int64_t)1 << 31) return Status::err(RK_DOMAIN, "simulation torus larger than 2^31 nodes");
     double2* Z = nullptr;
