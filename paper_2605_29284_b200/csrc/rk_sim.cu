@@ -96,19 +96,30 @@ __global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_col_kernel
   const int line = threadIdx.x / nthr;
   const int tl = threadIdx.x - line * nthr;
   const int b = blockIdx.y;
-  const int ix = blockIdx.x * a.lpc + line;
+  // two columns per line: only Re(IFFT(V)) is kept, which is the IFFT of V's Hermitian part
+  // H[k] = (V[k] + conj V[-k]) / 2; the IFFT of H_a + i H_b is Re IFFT V_a + i Re IFFT V_b
+  const int ca = 2 * (blockIdx.x * a.lpc + line), cb = ca + 1;
   double2* buf = smem + (size_t)line * n;
-  const double2* V = a.V + (int64_t)b * a.V_bstride + (int64_t)ix * a.ldV;
+  const double2* Va = a.V + (int64_t)b * a.V_bstride + (int64_t)ca * a.ldV;
+  const double2* Vb = Va + a.ldV;
+  const bool va = ca < a.ncols, vb = cb < a.ncols;
   const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
   pdl_wait();   // V is the predecessor's output
-  for (int y = tl; y < n; y += nthr) buf[y] = ix < a.ncols ? V[y] : make_double2(0.0, 0.0);
+  for (int y = tl; y < n; y += nthr) {
+    const int m = y ? n - y : 0;
+    const double2 A = va ? Va[y] : make_double2(0.0, 0.0), Am = va ? Va[m] : make_double2(0.0, 0.0);
+    const double2 B = vb ? Vb[y] : make_double2(0.0, 0.0), Bm = vb ? Vb[m] : make_double2(0.0, 0.0);
+    buf[y] = make_double2(0.5 * ((A.x + Am.x) - (B.y - Bm.y)), 0.5 * ((A.y - Am.y) + (B.x + Bm.x)));
+  }
   __syncthreads();
   fft_line<true, TWS, WIDE>(buf, pls, tl);
   double* g = a.g + (int64_t)b * a.g_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, y = idx / a.lpc;
-    const int col = blockIdx.x * a.lpc + l;
-    if (col < a.ncols) g[(int64_t)y * a.ncols + col] = smem[(size_t)l * n + y].x;
+    const int c0 = 2 * (blockIdx.x * a.lpc + l);
+    const double2 v = smem[(size_t)l * n + y];
+    if (c0 < a.ncols) g[(int64_t)y * a.ncols + c0] = v.x;
+    if (c0 + 1 < a.ncols) g[(int64_t)y * a.ncols + c0 + 1] = v.y;
   }
 }
 
@@ -619,8 +630,9 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     Zs = Z;
   }
   CsColArgs ca{};
-  ca.pl = plan_pick(e.ps2v, (int64_t)s->M1 * batch);
-  ca.lpc = pick_lpc(ca.pl, 4, (int64_t)s->M1 * batch);
+  const int64_t cpairs = (s->M1 + 1) / 2;   // two columns per line
+  ca.pl = plan_pick(e.ps2v, cpairs * batch);
+  ca.lpc = pick_lpc(ca.pl, 4, cpairs * batch);
   ca.ncols = s->M1;
   ca.keep = s->M2;
   ca.V = V;
@@ -629,7 +641,7 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   ca.g = g;
   ca.g_bstride = (int64_t)s->M1 * s->M2;
   {
-    const dim3 grid((unsigned)ceil_div(s->M1, ca.lpc), (unsigned)batch);
+    const dim3 grid((unsigned)ceil_div(cpairs, ca.lpc), (unsigned)batch);
     ca.tw_off = (int)(ca.lpc * (size_t)e.ps2);
     size_t smem = sizeof(double2) * (e.ps2 * (size_t)ca.lpc + ca.pl.ntw);
     const bool tws = smem <= 227 * 1024;
