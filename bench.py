@@ -295,8 +295,9 @@ def time_predict_e2e(pk, case, steps, warmup, flush):
     xg = None if case["xg"] is None else torch.from_numpy(np.ascontiguousarray(case["xg"])).pin_memory().numpy()
     beta = np.ascontiguousarray(case["beta"])
     out = torch.empty((m2, m1), dtype=torch.float64).pin_memory().numpy()
-    # every buffer set is captured as a graph on its second use: warm all of them up
-    for k in range(max(warmup, 2 * len(ch) + 1)):
+    # every buffer set is captured as a graph on its second use; freshly pinned buffers and
+    # the PCIe path also take some tens of calls to reach steady state (tools/pcie_probe.py)
+    for k in range(max(warmup, 2 * len(ch) + 1, 50)):
         pk.predict_rapid(st, ch[k % len(ch)], beta, xg, out=out)
     ms = []
     gc.disable()   # host-side timing: keep collector pauses out of the per-call numbers

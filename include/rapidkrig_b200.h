@@ -122,7 +122,9 @@ rk_status rk_convolve_spectrum(const double* spec_q_dev, int32_t p1, int32_t p2,
 rk_status rk_predict_dev(const rk_setup* s, const double* c_dev, const double* beta_dev,
                          int32_t p, const double* xg_dev, double* out_dev, void* stream);
 /* Same call on HOST buffers: H2D of c / beta / xg, compute, D2H of the field,
- * synchronous on `stream`. */
+ * synchronous on `stream`, or on the setup's own non-blocking stream when `stream` is
+ * NULL (such calls on one setup are serialised).  Pinned buffers take one captured graph
+ * with the X_g upload on a side stream overlapping the first two passes. */
 rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta, int32_t p,
                           const double* xg, double* out, void* stream);
 

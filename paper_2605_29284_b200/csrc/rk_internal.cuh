@@ -129,6 +129,8 @@ struct rk_setup {
   rk::Embedding emb;
   std::mutex ws_mu;
   std::map<cudaStream_t, rk::Workspace*> ws;
+  std::mutex host_mu;               // serialises host-buffer predicts on the library's own stream
+  cudaStream_t host_st = nullptr;   // that stream (created on first use)
 };
 
 struct rk_fit {

@@ -846,6 +846,10 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
 }
 
 void free_workspaces(rk_setup* s) {
+  if (s->host_st) {
+    cudaStreamDestroy(s->host_st);
+    s->host_st = nullptr;
+  }
   for (auto& kv : s->ws) {
     Workspace* w = kv.second;
     for (auto& g : w->graphs) cudaGraphExecDestroy(g.second);
@@ -1056,8 +1060,15 @@ rk_status rk_predict_traffic(const rk_setup* s, int32_t p, double* b) {
 
 rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta, int32_t p,
                           const double* xg, double* out, void* stream) {
+  rk_setup* hs = const_cast<rk_setup*>(s);
+  std::unique_lock<std::mutex> host_lock(hs->host_mu, std::defer_lock);
   auto run = [&]() -> Status {
     cudaStream_t st = (cudaStream_t)stream;
+    if (!st) {   // no caller stream: the setup's own non-blocking stream, one call at a time
+      host_lock.lock();
+      if (!hs->host_st) RK_CUDA_TRY(cudaStreamCreateWithFlags(&hs->host_st, cudaStreamNonBlocking));
+      st = hs->host_st;
+    }
     if (beta && !xg && p != 1)
       return Status::err(RK_DOMAIN, "grid covariates are required when beta_hat has more than one entry");
     if (p > 16) return Status::err(RK_DOMAIN, "at most 16 covariates");

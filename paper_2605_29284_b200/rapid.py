@@ -233,8 +233,8 @@ def predict_rapid(setup: RapidSetup, c, beta_hat=None, grid_covariates=None, *, 
     bh = None if beta is None else (beta.cpu().numpy() if D.is_device_tensor(beta) else beta)
     xh = None if xg is None else (xg.cpu().numpy() if D.is_device_tensor(xg) else D.host_f64(xg))
     res = np.empty((m2, m1)) if out is None else out
-    N.call("rk_predict_host", setup.handle, N.ptr(ch), N.ptr(bh), p, N.ptr(xh), N.ptr(res),
-           N.stream_ptr())
+    # synchronous host-buffer call: on the setup's own stream (no torch stream lookup)
+    N.call("rk_predict_host", setup.handle, N.ptr(ch), N.ptr(bh), p, N.ptr(xh), N.ptr(res), None)
     return res
 
 
