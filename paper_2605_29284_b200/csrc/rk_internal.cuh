@@ -59,8 +59,8 @@ struct GraphKey {
 struct Workspace {
   double2* T = nullptr;         // (H1, ldT)
   double2* U = nullptr;         // (H1, ldU)
-  double* c_in = nullptr;       // host-path staging
-  double* beta_in = nullptr;
+  double* c_in = nullptr;       // host-path staging: c, then beta at an even offset
+  double* beta_in = nullptr;    // (inside the c_in allocation)
   double* xg_in = nullptr;
   size_t xg_cap = 0;
   double* out = nullptr;
@@ -73,7 +73,7 @@ struct Workspace {
   cudaStream_t aux = nullptr;
   cudaEvent_t fork = nullptr;
   cudaEvent_t xev[kMaxChunks] = {};
-  double* beta_h = nullptr;     // pinned copy of beta (16)
+  double* cb_h = nullptr;       // pinned staging of c and beta (beta at beta_in - c_in)
   std::map<GraphKey, cudaGraphExec_t> hgraphs;
   std::map<GraphKey, int> hseen;
 };

@@ -832,14 +832,16 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
   const int64_t ldT = round_even(s->M2), ldU = round_even(s->m2);
   RK_CUDA_TRY(cudaMalloc(&w->T, sizeof(double2) * (size_t)s->H1 * ldT));
   RK_CUDA_TRY(cudaMalloc(&w->U, sizeof(double2) * (size_t)s->H1 * ldU));
-  RK_CUDA_TRY(cudaMalloc(&w->c_in, sizeof(double) * std::max<int64_t>(s->n, 2)));
-  RK_CUDA_TRY(cudaMalloc(&w->beta_in, sizeof(double) * 16));
+  // c and beta staged back to back (one upload per host-path call): beta at an even offset
+  const int64_t boff = (std::max<int64_t>(s->n, 2) + 1) & ~int64_t(1);
+  RK_CUDA_TRY(cudaMalloc(&w->c_in, sizeof(double) * (boff + 16)));
+  w->beta_in = w->c_in + boff;
   RK_CUDA_TRY(cudaMalloc(&w->out, sizeof(double) * (size_t)s->m1 * s->m2));
   RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
   RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->aux, cudaStreamNonBlocking));
   RK_CUDA_TRY(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
   for (auto& e : w->xev) RK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  RK_CUDA_TRY(cudaMallocHost(&w->beta_h, sizeof(double) * 16));
+  RK_CUDA_TRY(cudaMallocHost(&w->cb_h, sizeof(double) * (boff + 16)));
   s->ws[st] = w;
   *out = w;
   return Status::ok();
@@ -858,11 +860,10 @@ void free_workspaces(rk_setup* s) {
     if (w->fork) cudaEventDestroy(w->fork);
     for (auto& e : w->xev)
       if (e) cudaEventDestroy(e);
-    cudaFreeHost(w->beta_h);
+    cudaFreeHost(w->cb_h);
     cudaFree(w->T);
     cudaFree(w->U);
-    cudaFree(w->c_in);
-    cudaFree(w->beta_in);
+    cudaFree(w->c_in);   // beta_in lives in the same allocation
     cudaFree(w->xg_in);
     cudaFree(w->out);
     if (w->cap) cudaStreamDestroy(w->cap);
@@ -1110,20 +1111,31 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
     }
     // pinned buffers: uploads, kernels and downloads in one graph; X_g rows go up on the
     // side stream in row blocks that pass 3 consumes as they land
-    if (beta) memcpy(w->beta_h, beta, sizeof(double) * p);   // previous call has completed
+    // c and beta into one pinned staging block (the previous call has completed)
+    const int64_t boff = w->beta_in - w->c_in;
+    memcpy(w->cb_h, c, sizeof(double) * s->n);
+    if (beta) memcpy(w->cb_h + boff, beta, sizeof(double) * p);
+    const size_t cb_bytes = sizeof(double) * (size_t)(beta ? boff + p : s->n);
     // one block by default: on B200 (cfg2, 2.9 MB of X_g) the single side-stream upload
     // hidden behind the gather / FFT passes measured 114 us per call; 2 / 4 / 8 row blocks
     // 294 / 169 / 279 us (the interleaved small copies serialise on the copy engines)
     static const int k_env = getenv("RK_HOST_CHUNKS") ? atoi(getenv("RK_HOST_CHUNKS")) : 1;
     static const int graph_env = getenv("RK_HOST_GRAPH") ? atoi(getenv("RK_HOST_GRAPH")) : 1;
     const int K = std::max(1, std::min(k_env, Workspace::kMaxChunks));
+    // pass 3 writes the field straight into the pinned output through its device mapping:
+    // the device -> host traffic overlaps the last pass instead of following it
+    static const int zc_env = getenv("RK_HOST_ZEROCOPY") ? atoi(getenv("RK_HOST_ZEROCOPY")) : 1;
+    double* out_map = nullptr;
+    if (zc_env && cudaHostGetDevicePointer((void**)&out_map, out, 0) != cudaSuccess) {
+      cudaGetLastError();
+      out_map = nullptr;
+    }
+    if (out_map) pb.out = out_map;
     auto enqueue = [&](cudaStream_t q) -> Status {
-      RK_CUDA_TRY(cudaMemcpyAsync(w->c_in, c, sizeof(double) * s->n, cudaMemcpyHostToDevice, q));
-      if (beta) RK_CUDA_TRY(cudaMemcpyAsync(w->beta_in, w->beta_h, sizeof(double) * p, cudaMemcpyHostToDevice, q));
       HostIo hio;
       hio.chunks = K;
-      hio.out_host = out;
-      if (xg) {
+      hio.out_host = out_map ? nullptr : out;
+      if (xg) {   // fork first: the X_g upload starts before anything else
         RK_CUDA_TRY(cudaEventRecord(w->fork, q));
         RK_CUDA_TRY(cudaStreamWaitEvent(w->aux, w->fork, 0));
         const int per = chunk_rows(s->m2, K);
@@ -1136,6 +1148,7 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
         }
         hio.xev = w->xev;
       }
+      RK_CUDA_TRY(cudaMemcpyAsync(w->c_in, w->cb_h, cb_bytes, cudaMemcpyHostToDevice, q));
       return predict_batch(s, pb, q, nullptr, w, &hio);
     };
     const GraphKey key{(uintptr_t)c, (uintptr_t)(beta ? 1 : 0), (uintptr_t)xg, (uintptr_t)out, p};
