@@ -148,7 +148,9 @@ struct rk_fit {
   rk::MaternDev mat{};
   std::vector<double> gram_lu;  // (p, p) LU of B'B with partial pivoting (row-major)
   std::vector<int> gram_piv;
-  void* cublas = nullptr;
+  void* cublas = nullptr;                    // handle of the creating thread / default stream
+  std::mutex blas_mu;
+  std::map<cudaStream_t, void*> blas_by_stream;   // one handle per stream (own workspace)
 };
 
 namespace rk {

@@ -696,6 +696,23 @@ static Status obs_local(const rk_setup* s, double tau2, const double* g, uint64_
                                       " at " #expr);                                        \
   } while (0)
 
+// cuBLAS handle for `st`: one per stream, so ensemble chunks running concurrently on
+// different streams never share a handle's workspace
+static Status blas_for(rk_fit* f, cudaStream_t st, cublasHandle_t* out) {
+  std::lock_guard<std::mutex> lk(f->blas_mu);
+  auto it = f->blas_by_stream.find(st);
+  cublasHandle_t h;
+  if (it != f->blas_by_stream.end()) {
+    h = (cublasHandle_t)it->second;
+  } else {
+    RK_CUBLAS_TRY(cublasCreate(&h));
+    f->blas_by_stream[st] = h;
+  }
+  RK_CUBLAS_TRY(cublasSetStream(h, st));
+  *out = h;
+  return Status::ok();
+}
+
 // dense M = K + tau2 I (+ ridge) column-major, cdist distances (covariance.py:100-116)
 __global__ void dense_cov_kernel(MaternDev P, const double* __restrict__ obs, int64_t n, double diag_add,
                                  double* __restrict__ Mm, int* bad) {
@@ -796,8 +813,8 @@ static GramLU gram_args(const rk_fit* f) {
 // column-major) -> beta (p x batch), C (n x batch).  Used once per fit.
 static Status gls_trsm(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C,
                         cudaStream_t st) {
-  cublasHandle_t h = (cublasHandle_t)f->cublas;
-  RK_CUBLAS_TRY(cublasSetStream(h, st));
+  cublasHandle_t h;
+  RK_TRY(blas_for(const_cast<rk_fit*>(f), st, &h));
   const int n = (int)f->n, p = f->p, nb = (int)batch;
   const double one = 1.0, zero = 0.0;
   double* A = nullptr;
@@ -830,8 +847,8 @@ static Status ensure_uinv(rk_fit* f, cudaStream_t st);
 //   A = L^-1 Z ; beta = (B'B)^-1 B'A ; H = A - B beta (= L^-1 (Z - X beta)) ; C = L^-T H
 static Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C,
                         cudaStream_t st) {
-  cublasHandle_t h = (cublasHandle_t)f->cublas;
-  RK_CUBLAS_TRY(cublasSetStream(h, st));
+  cublasHandle_t h;
+  RK_TRY(blas_for(const_cast<rk_fit*>(f), st, &h));
   const int n = (int)f->n, p = f->p, nb = (int)batch;
   const double one = 1.0, zero = 0.0;
   RK_TRY(ensure_uinv(const_cast<rk_fit*>(f), st));
@@ -864,6 +881,7 @@ static void free_fit(rk_fit* f) {
   cudaFree(f->beta);
   cudaFree(f->c);
   if (f->cublas) cublasDestroy((cublasHandle_t)f->cublas);
+  for (auto& kv : f->blas_by_stream) cublasDestroy((cublasHandle_t)kv.second);
   delete f;
 }
 
@@ -1451,8 +1469,8 @@ rk_status rk_kriging_se_exact(rk_fit* f, const double* targets_dev, int64_t nt, 
     unsigned long long zero_bits;
     memcpy(&zero_bits, &zero_d, sizeof zero_bits);
     RK_CUDA_TRY(cudaMemcpyAsync(minv, &zero_bits, sizeof zero_bits, cudaMemcpyHostToDevice, st));
-    cublasHandle_t h = (cublasHandle_t)f->cublas;
-    RK_CUBLAS_TRY(cublasSetStream(h, st));
+    cublasHandle_t h;
+    RK_TRY(blas_for(const_cast<rk_fit*>(f), st, &h));
     const double one = 1.0, zer = 0.0;
     const GramLU g = gram_args(f);
     for (int64_t j0 = 0; j0 < nt; j0 += tc) {
