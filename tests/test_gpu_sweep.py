@@ -54,3 +54,27 @@ def test_random_configs_match_oracle(seed):
     ours = pk.predict_rapid(st, c, beta, xg)
     ref = ro.predict(ost, c, beta, xg)
     assert rel_err(ours, ref) < 1e-10, (seed, nu, L, dims, p)
+
+
+@pytest.mark.parametrize("dims,L,nu,alpha", [((24, 26), 2, 1.0, 12.0),    # torus 54 x 54 (not 4-aligned rows)
+                                             ((38, 36), 2, 0.5, 20.0),    # 81 x 81: odd rows
+                                             ((30, 50), 3, 1.5, 9.0),     # mixed sizes
+                                             ((60, 20), 1, 2.5, 25.0),
+                                             ((25, 31), 1, 1.0, 15.0)])   # odd M1: last column unpaired
+def test_unconditional_fields_any_torus_alignment(dims, L, nu, alpha):
+    """The fused Philox + row-IFFT generator (rows whose first word is not Philox-block
+    aligned when ps1 % 4 != 0) and the paired column pass against the oracle's field."""
+    import paper_2605_29284_b200 as pk
+    from paper_2605_29284_b200.simulate import embedding_dims
+    rng = np.random.default_rng(dims[0] * 100 + dims[1])
+    obs = rng.uniform(0, 1, size=(30, 2))
+    model = pk.CovarianceModel(1.0, alpha, nu, 0.05)
+    om = ro.Model(1.0, alpha, nu, 0.05)
+    grid = pk.build_padded_grid(UNIT, dims, L, obs)
+    og = ro.make_grid(UNIT, dims, L, obs)
+    root = ro.embedding_root(om, og)
+    assert embedding_dims(model, grid)[:2] == (root[0], root[1])
+    for seed in (3, 2 ** 63 + 5):
+        ours = pk.sim_unconditional_grid(model, grid, seed)
+        ref = ro.uncond_field(om, og, seed, root)
+        assert rel_err(ours, ref) < 1e-10, (dims, seed, root[:2])
