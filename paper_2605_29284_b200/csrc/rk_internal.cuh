@@ -175,4 +175,9 @@ void free_workspaces(rk_setup* s);
 // CS pieces (rk_sim.cu)
 Status ensure_embedding(rk_setup* s, cudaStream_t st);
 
+// exact-Kriging pieces (rk_exact.cu) used by the ensemble driver
+// batched refit: Z (n x batch, column-major) -> beta (p x batch), C (n x batch)
+Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C, cudaStream_t st);
+Status ensure_uinv(rk_fit* f, cudaStream_t st);   // U^-1 for the batched refits, built once
+
 }  // namespace rk
