@@ -61,7 +61,7 @@ Status plan_for(int n, FftPlan* out, int wide) {
   FftPlan pl{};
   if (!fft_factor(n, &pl, wide))
     return Status::err(RK_INTERNAL, "FFT length " + std::to_string(n) + " is not 2^a 3^b");
-  if (pl.nthr > (wide == 2 ? kFftWideThreads : 512))
+  if (pl.nthr > fft_sm_threads(wide))
     return Status::err(RK_DOMAIN, "FFT length " + std::to_string(n) + " too large for one CTA");
   std::vector<double2> tw;
   fft_stage_twiddles(pl, tw, [](double c, double s) { return make_double2(c, s); });
@@ -79,26 +79,32 @@ Status plan_for(int n, FftPlan* out, int wide) {
 Status plan_set(int n, PlanSet* out) {
   RK_TRY(plan_for(n, &out->v[0]));
   // the variants keep the stage twiddle table in smem next to the line: n <= 4608
-  for (int w = 1; w <= 2; ++w)
+  for (int w = 1; w <= 3; ++w)
     if (n > 4608 || !plan_for(n, &out->v[w], w).good()) out->v[w] = FftPlan{};
+  if (out->v[3].n && out->v[3].n9 == 0) out->v[3] = FftPlan{};   // split needs radix-9 stages
   return Status::ok();
 }
 
 const FftPlan& plan_pick(const PlanSet& ps, int64_t lines) {
-  // RK_WIDE: 0 normal only, 1 auto, 2 spread where available, 3 wide where available
+  // RK_WIDE: 0 normal only, 1 auto, 2 spread, 3 wide, 4 split (where available)
   static const int mode = getenv("RK_WIDE") ? atoi(getenv("RK_WIDE")) : 1;
   const FftPlan& sp = ps.v[1];
   const FftPlan& wd = ps.v[2];
+  const FftPlan& sl = ps.v[3];
   if (mode == 0) return ps.v[0];
   if (mode == 2) return sp.n ? sp : ps.v[0];
   if (mode == 3) return wd.n ? wd : ps.v[0];
-  if (sp.n && sp.nthr > ps.v[0].nthr) {   // one wave with the spread plan?
-    const int lpc = pick_lpc(sp, 4, lines);
-    const size_t line_bytes = (size_t)sp.n * sizeof(double2);
-    const int by_regs = 512 / (lpc * sp.nthr);
+  if (mode == 4) return sl.n ? sl : ps.v[0];
+  auto one_wave = [&](const FftPlan& pl) {   // every CTA of the launch resident at once?
+    if (!pl.n || pl.nthr <= ps.v[0].nthr) return false;
+    const int lpc = pick_lpc(pl, 4, lines);
+    const size_t line_bytes = (size_t)pl.n * sizeof(double2);
+    const int by_regs = fft_sm_threads(pl.wide) / (lpc * pl.nthr);
     const int by_smem = (int)((227 * 1024) / (lpc * line_bytes + line_bytes / 8 + 64));
-    if (ceil_div(lines, lpc) <= 148LL * std::min(by_regs, by_smem)) return sp;
-  }
+    return by_regs > 0 && ceil_div(lines, lpc) <= 148LL * std::min(by_regs, by_smem);
+  };
+  if (one_wave(sl)) return sl;
+  if (one_wave(sp)) return sp;
   return wd.n ? wd : ps.v[0];
 }
 
@@ -115,7 +121,7 @@ int pick_lpc(const FftPlan& pl, int max_lines, int64_t total_lines) {
   }();
   int best = 1;
   int64_t best_res = -1;
-  const int tmax = pl.wide == 2 ? kFftWideThreads : 512;   // resident FFT threads per SM (registers)
+  const int tmax = fft_sm_threads(pl.wide);   // resident FFT threads per SM (registers)
   for (int lpc = 1; lpc <= std::max(1, max_lines); ++lpc) {
     const int threads = lpc * pl.nthr;
     const size_t smem = lpc * line_bytes + line_bytes / 8 + 64;

@@ -39,7 +39,8 @@ struct FftPlan {
   int n9, r3, n8, r2;          // r3 in {1,3,6}, r2 in {1,2,4,16}; 16 = two radix-4 stages
   int ntw;                     // entries of the stage twiddle table (sum of Ns > 1)
   int wide;                    // 0 normal; 1 spread (one butterfly per thread, <= 512 threads);
-                               // 2 built for the WIDE kernels (fft_kmax_wide butterflies per thread)
+                               // 2 built for the WIDE kernels (fft_kmax_wide butterflies per thread);
+                               // 3 split radix-9 stages (fft_stage9_split, three lanes each)
   const double2* tw;           // per-stage twiddles, see fft_stage_twiddles()
 };
 
@@ -59,6 +60,12 @@ __device__ __forceinline__ FftPlan fft_twiddles_to_smem(const FftPlan& pl, doubl
 __host__ __device__ constexpr int fft_kmax_wide(int r) { return r >= 8 ? 1 : 2; }
 // threads per SM (and at most per line) of the WIDE kernels' launch bound
 constexpr int kFftWideThreads = 1024;
+// resident threads per SM of the split-radix-9 kernels (launch bound 576: <= 113 registers,
+// two 288-thread lines of a 729-point transform per SM)
+constexpr int kFftSplitThreads = 576;
+__host__ __device__ constexpr int fft_sm_threads(int wide) {
+  return wide == 2 ? kFftWideThreads : wide == 3 ? kFftSplitThreads : 512;
+}
 __host__ __device__ constexpr int fft_kmax(int r) {
   return r == 2 ? 9 : r == 3 ? 6 : r == 4 ? 4 : r == 6 ? 3 : r == 8 ? 2 : r == 9 ? 2 : r == 12 ? 2 : 1;
 }
@@ -244,16 +251,93 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
   __syncthreads();
 }
 
+// Radix-9 stage with each butterfly split over three lanes (the 3 x 3 form of Dft<9>): lane r
+// of a triple loads x[j + (r + 3 m) nb], applies the same twiddle powers, runs the first DFT3
+// and the internal twiddles, the triple transposes its 3 x 3 intermediate through two
+// shuffle rounds, and lane k1 runs the second DFT3 and stores outputs k1, k1 + 3, k1 + 6.
+// Ten butterflies per warp (lanes 30, 31 idle).  The arithmetic -- twiddle running products,
+// codelet, rounding -- is the one of fft_stage<9>, so every plan gives bitwise the same line;
+// what changes is the serial FP64 work per thread (~72 instead of ~148 instructions), which
+// is what a radix-9 stage of a latency-bound line waits on.
+template <bool INV, bool TWS>
+__device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int n, int Ns, int t,
+                                                 const double2* __restrict__ tw) {
+  const double C1 = 7.66044443118978013452e-01, S1 = 6.42787609686539362919e-01;
+  const double C2 = 1.73648177666930358942e-01, S2 = 9.84807753012208020316e-01;
+  const double C4 = -9.39692620785908427905e-01, S4 = 3.42020143325668712908e-01;
+  const double sg = INV ? 1.0 : -1.0;
+  const int nb = n / 9;
+  const int lane = t & 31;
+  const int sub = lane / 3, r = lane - 3 * sub;
+  const int j = (t >> 5) * 10 + sub;
+  const bool valid = lane < 30 && j < nb;
+  const int jm = valid ? j % Ns : 0;
+  double2 c0 = make_double2(0.0, 0.0), c1 = c0, c2 = c0;
+  if (valid) {
+    double2 a0 = buf[j + r * nb], a1 = buf[j + (r + 3) * nb], a2 = buf[j + (r + 6) * nb];
+    if (jm != 0) {   // powers w^r, w^(r+3), w^(r+6) from the running product of fft_stage
+      const double2 w1 = TWS ? tw[jm] : __ldg(&tw[jm]);
+      double2 wp[9];
+      wp[1] = w1;
+#pragma unroll
+      for (int k = 2; k < 9; ++k) wp[k] = cmul(wp[k - 1], w1);
+      const double2 wr = r == 1 ? wp[1] : wp[2];
+      const double2 wr3 = r == 0 ? wp[3] : r == 1 ? wp[4] : wp[5];
+      const double2 wr6 = r == 0 ? wp[6] : r == 1 ? wp[7] : wp[8];
+      if (r) a0 = INV ? cmulc(a0, wr) : cmul(a0, wr);
+      a1 = INV ? cmulc(a1, wr3) : cmul(a1, wr3);
+      a2 = INV ? cmulc(a2, wr6) : cmul(a2, wr6);
+    }
+    dft3<INV>(a0, a1, a2);
+    if (r) {   // internal twiddles w9^(r k1)
+      a1 = cmul(a1, r == 1 ? make_double2(C1, sg * S1) : make_double2(C2, sg * S2));
+      a2 = cmul(a2, r == 1 ? make_double2(C2, sg * S2) : make_double2(C4, sg * S4));
+    }
+    c0 = a0;
+    c1 = a1;
+    c2 = a2;
+  }
+  // transpose within the triple: lane r ends with d_m = C_m[r] (m = the sender's r); only
+  // compile-time register names (a runtime array index would spill to local memory)
+  const double2 own = r == 0 ? c0 : r == 1 ? c1 : c2;
+  double2 d0 = own, d1 = own, d2 = own;
+#pragma unroll
+  for (int rd = 1; rd < 3; ++rd) {
+    const int give = r + rd >= 3 ? r + rd - 3 : r + rd;      // C_self[(r + rd) % 3]
+    const double2 v = give == 0 ? c0 : give == 1 ? c1 : c2;
+    const int from = r - rd < 0 ? r - rd + 3 : r - rd;       // sender's r
+    const int src = 3 * sub + from;
+    double2 got;
+    got.x = __shfl_sync(0xffffffffu, v.x, src);
+    got.y = __shfl_sync(0xffffffffu, v.y, src);
+    if (from == 0) d0 = got;
+    else if (from == 1) d1 = got;
+    else d2 = got;
+  }
+  if (valid) dft3<INV>(d0, d1, d2);
+  __syncthreads();
+  if (valid) {
+    const int ob = (j - jm) * 9 + jm;
+    buf[ob + r * Ns] = d0;
+    buf[ob + (r + 3) * Ns] = d1;
+    buf[ob + (r + 6) * Ns] = d2;
+  }
+  __syncthreads();
+}
+
 // Full transform of the line at `buf` by thread t (0 <= t < pl.nthr or idle beyond).
-// Must be called by every thread of the CTA (contains barriers).
-template <bool INV, bool TWS = false, bool WIDE = false>
+// Must be called by every thread of the CTA (contains barriers).  FM (FFT mode): 0 normal /
+// spread plans, 1 WIDE (64-register kernels), 2 split radix-9 stages.
+template <bool INV, bool TWS = false, int FM = 0>
 __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t) {
+  constexpr bool WIDE = FM == 1;
   const int n = pl.n, nthr = pl.nthr;
   const double2* tw = pl.tw;   // stage 1 (Ns = 1) needs no twiddles and has no block
   int Ns = 1;
 #pragma unroll 1
   for (int s = 0; s < pl.n9; ++s) {
-    fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
+    if (FM == 2) fft_stage9_split<INV, TWS>(buf, n, Ns, t, tw);
+    else fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
     if (Ns > 1) tw += Ns;
     Ns *= 9;
   }
@@ -338,6 +422,11 @@ inline bool fft_factor(int n, FftPlan* pl, int wide = 0) {
     int mx = 1;
     for (int i = 0; i < pl->nstages; ++i) mx = mx > n / rad[i] ? mx : n / rad[i];
     need = need > (mx < 512 ? mx : 512) ? need : (mx < 512 ? mx : 512);
+  } else if (wide == 3) {   // split radix-9 stages: 3 lanes per butterfly, 10 per warp
+    if (pl->n9 > 0) {
+      const int w9 = ((n / 9) + 9) / 10 * 32;
+      need = need > w9 ? need : w9;
+    }
   } else if (wide == 2) {   // fft_kmax_wide butterflies per thread, up to 1024 threads per line
     need = 1;
     for (int i = 0; i < pl->nstages; ++i) {

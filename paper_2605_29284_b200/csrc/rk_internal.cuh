@@ -14,9 +14,10 @@ namespace rk {
 // --------------------------------------------------------------- bookkeeping
 void count_launch(int k = 1);
 Status plan_for(int n, FftPlan* out, int wide = 0);   // cached per (device, n, wide)
-// the plan variants of one length: v[0] normal, v[1] spread, v[2] wide (n == 0 if absent)
+// the plan variants of one length: v[0] normal, v[1] spread, v[2] wide, v[3] split radix-9
+// (n == 0 if absent)
 struct PlanSet {
-  FftPlan v[3] = {};
+  FftPlan v[4] = {};
 };
 Status plan_set(int n, PlanSet* out);
 // spread while the launch's CTAs are all resident at once (latency-bound small grids), else

@@ -102,10 +102,10 @@ struct RowFwdArgs {
 };
 
 // FFT kernels: WIDE instantiations run 64-register threads (fft_kmax_wide butterflies each)
-#define RK_FFT_BOUNDS(WIDE) __launch_bounds__((WIDE) ? kFftWideThreads : 512, 1)
+#define RK_FFT_BOUNDS(FM) __launch_bounds__((FM) == 1 ? kFftWideThreads : (FM) == 2 ? kFftSplitThreads : 512, 1)
 
-template <int SRC, bool TWS, bool WIDE>
-__global__ void RK_FFT_BOUNDS(WIDE) row_fwd_kernel(const RowFwdArgs a) {
+template <int SRC, bool TWS, int FM>   // FM: FFT mode of fft_line (0 normal / spread, 1 WIDE, 2 split)
+__global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -237,7 +237,7 @@ __global__ void RK_FFT_BOUNDS(WIDE) row_fwd_kernel(const RowFwdArgs a) {
   }
   __syncthreads();
   RK_PHASE(0, 2);
-  fft_line<false, TWS, WIDE>(buf, pls, tl);
+  fft_line<false, TWS, FM>(buf, pls, tl);
   RK_PHASE(0, 3);
   pdl_trigger();   // the column pass may start staging while the split rows are stored
   // split Z = FFT(u + i v) into U = (Z + conj Z[-k]) / 2, V = (Z - conj Z[-k]) / 2i
@@ -278,8 +278,8 @@ struct ColArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
-template <int MODE, bool TWS, bool WIDE>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
-__global__ void RK_FFT_BOUNDS(WIDE) col_kernel(const ColArgs a) {
+template <int MODE, bool TWS, int FM>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
+__global__ void RK_FFT_BOUNDS(FM) col_kernel(const ColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -320,13 +320,13 @@ __global__ void RK_FFT_BOUNDS(WIDE) col_kernel(const ColArgs a) {
   mbar_wait(bar, 0);
   __syncthreads();
   RK_PHASE(1, 1);
-  fft_line<false, TWS, WIDE>(buf, pls, tl);
+  fft_line<false, TWS, FM>(buf, pls, tl);
   RK_PHASE(1, 2);
   if (MODE == 0) {
     const double* S = specs + (size_t)line * a.ldq;
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     __syncthreads();
-    fft_line<true, TWS, WIDE>(buf, pls, tl);
+    fft_line<true, TWS, FM>(buf, pls, tl);
     RK_PHASE(1, 3);
     pdl_trigger();
     // TMA bulk store of the kept rows
@@ -373,8 +373,8 @@ struct RowInvArgs {
   int xg_bulk;               // X_g is 16-byte aligned: one TMA bulk copy per CTA
 };
 
-template <bool TWS, bool WIDE>
-__global__ void RK_FFT_BOUNDS(WIDE) row_inv_kernel(const RowInvArgs a) {
+template <bool TWS, int FM>
+__global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -456,7 +456,7 @@ __global__ void RK_FFT_BOUNDS(WIDE) row_inv_kernel(const RowInvArgs a) {
   __syncthreads();
   RK_PHASE(2, 2);
   double2* buf = smem + (size_t)line * n;
-  fft_line<true, TWS, WIDE>(buf, pls, tl);
+  fft_line<true, TWS, FM>(buf, pls, tl);
   if (xwait) mbar_wait(bar, 0);   // init is ordered by the barrier above
   RK_PHASE(2, 3);
   const int ya = 2 * (blockIdx.x * a.lpc + line);
@@ -495,7 +495,7 @@ static constexpr size_t kSmemMax = 227 * 1024;
 static inline bool tw_fits(size_t bytes_before, const FftPlan& pl) { return with_tw(bytes_before, pl) <= kSmemMax; }
 // WIDE kernels are only instantiated with the table in smem (wide plans exist for n <= 4608)
 static inline Status wide_needs_tws(const FftPlan& pl, bool tws) {
-  if (pl.wide == 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+  if (pl.wide >= 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
   return Status::ok();
 }
 
@@ -514,12 +514,15 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStrea
   const bool tws = tw_fits(smem, a.pl);
   if (tws) smem = with_tw(smem, a.pl);
   RK_TRY(wide_needs_tws(a.pl, tws));
-  auto kern = a.pl.wide == 2 ? (src == SRC_ROWS ? row_fwd_kernel<SRC_ROWS, true, true>
-                           : src == SRC_LAG ? row_fwd_kernel<SRC_LAG, true, true>
-                                            : row_fwd_kernel<SRC_SPARSE, true, true>)
-              : src == SRC_ROWS ? (tws ? row_fwd_kernel<SRC_ROWS, true, false> : row_fwd_kernel<SRC_ROWS, false, false>)
-              : src == SRC_LAG  ? (tws ? row_fwd_kernel<SRC_LAG, true, false> : row_fwd_kernel<SRC_LAG, false, false>)
-                                : (tws ? row_fwd_kernel<SRC_SPARSE, true, false> : row_fwd_kernel<SRC_SPARSE, false, false>);
+  auto kern = a.pl.wide == 2 ? (src == SRC_ROWS ? row_fwd_kernel<SRC_ROWS, true, 1>
+                                : src == SRC_LAG ? row_fwd_kernel<SRC_LAG, true, 1>
+                                                 : row_fwd_kernel<SRC_SPARSE, true, 1>)
+              : a.pl.wide == 3 ? (src == SRC_ROWS ? row_fwd_kernel<SRC_ROWS, true, 2>
+                                  : src == SRC_LAG ? row_fwd_kernel<SRC_LAG, true, 2>
+                                                   : row_fwd_kernel<SRC_SPARSE, true, 2>)
+              : src == SRC_ROWS ? (tws ? row_fwd_kernel<SRC_ROWS, true, 0> : row_fwd_kernel<SRC_ROWS, false, 0>)
+              : src == SRC_LAG  ? (tws ? row_fwd_kernel<SRC_LAG, true, 0> : row_fwd_kernel<SRC_LAG, false, 0>)
+                                : (tws ? row_fwd_kernel<SRC_SPARSE, true, 0> : row_fwd_kernel<SRC_SPARSE, false, 0>);
   RK_TRY(set_smem_attr((const void*)kern, smem));
   RK_CUDA_TRY(launch_pdl(kern, grid, dim3(threads), smem, st, a));
   count_launch();
@@ -537,9 +540,10 @@ static Status launch_col(int mode, const ColArgs& a0, int batch, cudaStream_t st
   const bool tws = tw_fits(smem, a.pl);
   if (tws) smem = with_tw(smem, a.pl);
   RK_TRY(wide_needs_tws(a.pl, tws));
-  auto kern = a.pl.wide == 2 ? (mode == 0 ? col_kernel<0, true, true> : col_kernel<1, true, true>)
-              : mode == 0 ? (tws ? col_kernel<0, true, false> : col_kernel<0, false, false>)
-                          : (tws ? col_kernel<1, true, false> : col_kernel<1, false, false>);
+  auto kern = a.pl.wide == 2 ? (mode == 0 ? col_kernel<0, true, 1> : col_kernel<1, true, 1>)
+              : a.pl.wide == 3 ? (mode == 0 ? col_kernel<0, true, 2> : col_kernel<1, true, 2>)
+              : mode == 0 ? (tws ? col_kernel<0, true, 0> : col_kernel<0, false, 0>)
+                          : (tws ? col_kernel<1, true, 0> : col_kernel<1, false, 0>);
   RK_TRY(set_smem_attr((const void*)kern, smem));
   RK_CUDA_TRY(launch_pdl(kern, grid, dim3(threads), smem, st, a));
   count_launch();
@@ -564,7 +568,9 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
   const bool tws = tw_fits(smem, a.pl);
   if (tws) smem = with_tw(smem, a.pl);
   RK_TRY(wide_needs_tws(a.pl, tws));
-  auto kern = a.pl.wide == 2 ? row_inv_kernel<true, true> : tws ? row_inv_kernel<true, false> : row_inv_kernel<false, false>;
+  auto kern = a.pl.wide == 2 ? row_inv_kernel<true, 1>
+              : a.pl.wide == 3 ? row_inv_kernel<true, 2>
+              : tws ? row_inv_kernel<true, 0> : row_inv_kernel<false, 0>;
   RK_TRY(set_smem_attr((const void*)kern, smem));
   RK_CUDA_TRY(launch_pdl(kern, grid, dim3(a.lpc * a.pl.nthr), smem, st, a));
   count_launch();

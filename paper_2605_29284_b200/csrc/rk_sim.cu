@@ -90,8 +90,8 @@ struct CsColArgs {
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
-template <bool TWS, bool WIDE>
-__global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_col_kernel(const CsColArgs a) {
+template <bool TWS, int FM>
+__global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSplitThreads : 512, 1) cs_col_kernel(const CsColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_col_kernel
     buf[y] = make_double2(0.5 * ((A.x + Am.x) - (B.y - Bm.y)), 0.5 * ((A.y - Am.y) + (B.x + Bm.x)));
   }
   __syncthreads();
-  fft_line<true, TWS, WIDE>(buf, pls, tl);
+  fft_line<true, TWS, FM>(buf, pls, tl);
   double* g = a.g + (int64_t)b * a.g_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, y = idx / a.lpc;
@@ -392,8 +392,8 @@ struct CsFftArgs {
   int tw_off;
 };
 
-template <bool TWS, bool WIDE>
-__global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_rowfft_kernel(const CsFftArgs a) {
+template <bool TWS, int FM>
+__global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSplitThreads : 512, 1) cs_rowfft_kernel(const CsFftArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_rowfft_ker
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
-  fft_line<true, TWS, WIDE>(buf, pls, tl);
+  fft_line<true, TWS, FM>(buf, pls, tl);
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, ix = idx / a.lpc;
@@ -469,8 +469,8 @@ __device__ __forceinline__ void philox_words4(uint64_t w, uint64_t fs, uint64_t 
   }
 }
 
-template <bool TWS, bool WIDE>
-__global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_rowgen_kernel(const CsGenArgs a) {
+template <bool TWS, int FM>
+__global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSplitThreads : 512, 1) cs_rowgen_kernel(const CsGenArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(WIDE ? kFftWideThreads : 512, 1) cs_rowgen_ker
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  fft_line<true, TWS, WIDE>(buf, pls, tl);
+  fft_line<true, TWS, FM>(buf, pls, tl);
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, ix = idx / a.lpc;
@@ -582,9 +582,9 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     size_t smem = sizeof(double2) * ((size_t)ga.tw_off + ga.pl.ntw);
     const bool tws = smem <= 227 * 1024;
     if (!tws) smem = sizeof(double2) * (size_t)ga.tw_off;
-    if (ga.pl.wide == 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
-    auto kern = ga.pl.wide == 2 ? cs_rowgen_kernel<true, true> : tws ? cs_rowgen_kernel<true, false>
-                                                                     : cs_rowgen_kernel<false, false>;
+    if (ga.pl.wide >= 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+    auto kern = ga.pl.wide == 2 ? cs_rowgen_kernel<true, 1> : ga.pl.wide == 3 ? cs_rowgen_kernel<true, 2>
+                : tws ? cs_rowgen_kernel<true, 0> : cs_rowgen_kernel<false, 0>;
     RK_TRY(set_smem_attr((const void*)kern, smem));
     const dim3 grid((unsigned)ceil_div(e.ps2, ga.lpc), (unsigned)batch);
     kern<<<grid, ga.lpc * ga.pl.nthr, smem, st>>>(ga);
@@ -624,8 +624,9 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     size_t smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1 + fa.pl.ntw);
     const bool tws = smem <= 227 * 1024;   // else twiddles are read through L1/L2
     if (!tws) smem = sizeof(double2) * (e.ps1 * (size_t)fa.lpc + 1);
-    if (fa.pl.wide == 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
-    auto kern = fa.pl.wide == 2 ? cs_rowfft_kernel<true, true> : tws ? cs_rowfft_kernel<true, false> : cs_rowfft_kernel<false, false>;
+    if (fa.pl.wide >= 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+    auto kern = fa.pl.wide == 2 ? cs_rowfft_kernel<true, 1> : fa.pl.wide == 3 ? cs_rowfft_kernel<true, 2>
+                : tws ? cs_rowfft_kernel<true, 0> : cs_rowfft_kernel<false, 0>;
     RK_TRY(set_smem_attr((const void*)kern, smem));
     RK_CUDA_TRY(launch_pdl(kern, grid, dim3(fa.lpc * fa.pl.nthr), smem, st, fa));
     count_launch();
@@ -648,8 +649,9 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     size_t smem = sizeof(double2) * (e.ps2 * (size_t)ca.lpc + ca.pl.ntw);
     const bool tws = smem <= 227 * 1024;
     if (!tws) smem = sizeof(double2) * e.ps2 * (size_t)ca.lpc;
-    if (ca.pl.wide == 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
-    auto kern = ca.pl.wide == 2 ? cs_col_kernel<true, true> : tws ? cs_col_kernel<true, false> : cs_col_kernel<false, false>;
+    if (ca.pl.wide >= 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+    auto kern = ca.pl.wide == 2 ? cs_col_kernel<true, 1> : ca.pl.wide == 3 ? cs_col_kernel<true, 2>
+                : tws ? cs_col_kernel<true, 0> : cs_col_kernel<false, 0>;
     RK_TRY(set_smem_attr((const void*)kern, smem));
     RK_CUDA_TRY(launch_pdl(kern, grid, dim3(ca.lpc * ca.pl.nthr), smem, st, ca));
     count_launch();
