@@ -103,7 +103,9 @@ const FftPlan& plan_pick(const PlanSet& ps, int64_t lines) {
     const int by_smem = (int)((227 * 1024) / (lpc * line_bytes + line_bytes / 8 + 64));
     return by_regs > 0 && ceil_div(lines, lpc) <= 148LL * std::min(by_regs, by_smem);
   };
-  if (one_wave(sl)) return sl;
+  // split only while the launch has at most one line per SM: measured on cfg2 (178 row pairs)
+  // the split rows were neutral back to back and ~2 us slower with a cold L2
+  if (sl.n && lines <= 148 && one_wave(sl)) return sl;
   if (one_wave(sp)) return sp;
   return wd.n ? wd : ps.v[0];
 }

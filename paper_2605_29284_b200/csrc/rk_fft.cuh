@@ -330,7 +330,7 @@ __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int 
 // spread plans, 1 WIDE (64-register kernels), 2 split radix-9 stages.
 template <bool INV, bool TWS = false, int FM = 0>
 __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t) {
-  constexpr bool WIDE = FM == 1;
+  constexpr bool WIDE = FM >= 1;   // split plans also keep the small register footprint elsewhere
   const int n = pl.n, nthr = pl.nthr;
   const double2* tw = pl.tw;   // stage 1 (Ns = 1) needs no twiddles and has no block
   int Ns = 1;
@@ -422,10 +422,13 @@ inline bool fft_factor(int n, FftPlan* pl, int wide = 0) {
     int mx = 1;
     for (int i = 0; i < pl->nstages; ++i) mx = mx > n / rad[i] ? mx : n / rad[i];
     need = need > (mx < 512 ? mx : 512) ? need : (mx < 512 ? mx : 512);
-  } else if (wide == 3) {   // split radix-9 stages: 3 lanes per butterfly, 10 per warp
-    if (pl->n9 > 0) {
-      const int w9 = ((n / 9) + 9) / 10 * 32;
-      need = need > w9 ? need : w9;
+  } else if (wide == 3) {   // split radix-9 stages: 3 lanes per butterfly, 10 per warp;
+    need = 1;               // the other radices as in the WIDE kernels
+    for (int i = 0; i < pl->nstages; ++i) {
+      const int nb = n / rad[i];
+      const int k = rad[i] == 9 ? 0 : fft_kmax_wide(rad[i]);
+      const int th = k ? (nb + k - 1) / k : (nb + 9) / 10 * 32;
+      need = need > th ? need : th;
     }
   } else if (wide == 2) {   // fft_kmax_wide butterflies per thread, up to 1024 threads per line
     need = 1;
