@@ -226,6 +226,48 @@ def profile_passes(pk, case, reps, flush):
     return acc / reps, np.array(list(b))
 
 
+def cufft_reference(pk, case, reps, flush):
+    """Reference point only (north_star): the same convolution + crop + fixed part done with
+    cuFFT (torch.fft rfft2 / irfft2, fp64) on c* from our own scatter, L2 flushed before each
+    rep; returns (ms median, max rel diff vs our predict).  Not part of any reported value."""
+    import torch
+    st = case["setup"]
+    g = st.grid
+    cd = torch.as_tensor(case["cs"][0], device="cuda")
+    bd = torch.as_tensor(case["beta"], device="cuda")
+    xd = None if case["xg"] is None else torch.as_tensor(case["xg"], device="cuda").contiguous()
+    p1, p2 = st.embed_dims
+    M1, M2 = g.total_dims
+    m1, m2 = g.interior_dims
+    l, _, b, _ = g.pad
+    spec = torch.as_tensor(np.ascontiguousarray(np.asarray(st.filter_spectrum).real[:, : p1 // 2 + 1]),
+                           device="cuda")
+    cstar = st.coefficients_to_grid(cd)
+    xpad = torch.zeros((p2, p1), dtype=torch.float64, device="cuda")
+
+    def conv():
+        xpad[:M2, :M1].copy_(cstar)
+        y = torch.fft.irfft2(torch.fft.rfft2(xpad) * spec, s=(p2, p1))
+        f = y[b:b + m2, l:l + m1]
+        if xd is not None:
+            return f + (xd @ bd).reshape(m2, m1)
+        return f + bd[0]
+
+    for _ in range(3):
+        conv()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for k in range(reps):
+        flush()
+        ev[k][0].record()
+        conv()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    ours = pk.predict_rapid(st, cd, bd, xd)
+    ref = conv()
+    diff = float((ours - ref).abs().max() / ref.abs().max())
+    return statistics.median(a.elapsed_time(b) for a, b in ev), diff
+
+
 def fft_flops(n):
     """Real fp64 flops of one complex length-n transform in our radix-9/6/8/4/2 schedule."""
     per_pt = {9: 16.0, 6: 12.7, 8: 10.5, 4: 8.5, 3: 12.0, 2: 6.0}   # codelet + twiddle flops per point
@@ -482,6 +524,7 @@ def main():
     N = wl.dims[0] * wl.dims[1]
     value = N * args.steps * world / (tot_ms * 1e-3)
     pass_ms, pass_bytes = profile_passes(pk, case, 10, flush)
+    cu_ms, cu_diff = cufft_reference(pk, case, 20, flush)
     e2e_ms, h2d, d2h = time_predict_e2e(pk, case, max(args.steps, 200), args.warmup, flush)   # host-timed: more samples
     e2e_tot = max_over_ranks(sum(e2e_ms), world)
     line = {
@@ -497,6 +540,10 @@ def main():
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind, "cfg2"),
         "gpu_launches": int(launches),
+        "cufft_reference": {"ms": round(cu_ms, 5), "ours_ms": round(statistics.median(ms), 5),
+                            "max_rel_diff": cu_diff,
+                            "what": "reference point only: c* (ours, precomputed) -> torch.fft rfft2 x spectrum -> "
+                                    "irfft2 -> crop + fixed part, fp64 cuFFT, L2 flushed; ours_ms includes the scatter"},
         "clocks": {**clk.summary(), "window": "0.5 s soak of the same flushed predicts + the timed steps"},
     }
     if rank == 0:
@@ -517,12 +564,14 @@ def main():
         ms3, l3, _ = time_predict_device(pk, case3, max(5, args.steps // 5), 3, flush)
         t3 = max_over_ranks(sum(ms3), world)
         pm3, pb3 = profile_passes(pk, case3, 5, flush)
+        cu3_ms, cu3_diff = cufft_reference(pk, case3, 5, flush)
         N3 = wl3.dims[0] * wl3.dims[1]
         extra["predict_cfg3"] = {
             "metric": "predicted grid points/s (fp64)", "value": round(N3 * len(ms3) * world / (t3 * 1e-3), 1),
             "unit": "points/s", "ms_per_predict": round(t3 / len(ms3), 4),
             "config": {"workload": "cfg3: n=20000, 2048x2048, L=4, nu=2.5", "embed": list(case3["setup"].embed_dims)},
             "roofline": roofline_obj(case3, pm3, pb3, peaks, peaks_kind, "cfg3"), "setup_s": round(case3["t_setup"], 3),
+            "cufft_reference": {"ms": round(cu3_ms, 4), "max_rel_diff": cu3_diff},
             "fit_s": round(case3["t_fit"], 3)}
         del case3
         torch.cuda.empty_cache()

@@ -349,6 +349,128 @@ __global__ void __launch_bounds__(256) weights_kernel(WArgs a) {
   }
 }
 
+// Same computation with the neighbour order a compile-time constant (L <= 4, M <= 64): the
+// substitutions are fully unrolled, the factor's reciprocal diagonal replaces the division in
+// each step, and for M <= 16 one warp serves 32 / M observations (shuffles of width M).  A
+// step of the serial chain is then shuffle -> multiply -> FMA (~40 cycles), where the
+// generic kernel pays a division, runtime index arithmetic and the loop bounds.
+template <int L>
+__global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
+  constexpr int BS = 2 * L, M = BS * BS;
+  constexpr int LPO = M <= 4 ? 4 : M <= 16 ? 16 : 32;   // lanes per observation
+  constexpr int G = 32 / LPO;                            // observations per warp
+  constexpr int MPL = (M + 31) / 32;
+  extern __shared__ double wsm[];
+  double* Lc = wsm;                // Lc[c * M + r] = L[r][c]   (forward: column c)
+  double* Lr = wsm + M * M;        // Lr[c * M + r] = L[c][r]   (backward: row c)
+  double* rd = wsm + 2 * M * M;    // 1 / L[c][c]
+  for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
+    const int r = e / M, c = e % M;
+    const double v = a.chol[e];
+    Lr[e] = v;
+    Lc[c * M + r] = v;
+  }
+  for (int c = threadIdx.x; c < M; c += blockDim.x) rd[c] = 1.0 / a.chol[c * M + c];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPO, sl = lane - sub * LPO;
+  const int warp = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  const int64_t nw = (a.n + G - 1) / G;
+  for (int64_t wi = (int64_t)blockIdx.x * wpb + warp; wi < nw; wi += (int64_t)gridDim.x * wpb) {
+    const int64_t i = wi * G + sub;
+    bool live = i < a.n;
+    const double x = live ? a.obs[2 * i] : a.px0, y = live ? a.obs[2 * i + 1] : a.py0;
+    const double tx = __ddiv_rn(__dsub_rn(x, a.px0), a.hx);
+    const double ty = __ddiv_rn(__dsub_rn(y, a.py0), a.hy);
+    int cx = 0, cy = 0;
+    if (live && !(tx >= -1.0e-9 && tx <= a.hix && ty >= -1.0e-9 && ty <= a.hiy)) {
+      if (sl == 0) atomicMin(&a.err[0], (int)i);
+      live = false;
+    }
+    if (live) {
+      cx = snap_cell(tx);
+      cy = snap_cell(ty);
+      if (cx - (L - 1) < 0 || cy - (L - 1) < 0 || cx + L > a.M1 - 1 || cy + L > a.M2 - 1) {
+        if (sl == 0) atomicMin(&a.err[1], (int)i);
+        live = false;
+      }
+    }
+    const int xlo = cx - (L - 1), ylo = cy - (L - 1);
+    const double ox = __dsub_rn(tx, (double)cx), oy = __dsub_rn(ty, (double)cy);
+    const bool on_node = fabs(ox) <= 1.0e-9 && fabs(oy) <= 1.0e-9;
+    double k[MPL], v[MPL];
+    int bad = 0;
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) {
+      const int m = s * 32 + sl;
+      k[s] = 0.0;
+      if (live && m < M) {
+        const int r = m / BS, q = m % BS;
+        const double nx = __dadd_rn(a.px0, __dmul_rn((double)(xlo + q), a.hx));
+        const double ny = __dadd_rn(a.py0, __dmul_rn((double)(ylo + r), a.hy));
+        const double dist = hypot(__dsub_rn(nx, x), __dsub_rn(ny, y));
+        k[s] = matern_cov(a.P, dist, &bad);
+      }
+      v[s] = k[s];
+    }
+    if (bad) atomicOr(&a.err[2], 1);
+    // forward substitution L y = k, column oriented (y overwrites v)
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) {
+      constexpr int W = LPO;
+      const int ncc = s == MPL - 1 ? M - s * 32 : 32;
+#pragma unroll 8
+      for (int cc = 0; cc < ncc; ++cc) {
+        const int c = s * 32 + cc;
+        const double yc = __shfl_sync(0xffffffffu, v[s], cc, W) * rd[c];
+        if (sl == cc) v[s] = yc;
+#pragma unroll
+        for (int s2 = s; s2 < MPL; ++s2) {
+          const int r = s2 * 32 + sl;
+          if (r > c && r < M) v[s2] = fma(-Lc[c * M + r], yc, v[s2]);
+        }
+      }
+    }
+    // back substitution L' w = y
+#pragma unroll
+    for (int s = MPL - 1; s >= 0; --s) {
+      constexpr int W = LPO;
+      const int ncc = s == MPL - 1 ? M - s * 32 : 32;
+#pragma unroll 8
+      for (int cc = ncc - 1; cc >= 0; --cc) {
+        const int c = s * 32 + cc;
+        const double wc = __shfl_sync(0xffffffffu, v[s], cc, W) * rd[c];
+        if (sl == cc) v[s] = wc;
+#pragma unroll
+        for (int s2 = 0; s2 <= s; ++s2) {
+          const int r = s2 * 32 + sl;
+          if (r < c) v[s2] = fma(-Lr[c * M + r], wc, v[s2]);
+        }
+      }
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) part = fma(v[s], k[s], part);
+#pragma unroll
+    for (int o = LPO / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o, LPO);
+    if (!live) continue;
+    double cv = a.P.sigma2 - part;
+    constexpr int corner = (L - 1) * BS + (L - 1);
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) {
+      const int m = s * 32 + sl;
+      if (m < M) a.weights[i * M + m] = on_node ? (m == corner ? 1.0 : 0.0) : v[s];
+    }
+    if (on_node) cv = 0.0;
+    if (cv < 0.0 && cv > -1.0e-10 * a.P.sigma2) cv = 0.0;
+    if (sl == 0) {
+      a.cond_var[i] = cv;
+      a.base[i] = ylo * a.M1 + xlo;
+    }
+  }
+}
+
 // cell_start[b] = lower_bound(sorted keys, b) for b in [0, nb]
 __global__ void cell_start_kernel(const int32_t* __restrict__ keys, int64_t n, int32_t* cs,
                                   int64_t nb) {
@@ -723,7 +845,21 @@ static Status build_setup(const rk_model* model, const rk_grid* grid, int L, con
     kern<<<wblocks, 256, wsm>>>(wa);
     return Status::ok();
   };
-  if (mpl <= 1) {
+  static const bool generic = getenv("RK_WEIGHTS_GENERIC") && atoi(getenv("RK_WEIGHTS_GENERIC"));
+  if (L <= 4 && !generic) {
+    const size_t wsl = sizeof(double) * (2 * M * M + M);
+    const int G = M <= 4 ? 8 : M <= 16 ? 2 : 1;
+    const int wbl = (int)std::min<int64_t>(ceil_div(ceil_div(n, G), 8), 148 * 16);
+    auto launch_l = [&](auto kern) -> Status {
+      RK_TRY(set_smem_attr((const void*)kern, wsl));
+      kern<<<wbl, 256, wsl>>>(wa);
+      return Status::ok();
+    };
+    if (L == 1) RK_TRY(launch_l(weights_kernel_l<1>));
+    else if (L == 2) RK_TRY(launch_l(weights_kernel_l<2>));
+    else if (L == 3) RK_TRY(launch_l(weights_kernel_l<3>));
+    else RK_TRY(launch_l(weights_kernel_l<4>));
+  } else if (mpl <= 1) {
     RK_TRY(launch_w(weights_kernel<1>));
   } else if (mpl <= 2) {
     RK_TRY(launch_w(weights_kernel<2>));

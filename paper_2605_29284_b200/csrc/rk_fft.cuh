@@ -53,6 +53,33 @@ __device__ __forceinline__ FftPlan fft_twiddles_to_smem(const FftPlan& pl, doubl
   return p;
 }
 
+// The same copy split in two so a cold table read does not serialise with the kernel's
+// other global round trips: twiddles_prefetch issues the loads into registers (nothing waits
+// on them), twiddles_commit stores them (and any remainder) later; caller syncs after.
+struct TwPrefetch {
+  double2 v[2];
+};
+__device__ __forceinline__ TwPrefetch twiddles_prefetch(const FftPlan& pl) {
+  TwPrefetch r;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    r.v[k] = i < pl.ntw ? __ldg(&pl.tw[i]) : make_double2(0.0, 0.0);
+  }
+  return r;
+}
+__device__ __forceinline__ FftPlan twiddles_commit(const FftPlan& pl, const TwPrefetch& r, double2* dst) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < pl.ntw) dst[i] = r.v[k];
+  }
+  for (int i = threadIdx.x + 2 * blockDim.x; i < pl.ntw; i += blockDim.x) dst[i] = __ldg(&pl.tw[i]);
+  FftPlan p = pl;
+  p.tw = dst;
+  return p;
+}
+
 // butterflies each thread keeps in registers for a stage of radix R
 // WIDE kernels (__launch_bounds__(1024): 64 registers) hold one radix-8/9 butterfly or two
 // smaller ones per thread, so a line spreads over up to 1024 threads and an SM keeps 32

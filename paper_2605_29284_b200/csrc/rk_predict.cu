@@ -98,6 +98,8 @@ struct RowFwdArgs {
   SparseSrc sp;              // SRC_SPARSE: gather plan + coefficients
   int prod_off, prod_cap;    // SRC_SPARSE: smem offset (double2 units) / per-line size (doubles)
                              // of the staged products w * c of the line's row pair
+  int c_off, c_n;            // SRC_SPARSE, c_n > 0: the whole coefficient vector (c_n entries)
+                             // is bulk-copied to smem at offset c_off (double2 units) up front
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
@@ -117,7 +119,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
   const int yb = ya + 1;
   const bool va = ya < a.nrows, vb = yb < a.nrows;
   RK_PHASE(0, 0);
-  const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
+  const TwPrefetch twp = TWS ? twiddles_prefetch(a.pl) : TwPrefetch{};
   pdl_wait();   // everything below reads the predecessor's output
   if (SRC == SRC_ROWS) {
     const double* rin = a.rows + (int64_t)b * a.in_bstride;
@@ -180,6 +182,24 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
     double* __restrict__ prod = (double*)(smem + a.prod_off) + (size_t)line * 2 * a.prod_cap;
     int2* __restrict__ nrec = (int2*)(prod + a.prod_cap);
     const int pidx = blockIdx.x * a.lpc + line;
+    // the coefficients travel by one TMA bulk copy issued before the plan is read, so the
+    // per-contribution lookups c[j] hit shared memory: two dependent global round trips
+    // (pair record, plan entries) instead of three
+    const double* __restrict__ cl = cb;
+    uint64_t* cbar = nullptr;
+    if (a.c_n > 0) {
+      double* cs = (double*)(smem + a.c_off);
+      cbar = (uint64_t*)(cs + ((a.c_n + 1) & ~1));
+      if (threadIdx.x == 0) {
+        const uint32_t b16 = (uint32_t)(a.c_n * 8) & ~15u;
+        mbar_init(cbar, 1);
+        mbar_expect_tx(cbar, b16);
+        if (b16) bulk_g2s(cs, cb, b16, cbar);
+        if (a.c_n & 1) cs[a.c_n - 1] = __ldg(&cb[a.c_n - 1]);
+      }
+      cl = cs;
+      __syncthreads();   // barrier initialised before anyone waits on it
+    }
     int4 P0 = make_int4(0, 0, 0, 0), P1 = P0;
     if (va) {
       P0 = __ldg(&g.pair_info[pidx]);
@@ -189,6 +209,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
     const int nn = P1.x - n0, cnt = P1.z - e0;
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
     const int rowq = ya * g.M1;
+    bool cwait = cbar != nullptr;
     // one pass issues the contribution loads and the node-record loads together; only the
     // coefficient loads depend on them
     constexpr int U = 4;
@@ -204,9 +225,13 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
         nq[u] = i < nn ? __ldg(&g.node_q[n0 + i]) : 0;
         ne[u] = i < nn ? __ldg(&g.node_off[n0 + i + 1]) : 0;
       }
+      if (cwait) {   // first use: the bulk copy (init ordered by the barrier above) has landed
+        mbar_wait(cbar, 0);
+        cwait = false;
+      }
       double cv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) cv[u] = i0 + u * nthr < cnt ? __ldg(&cb[ci[u]]) : 0.0;
+      for (int u = 0; u < U; ++u) cv[u] = i0 + u * nthr < cnt ? cl[ci[u]] : 0.0;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i = i0 + u * nthr;
@@ -217,6 +242,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
         }
       }
     }
+    if (cwait) mbar_wait(cbar, 0);   // no contributions here: still retire the copy before exit
     __syncthreads();
     RK_PHASE(0, 1);
     double* bd = (double*)buf;
@@ -235,6 +261,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
       buf[x] = make_double2(u, v);
     }
   }
+  const FftPlan pls = TWS ? twiddles_commit(a.pl, twp, smem + a.tw_off) : a.pl;
   __syncthreads();
   RK_PHASE(0, 2);
   fft_line<false, TWS, FM>(buf, pls, tl);
@@ -384,7 +411,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
   const int H = n / 2 + 1;
   const double2* U = a.U + (int64_t)b * a.U_bstride;
   RK_PHASE(2, 0);
-  const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
+  const TwPrefetch twp = TWS ? twiddles_prefetch(a.pl) : TwPrefetch{};
   // prefetch the epilogue operands of the CTA's rows (covariates X_g: one contiguous block,
   // a TMA bulk copy; CS field g: strided rows, 8-byte async copies); they land while the U
   // rows are gathered and transformed
@@ -452,6 +479,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
     }
   }
   RK_PHASE(2, 1);
+  const FftPlan pls = TWS ? twiddles_commit(a.pl, twp, smem + a.tw_off) : a.pl;
   cp_async_wait_all();
   __syncthreads();
   RK_PHASE(2, 2);
@@ -492,6 +520,7 @@ static inline size_t with_tw(size_t bytes_before, const FftPlan& pl) {
 }
 // the table is staged in smem when it fits next to the lines (else read through L1/L2)
 static constexpr size_t kSmemMax = 227 * 1024;
+static constexpr size_t kCSmemMax = 16 * 1024;   // largest c (bytes) pass 1 stages in smem
 static inline bool tw_fits(size_t bytes_before, const FftPlan& pl) { return with_tw(bytes_before, pl) <= kSmemMax; }
 // WIDE kernels are only instantiated with the table in smem (wide plans exist for n <= 4608)
 static inline Status wide_needs_tws(const FftPlan& pl, bool tws) {
@@ -509,6 +538,15 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStrea
   if (src == SRC_SPARSE) {
     a.prod_off = tw_slot(smem);
     smem = (size_t)a.prod_off * 16 + sizeof(double) * (size_t)a.lpc * 2 * a.prod_cap;
+    if (a.c_n > 0) {   // whole c in smem only while it stays a small share of the CTA's budget
+      const bool aligned = (reinterpret_cast<uintptr_t>(a.sp.c) & 15) == 0 && (a.sp.c_stride * 8) % 16 == 0;
+      if (aligned && (size_t)a.c_n * 8 <= kCSmemMax) {
+        a.c_off = tw_slot(smem);
+        smem = (size_t)a.c_off * 16 + sizeof(double) * (size_t)((a.c_n + 1) & ~1) + 16;
+      } else {
+        a.c_n = 0;
+      }
+    }
   }
   a.tw_off = tw_slot(smem);
   const bool tws = tw_fits(smem, a.pl);
@@ -731,6 +769,8 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     ra.sp = *sp;
     ra.tma = 0;
     ra.prod_cap = (int)((s->max_pair_ent + 1) & ~int64_t(1));
+    static const bool c_smem = !(getenv("RK_C_SMEM") && atoi(getenv("RK_C_SMEM")) == 0);
+    ra.c_n = c_smem ? (int)s->n : 0;
   }
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[1], st));
   RK_TRY(launch_row_fwd(sp ? SRC_SPARSE : SRC_ROWS, ra, batch, st));
@@ -894,6 +934,8 @@ static Status predict_graphed(rk_setup* s, Workspace* w, const PredictBatch& pb,
     if (it != w->graphs.end()) exec = it->second;
     else capture = (++w->seen[key] >= 2) && w->graphs.size() < 64;
   }
+  static const bool use_graph = !(getenv("RK_DEV_GRAPH") && atoi(getenv("RK_DEV_GRAPH")) == 0);
+  if (!use_graph) return predict_batch(s, pb, st, nullptr, w);
   if (exec) {
     RK_CUDA_TRY(cudaGraphLaunch(exec, st));
     count_launch(kPredictKernels);
