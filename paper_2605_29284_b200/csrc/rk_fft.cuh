@@ -22,11 +22,14 @@
 // wide); threads whose butterfly index runs past n/R just idle.
 #pragma once
 
+#include <cstring>
+
 #include "rk_common.cuh"
 
 namespace rk {
 
 constexpr int FFT_MAX_STAGES = 16;
+constexpr int kFftMagicSlots = FFT_MAX_STAGES / 4;   // double2 entries holding the stage divisors
 
 // n = 9^n9 * r3 * 8^n8 * r2.  Kept as counts (not a radix array) so the stage
 // code is straight-line per radix with only small runtime arms: a switch over many
@@ -37,7 +40,9 @@ struct FftPlan {
   int nstages;
   int nthr;                    // threads cooperating on one line (multiple of 32)
   int n9, r3, n8, r2;          // r3 in {1,3,6}, r2 in {1,2,4,16}; 16 = two radix-4 stages
-  int ntw;                     // entries of the stage twiddle table (sum of Ns > 1)
+  int ntw;                     // entries of the stage twiddle table (sum of Ns > 1), plus
+                               // kFftMagicSlots trailing entries holding, per stage,
+                               // ceil(2^32 / Ns) as uint32 (j mod Ns by a multiply-high)
   int wide;                    // 0 normal; 1 spread (one butterfly per thread, <= 512 threads);
                                // 2 built for the WIDE kernels (fft_kmax_wide butterflies per thread);
                                // 3 split radix-9 stages (fft_stage9_split, three lanes each)
@@ -233,16 +238,24 @@ struct Dft<9, INV> {
 // bandwidth the engine is bound by for FP64 work it has spare.  The whole table has
 // sum(Ns) entries (~n / R_last), small enough to stage in shared memory per CTA
 // (fft_twiddles_to_smem); warp loads are contiguous.  TWS: table in shared memory.
+// j mod Ns for 0 <= j < 2^16 and 1 < Ns < 2^16 with m = ceil(2^32 / Ns): exact (the rounding
+// error of m contributes < j / 2^32 < 1 / Ns to the quotient)
+// (m == 0: plain modulo -- the CS row generator keeps it: measured, in that 64-register kernel
+// the divisor table pointer and stage index cost spills)
+__device__ __forceinline__ int mod_magic(int j, int Ns, uint32_t m) {
+  return Ns == 1 ? 0 : m == 0 ? j % Ns : j - Ns * (int)__umulhi((uint32_t)j, m);
+}
+
 template <int R, bool INV, bool TWS = false, bool WIDE = false>
 __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
-                                          const double2* __restrict__ tw) {
+                                          const double2* __restrict__ tw, uint32_t nsm) {
   constexpr int K = WIDE ? fft_kmax_wide(R) : fft_kmax(R);
   const int nb = n / R;
   double2 a[K][R];
   int outb[K];
   // j mod Ns for j = t + q nthr, updated incrementally (one division per stage, not per butterfly)
-  int jm = t % Ns;
-  const int jstep = nthr % Ns;
+  int jm = mod_magic(t, Ns, nsm);
+  const int jstep = mod_magic(nthr, Ns, nsm);
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     const int j = t + q * nthr;
@@ -288,7 +301,7 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
 // is what a radix-9 stage of a latency-bound line waits on.
 template <bool INV, bool TWS>
 __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int n, int Ns, int t,
-                                                 const double2* __restrict__ tw) {
+                                                 const double2* __restrict__ tw, uint32_t nsm) {
   const double C1 = 7.66044443118978013452e-01, S1 = 6.42787609686539362919e-01;
   const double C2 = 1.73648177666930358942e-01, S2 = 9.84807753012208020316e-01;
   const double C4 = -9.39692620785908427905e-01, S4 = 3.42020143325668712908e-01;
@@ -298,7 +311,7 @@ __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int 
   const int sub = lane / 3, r = lane - 3 * sub;
   const int j = (t >> 5) * 10 + sub;
   const bool valid = lane < 30 && j < nb;
-  const int jm = valid ? j % Ns : 0;
+  const int jm = valid ? mod_magic(j, Ns, nsm) : 0;
   double2 c0 = make_double2(0.0, 0.0), c1 = c0, c2 = c0;
   if (valid) {
     double2 a0 = buf[j + r * nb], a1 = buf[j + (r + 3) * nb], a2 = buf[j + (r + 6) * nb];
@@ -355,42 +368,48 @@ __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int 
 // Full transform of the line at `buf` by thread t (0 <= t < pl.nthr or idle beyond).
 // Must be called by every thread of the CTA (contains barriers).  FM (FFT mode): 0 normal /
 // spread plans, 1 WIDE (64-register kernels), 2 split radix-9 stages.
-template <bool INV, bool TWS = false, int FM = 0>
+template <bool INV, bool TWS = false, int FM = 0, bool MAG = true>   // MAG: magic-divisor modulo
 __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t) {
   constexpr bool WIDE = FM >= 1;   // split plans also keep the small register footprint elsewhere
   const int n = pl.n, nthr = pl.nthr;
   const double2* tw = pl.tw;   // stage 1 (Ns = 1) needs no twiddles and has no block
-  int Ns = 1;
+  const uint32_t* mg = reinterpret_cast<const uint32_t*>(pl.tw + pl.ntw - kFftMagicSlots);
+  int Ns = 1, si = 0;   // si: stage index (magic divisors)
 #pragma unroll 1
   for (int s = 0; s < pl.n9; ++s) {
-    if (FM == 2) fft_stage9_split<INV, TWS>(buf, n, Ns, t, tw);
-    else fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
+    if (FM == 2) fft_stage9_split<INV, TWS>(buf, n, Ns, t, tw, MAG ? mg[si] : 0u);
+    else fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
     if (Ns > 1) tw += Ns;
     Ns *= 9;
+    ++si;
   }
   if (pl.r3 == 6) {
-    fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
+    fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
     if (Ns > 1) tw += Ns;
     Ns *= 6;
+    ++si;
   } else if (pl.r3 == 3) {
-    fft_stage<3, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
+    fft_stage<3, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
     if (Ns > 1) tw += Ns;
     Ns *= 3;
+    ++si;
   }
 #pragma unroll 1
   for (int s = 0; s < pl.n8; ++s) {
-    fft_stage<8, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
+    fft_stage<8, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
     if (Ns > 1) tw += Ns;
     Ns *= 8;
+    ++si;
   }
   if (pl.r2 == 2) {
-    fft_stage<2, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
+    fft_stage<2, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
   } else if (pl.r2 >= 4) {
 #pragma unroll 1
     for (int s = 0; s < (pl.r2 == 16 ? 2 : 1); ++s) {
-      fft_stage<4, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw);
+      fft_stage<4, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
       if (Ns > 1) tw += Ns;
       Ns *= 4;
+      ++si;
     }
   }
 }
@@ -487,6 +506,18 @@ inline void fft_stage_twiddles(const FftPlan& pl, Vec& out, Make make_c) {
       }
     }
     Ns *= R;
+  }
+  // trailing magic divisors: kFftMagicSlots entries = 4 * kFftMagicSlots uint32 (one per stage)
+  uint32_t mg[4 * kFftMagicSlots] = {};
+  Ns = 1;
+  for (int s = 0; s < ns; ++s) {
+    mg[s] = Ns > 1 ? (uint32_t)(((1ULL << 32) + (unsigned long long)Ns - 1) / (unsigned long long)Ns) : 0u;
+    Ns *= rad[s];
+  }
+  for (int k = 0; k < kFftMagicSlots; ++k) {
+    double v[2];
+    memcpy(v, mg + 4 * k, sizeof v);
+    out.push_back(make_c(v[0], v[1]));
   }
 }
 

@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSpli
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  fft_line<true, TWS, FM>(buf, pls, tl);
+  fft_line<true, TWS, FM, false>(buf, pls, tl);
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, ix = idx / a.lpc;
