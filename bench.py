@@ -268,6 +268,22 @@ def cufft_reference(pk, case, reps, flush):
     return statistics.median(a.elapsed_time(b) for a, b in ev), diff
 
 
+def weights_k1(case, peaks, reps=20):
+    """K1: the per-observation weights kernel on this setup, CUDA-event timed
+    (average of back-to-back launches), with its FP64 roofline: F_w = n (2 M^2 + 20 M)."""
+    import ctypes as C
+    from paper_2605_29284_b200 import _native as N
+    st = case["setup"]
+    ms = C.c_float(0.0)
+    N.call("rk_setup_time_weights", st.handle, N.stream_ptr(), reps, C.byref(ms))
+    n, M = st.n_obs, st.block_size
+    flops = n * (2 * M * M + 20 * M)
+    tf = flops / (ms.value * 1e-3) / 1e12
+    return {"ms": round(ms.value, 5), "n": n, "M": M, "flops": flops, "fp64_tflops": round(tf, 3),
+            "fp64_peak_tflops": FP64_TFLOPS_MEASURED, "fp64_frac": round(tf / FP64_TFLOPS_MEASURED, 4),
+            "what": "weights kernel alone (rapid.py:202-225), back-to-back launches; F_w = n(2M^2+20M)"}
+
+
 def fft_flops(n):
     """Real fp64 flops of one complex length-n transform in our radix-9/6/8/4/2 schedule."""
     per_pt = {9: 16.0, 6: 12.7, 8: 10.5, 4: 8.5, 3: 12.0, 2: 6.0}   # codelet + twiddle flops per point
@@ -524,8 +540,9 @@ def main():
     N = wl.dims[0] * wl.dims[1]
     value = N * args.steps * world / (tot_ms * 1e-3)
     pass_ms, pass_bytes = profile_passes(pk, case, 10, flush)
-    cu_ms, cu_diff = cufft_reference(pk, case, 20, flush)
     e2e_ms, h2d, d2h = time_predict_e2e(pk, case, max(args.steps, 200), args.warmup, flush)   # host-timed: more samples
+    cu_ms, cu_diff = cufft_reference(pk, case, 20, flush)
+    k1 = weights_k1(case, peaks)
     e2e_tot = max_over_ranks(sum(e2e_ms), world)
     line = {
         "metric": "predicted grid points/s (fp64)", "value": round(value, 1), "unit": "points/s",
@@ -540,6 +557,11 @@ def main():
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind, "cfg2"),
         "gpu_launches": int(launches),
+        "weights_k1": k1,
+        "predict_incl_weights": {
+            "value": round(N / ((tot_ms / args.steps + k1["ms"]) * 1e-3), 1), "unit": "points/s",
+            "ms": round(tot_ms / args.steps + k1["ms"], 5),
+            "what": "T_predict = K1 (weights kernel) + T_apply (the headline step), SURVEY 8(d)"},
         "cufft_reference": {"ms": round(cu_ms, 5), "ours_ms": round(statistics.median(ms), 5),
                             "max_rel_diff": cu_diff,
                             "what": "reference point only: c* (ours, precomputed) -> torch.fft rfft2 x spectrum -> "
@@ -565,6 +587,7 @@ def main():
         t3 = max_over_ranks(sum(ms3), world)
         pm3, pb3 = profile_passes(pk, case3, 5, flush)
         cu3_ms, cu3_diff = cufft_reference(pk, case3, 5, flush)
+        k13 = weights_k1(case3, peaks, reps=5)
         N3 = wl3.dims[0] * wl3.dims[1]
         extra["predict_cfg3"] = {
             "metric": "predicted grid points/s (fp64)", "value": round(N3 * len(ms3) * world / (t3 * 1e-3), 1),
@@ -572,6 +595,7 @@ def main():
             "config": {"workload": "cfg3: n=20000, 2048x2048, L=4, nu=2.5", "embed": list(case3["setup"].embed_dims)},
             "roofline": roofline_obj(case3, pm3, pb3, peaks, peaks_kind, "cfg3"), "setup_s": round(case3["t_setup"], 3),
             "cufft_reference": {"ms": round(cu3_ms, 4), "max_rel_diff": cu3_diff},
+            "weights_k1": k13,
             "fit_s": round(case3["t_fit"], 3)}
         del case3
         torch.cuda.empty_cache()

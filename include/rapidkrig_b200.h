@@ -128,6 +128,12 @@ rk_status rk_predict_dev(const rk_setup* s, const double* c_dev, const double* b
 rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta, int32_t p,
                           const double* xg, double* out, void* stream);
 
+/* Benchmark support: average CUDA-event duration (ms) of the per-observation weights
+ * kernel (rapid.py:202-225: stencil, Matern cross covariance, two substitutions against
+ * the K_N factor, cond_var) over `reps` back-to-back launches on this setup's
+ * observations, into scratch outputs (the setup is unchanged); synchronises the stream. */
+rk_status rk_setup_time_weights(const rk_setup* s, void* stream, int32_t reps, float* ms_out);
+
 /* predict_rapid with per-kernel CUDA-event timing on `stream` (benchmark support):
  * ms_out[0..3] = gather (c* = A'c), pass 1 (row FFT), pass 2 (column filter),
  * pass 3 (row IFFT + epilogue) durations in milliseconds; synchronises the stream. */

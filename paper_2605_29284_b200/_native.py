@@ -64,6 +64,7 @@ _PROTOS = {
     "rk_predict_host": (_i32, [_vp, _dp, _dp, _i32, _dp, _dp, _vp]),
     "rk_predict_profile": (_i32, [_vp, _dp, _dp, _i32, _dp, _dp, _vp, C.POINTER(C.c_float * 4)]),
     "rk_predict_traffic": (_i32, [_vp, _i32, C.POINTER(C.c_double * 4)]),
+    "rk_setup_time_weights": (_i32, [_vp, _vp, _i32, C.POINTER(C.c_float)]),
     "rk_fit_create": (_i32, [C.POINTER(RkModel), _dp, _i64, _dp, _dp, _i32, C.POINTER(_vp),
                              C.POINTER(_i32)]),
     "rk_fit_import": (_i32, [C.POINTER(RkModel), _dp, _i64, _dp, _i32, _dp, _dp, _dp,

@@ -759,6 +759,72 @@ static void free_setup(rk_setup* s) {
   delete s;
 }
 
+// weights + stencil base + cond_var for every observation of the setup (rapid.py:202-225);
+// also used by rk_setup_time_weights to time the kernel on its own
+static Status launch_weights(const rk_setup* s, int32_t* base, double* weights, double* cond_var, int* err,
+                             cudaStream_t st) {
+  const int64_t n = s->n;
+  const int L = s->L, M = s->M;
+  WArgs wa;
+  wa.P = s->mat;
+  wa.obs = s->obs;
+  wa.n = n;
+  wa.px0 = s->px0;
+  wa.py0 = s->py0;
+  wa.hx = s->grid.hx;
+  wa.hy = s->grid.hy;
+  wa.hix = (double)(s->M1 - 1) + 1.0e-9;
+  wa.hiy = (double)(s->M2 - 1) + 1.0e-9;
+  wa.L = L;
+  wa.bs = s->bs;
+  wa.M = M;
+  wa.M1 = s->M1;
+  wa.M2 = s->M2;
+  wa.chol = s->kn_chol_dev;
+  wa.base = base;
+  wa.weights = weights;
+  wa.cond_var = cond_var;
+  wa.err = err;
+  const size_t wsm = M <= 64 ? sizeof(double) * 2 * M * M : 0;
+  const int wblocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 16);
+  const int mpl = (M + 31) / 32;
+  auto launch_w = [&](auto kern) -> Status {
+    RK_TRY(set_smem_attr((const void*)kern, wsm));
+    kern<<<wblocks, 256, wsm, st>>>(wa);
+    return Status::ok();
+  };
+  static const bool generic = getenv("RK_WEIGHTS_GENERIC") && atoi(getenv("RK_WEIGHTS_GENERIC"));
+  if (L <= 4 && !generic) {
+    const size_t wsl = sizeof(double) * (2 * M * M + M);
+    const int G = M <= 4 ? 8 : M <= 16 ? 2 : 1;
+    const int wbl = (int)std::min<int64_t>(ceil_div(ceil_div(n, G), 8), 148 * 16);
+    auto launch_l = [&](auto kern) -> Status {
+      RK_TRY(set_smem_attr((const void*)kern, wsl));
+      kern<<<wbl, 256, wsl, st>>>(wa);
+      return Status::ok();
+    };
+    if (L == 1) RK_TRY(launch_l(weights_kernel_l<1>));
+    else if (L == 2) RK_TRY(launch_l(weights_kernel_l<2>));
+    else if (L == 3) RK_TRY(launch_l(weights_kernel_l<3>));
+    else RK_TRY(launch_l(weights_kernel_l<4>));
+  } else if (mpl <= 1) {
+    RK_TRY(launch_w(weights_kernel<1>));
+  } else if (mpl <= 2) {
+    RK_TRY(launch_w(weights_kernel<2>));
+  } else if (mpl <= 4) {
+    RK_TRY(launch_w(weights_kernel<4>));
+  } else if (mpl <= 8) {
+    RK_TRY(launch_w(weights_kernel<8>));
+  } else if (mpl <= 16) {
+    RK_TRY(launch_w(weights_kernel<16>));
+  } else {
+    RK_TRY(launch_w(weights_kernel<32>));
+  }
+  count_launch();
+  RK_LAUNCH_CHECK();
+  return Status::ok();
+}
+
 static Status build_setup(const rk_model* model, const rk_grid* grid, int L, const double* obs_host,
                           int64_t n, rk_setup** out, int32_t* ridge_applied, bool grid_only = false) {
   if (n <= 0 && !grid_only) return Status::err(RK_DOMAIN, "build_setup requires at least one observation");
@@ -817,63 +883,7 @@ static Status build_setup(const rk_model* model, const rk_grid* grid, int L, con
   int herr[4] = {INT_MAX, INT_MAX, 0, 0};
   RK_CUDA_TRY(cudaMemcpy(err, herr, sizeof(herr), cudaMemcpyHostToDevice));
 
-  WArgs wa;
-  wa.P = s->mat;
-  wa.obs = s->obs;
-  wa.n = n;
-  wa.px0 = s->px0;
-  wa.py0 = s->py0;
-  wa.hx = grid->hx;
-  wa.hy = grid->hy;
-  wa.hix = (double)(s->M1 - 1) + 1.0e-9;
-  wa.hiy = (double)(s->M2 - 1) + 1.0e-9;
-  wa.L = L;
-  wa.bs = s->bs;
-  wa.M = M;
-  wa.M1 = s->M1;
-  wa.M2 = s->M2;
-  wa.chol = s->kn_chol_dev;
-  wa.base = s->base;
-  wa.weights = s->weights;
-  wa.cond_var = s->cond_var;
-  wa.err = err;
-  const size_t wsm = M <= 64 ? sizeof(double) * 2 * M * M : 0;
-  const int wblocks = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 16);
-  const int mpl = (M + 31) / 32;
-  auto launch_w = [&](auto kern) -> Status {
-    RK_TRY(set_smem_attr((const void*)kern, wsm));
-    kern<<<wblocks, 256, wsm>>>(wa);
-    return Status::ok();
-  };
-  static const bool generic = getenv("RK_WEIGHTS_GENERIC") && atoi(getenv("RK_WEIGHTS_GENERIC"));
-  if (L <= 4 && !generic) {
-    const size_t wsl = sizeof(double) * (2 * M * M + M);
-    const int G = M <= 4 ? 8 : M <= 16 ? 2 : 1;
-    const int wbl = (int)std::min<int64_t>(ceil_div(ceil_div(n, G), 8), 148 * 16);
-    auto launch_l = [&](auto kern) -> Status {
-      RK_TRY(set_smem_attr((const void*)kern, wsl));
-      kern<<<wbl, 256, wsl>>>(wa);
-      return Status::ok();
-    };
-    if (L == 1) RK_TRY(launch_l(weights_kernel_l<1>));
-    else if (L == 2) RK_TRY(launch_l(weights_kernel_l<2>));
-    else if (L == 3) RK_TRY(launch_l(weights_kernel_l<3>));
-    else RK_TRY(launch_l(weights_kernel_l<4>));
-  } else if (mpl <= 1) {
-    RK_TRY(launch_w(weights_kernel<1>));
-  } else if (mpl <= 2) {
-    RK_TRY(launch_w(weights_kernel<2>));
-  } else if (mpl <= 4) {
-    RK_TRY(launch_w(weights_kernel<4>));
-  } else if (mpl <= 8) {
-    RK_TRY(launch_w(weights_kernel<8>));
-  } else if (mpl <= 16) {
-    RK_TRY(launch_w(weights_kernel<16>));
-  } else {
-    RK_TRY(launch_w(weights_kernel<32>));
-  }
-  count_launch();
-  RK_LAUNCH_CHECK();
+  RK_TRY(launch_weights(s, s->base, s->weights, s->cond_var, err, 0));
   RK_CUDA_TRY(cudaMemcpy(herr, err, sizeof(herr), cudaMemcpyDeviceToHost));
   cudaFree(err);
   if (herr[0] != INT_MAX) {
@@ -1073,6 +1083,42 @@ rk_status rk_setup_info(const rk_setup* s, int64_t* n_obs, int32_t* L, int32_t e
   if (embed) { embed[0] = s->p1; embed[1] = s->p2; }
   if (total) { total[0] = s->M1; total[1] = s->M2; }
   return RK_OK;
+}
+
+rk_status rk_setup_time_weights(const rk_setup* s, void* stream, int32_t reps, float* ms_out) {
+  auto run = [&]() -> Status {
+    if (!s || s->n <= 0 || reps < 1) return Status::err(RK_DOMAIN, "time_weights needs a setup with observations");
+    const cudaStream_t st = (cudaStream_t)stream;
+    int32_t* base = nullptr;
+    double *w = nullptr, *cv = nullptr;
+    int* err = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    RK_TRY(scratch_alloc((void**)&base, sizeof(int32_t) * s->n, st));
+    RK_TRY(scratch_alloc((void**)&w, sizeof(double) * s->n * s->M, st));
+    RK_TRY(scratch_alloc((void**)&cv, sizeof(double) * s->n, st));
+    RK_TRY(scratch_alloc((void**)&err, sizeof(int) * 4, st));
+    const int herr[4] = {INT_MAX, INT_MAX, 0, 0};
+    RK_CUDA_TRY(cudaMemcpyAsync(err, herr, sizeof(herr), cudaMemcpyHostToDevice, st));
+    RK_CUDA_TRY(cudaEventCreate(&e0));
+    RK_CUDA_TRY(cudaEventCreate(&e1));
+    RK_TRY(launch_weights(s, base, w, cv, err, st));   // warm-up
+    RK_CUDA_TRY(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; ++r) RK_TRY(launch_weights(s, base, w, cv, err, st));
+    RK_CUDA_TRY(cudaEventRecord(e1, st));
+    RK_CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    RK_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_out = ms / (float)reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    scratch_free(base, st);
+    scratch_free(w, st);
+    scratch_free(cv, st);
+    scratch_free(err, st);
+    RK_CUDA_TRY(cudaStreamSynchronize(st));
+    return Status::ok();
+  };
+  return (rk_status)finish(run());
 }
 
 rk_status rk_setup_copy_out(const rk_setup* s, int64_t* indices_host, double* weights_host,

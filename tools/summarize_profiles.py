@@ -93,6 +93,23 @@ def main(tag):
             wr = float(d["dram__bytes_write.sum"]) * SCALE[units[h.index("dram__bytes_write.sum")]]
             traffic["kernels"].setdefault(cfg, {})[name] = {"dram_bytes": rd + wr, "read": rd, "write": wr,
                                                              "ncu_us": float(d["gpu__time_duration.sum"])}
+    # optional captures: the weights kernel (K1) per config and the CS ensemble kernels
+    extra_metrics = FULL_METRICS + ["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+                                    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+                                    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
+    for label, fname in [("weights kernel (K1), cfg2", f"prof_weights_cfg2_{tag}.ncu-rep"),
+                         ("weights kernel (K1), cfg3", f"prof_weights_cfg3_{tag}.ncu-rep"),
+                         ("CS ensemble kernels, cfg4 (tools/cs_probe.py 64 32)", f"prof_cs_{tag}.ncu-rep")]:
+        rep = os.path.join(RAW, fname)
+        if not os.path.exists(rep):
+            continue
+        h, units, recs = ncu_raw(rep, extra_metrics)
+        out.append(f"== {label}: ncu --set full --clock-control none --import-source on ({fname})")
+        for d in recs:
+            out.append(f"  {d['Kernel Name'][:70]}")
+            for k, u in zip(h, units):
+                if "__" in k:
+                    out.append(f"     {k:90s} {d[k]} {u}")
     open(os.path.join(OUT, f"round1_ncu_full_{tag}_summary.txt"), "w").write("\n".join(out) + "\n")
     json.dump(traffic, open(os.path.join(OUT, "round1_traffic.json"), "w"), indent=1)
     print("\n".join(lines[:12]))
