@@ -147,3 +147,55 @@ def test_bad_inputs_raise_reference_exceptions(pk):
     with warnings.catch_warnings():
         warnings.simplefilter("error")
         pk.predict_rapid(st, f.c, f.beta_hat)   # no stray warnings on the hot path
+
+
+def test_weights_kernel_timing_leaves_setup_unchanged(pk):
+    import ctypes as C
+    from paper_2605_29284_b200 import _native as N
+    obs = _pts(300, 11)
+    model = pk.CovarianceModel(1.0, 8.0, 1.0)
+    st = pk.build_setup(model, pk.build_padded_grid(UNIT, (40, 40), 3, obs), 3, obs)
+    w0, cv0 = st.weights.copy(), st.cond_var.copy()
+    ms = C.c_float(0.0)
+    N.call("rk_setup_time_weights", st.handle, N.stream_ptr(), 3, C.byref(ms))
+    assert ms.value > 0.0
+    st._cache.clear()
+    assert np.array_equal(st.weights, w0) and np.array_equal(st.cond_var, cv0)
+
+
+_WEIGHTS_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2605_29284_b200 as pk
+obs = np.random.default_rng(12).uniform(0.05, 0.95, size=(257, 2))
+out = {}
+for L, nu in [(1, 0.5), (2, 1.5), (3, 1.0), (4, 2.5)]:
+    m = pk.CovarianceModel(1.0, 9.0, nu)
+    st = pk.build_setup(m, pk.build_padded_grid((0, 1, 0, 1), (48, 40), L, obs), L, obs)
+    out[f"w{L}"], out[f"c{L}"], out[f"i{L}"] = st.weights, st.cond_var, st.neighbor_indices
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_specialised_weights_kernel_matches_generic(pk, tmp_path):
+    """weights_kernel_l<L> (unrolled, reciprocal diagonal, 32/M observations per warp) against
+    the runtime-M kernel (RK_WEIGHTS_GENERIC=1, per-step division) for L = 1..4: identical
+    stencils; weights equal to the conditioning of K_N (the L = 4, nu = 2.5 factor is
+    ill-conditioned, so two correctly rounded substitutions differ at ~1e-11); conditional
+    variances (well conditioned) to 1e-12."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for gen in ("0", "1"):
+        f = tmp_path / f"w{gen}.npz"
+        env = dict(os.environ, RK_WEIGHTS_GENERIC=gen)
+        subprocess.run([sys.executable, "-c", _WEIGHTS_CHILD, root, str(f)], env=env, check=True)
+        res[gen] = np.load(f)
+    for L in range(1, 5):
+        a, b = res["0"], res["1"]
+        assert np.array_equal(a[f"i{L}"], b[f"i{L}"])
+        w_scale = np.abs(b[f"w{L}"]).max()
+        assert np.abs(a[f"w{L}"] - b[f"w{L}"]).max() <= (1e-12 if L < 4 else 1e-9) * w_scale, L
+        assert np.abs(a[f"c{L}"] - b[f"c{L}"]).max() <= 1e-12, L
