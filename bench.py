@@ -319,6 +319,16 @@ def _ncu_traffic(cfg, kernel):
         return None
 
 
+def _ncu_smem(cfg, kernel):
+    """Shared-memory data-pipe busy fraction of `kernel` (ncu wavefronts / (148 SMs x cycles))
+    from the committed capture, or None: the FFT passes stage every line in smem."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round1_traffic.json")) as f:
+            return json.load(f)["kernels"][cfg][kernel]["smem_busy_frac"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind, cfg=None):
     st = case["setup"]
     p1, p2 = st.embed_dims
@@ -338,6 +348,7 @@ def roofline_obj(case, pass_ms, pass_bytes, peaks, peaks_kind, cfg=None):
         "algorithmic_bytes": float(pass_bytes[dom]), "kernel_ms": round(float(pass_ms[dom]), 5),
         "fp64_tflops": round(fl, 3), "fp64_peak_tflops": FP64_TFLOPS_MEASURED,
         "fp64_frac": round(fl / FP64_TFLOPS_MEASURED, 4),
+        "smem_busy_frac": _ncu_smem(cfg, names[dom]),
         "passes": {names[i]: {"ms": round(float(pass_ms[i]), 5), "GB/s": round(pass_bytes[i] / (pass_ms[i] * 1e-3) / 1e9, 1),
                               "fp64_TF/s": round(flops[i] / (pass_ms[i] * 1e-3) / 1e12, 3)}
                    for i in range(4) if pass_bytes[i] > 0},   # the scatter is fused into pass 1

@@ -48,5 +48,7 @@ for mode in ["warm", "cold"]:
         rel = (v - t0) / 1000.0
         ph = " | ".join(f"{PHASES[nm][p - 1]} {np.median(rel[:, p] - rel[:, 0]):.2f}/{(rel[:, p] - rel[:, 0]).max():.2f}"
                         for p in range(1, 5))
+        if nm == "col" and (v[:, 5] > 0).all():
+            print(f"   col: spectrum multiply done at {np.median((v[:, 5] - v[:, 0]) / 1000.0):.2f} us (median)")
         print(f"{mode} {nm}: {len(v)} CTAs start {rel[:, 0].min():.2f}..{rel[:, 0].max():.2f} us; {ph}; "
               f"last end {rel[:, 4].max():.2f} us")

@@ -24,7 +24,7 @@ FULL_METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_w
                 "sm__warps_active.avg.pct_of_peak_sustained_active",
                 "smsp__issue_active.avg.pct_of_peak_sustained_active",
                 "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-                "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "sm__cycles_elapsed.avg", "smsp__inst_executed.sum",
                 "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
                 "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
                 "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
@@ -91,8 +91,13 @@ def main(tag):
                     out.append(f"     {k:90s} {d[k]} {u}")
             rd = float(d["dram__bytes_read.sum"]) * SCALE[units[h.index("dram__bytes_read.sum")]]
             wr = float(d["dram__bytes_write.sum"]) * SCALE[units[h.index("dram__bytes_write.sum")]]
+            # shared-memory data pipe: one 128-byte wavefront per SM cycle at most
+            wf = float(d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"])
+            cyc = float(d["sm__cycles_elapsed.avg"])
             traffic["kernels"].setdefault(cfg, {})[name] = {"dram_bytes": rd + wr, "read": rd, "write": wr,
-                                                             "ncu_us": float(d["gpu__time_duration.sum"])}
+                                                             "ncu_us": float(d["gpu__time_duration.sum"]),
+                                                             "smem_wavefronts": wf,
+                                                             "smem_busy_frac": round(wf / (148 * cyc), 4)}
     # optional captures: the weights kernel (K1) per config and the CS ensemble kernels
     extra_metrics = FULL_METRICS + ["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
                                     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
