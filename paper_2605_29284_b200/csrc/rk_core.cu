@@ -354,6 +354,8 @@ __global__ void __launch_bounds__(256) weights_kernel(WArgs a) {
 // each step, and for M <= 16 one warp serves 32 / M observations (shuffles of width M).  A
 // step of the serial chain is then shuffle -> multiply -> FMA (~40 cycles), where the
 // generic kernel pays a division, runtime index arithmetic and the loop bounds.
+__device__ __forceinline__ int cb0(int c0) { return c0 >> 2; }   // 4-column block of column c0
+
 template <int L>
 __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
   constexpr int BS = 2 * L, M = BS * BS;
@@ -361,23 +363,30 @@ __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
   constexpr int G = 32 / LPO;                            // observations per warp
   constexpr int MPL = (M + 31) / 32;
   extern __shared__ double wsm[];
-  double* Lc = wsm;                // Lc[c * M + r] = L[r][c]   (forward: column c)
-  double* Lr = wsm + M * M;        // Lr[c * M + r] = L[c][r]   (backward: row c)
+  // the factor in two 4-column-blocked layouts, so a lane's four entries of a block are one
+  // contiguous 32-byte read and a warp's reads are contiguous (no bank conflicts):
+  double* LF = wsm;                // LF[((c / 4) * M + r) * 4 + c % 4] = L[r][c]   (forward)
+  double* LB = wsm + M * M;        // LB[((c / 4) * M + r) * 4 + c % 4] = L[c][r]   (backward)
   double* rd = wsm + 2 * M * M;    // 1 / L[c][c]
   for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
     const int r = e / M, c = e % M;
     const double v = a.chol[e];
-    Lr[e] = v;
-    Lc[c * M + r] = v;
+    LF[((c >> 2) * M + r) * 4 + (c & 3)] = v;
+    LB[((r >> 2) * M + c) * 4 + (r & 3)] = v;
   }
   for (int c = threadIdx.x; c < M; c += blockDim.x) rd[c] = 1.0 / a.chol[c * M + c];
-  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPO, sl = lane - sub * LPO;
   const int warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
   const int64_t nw = (a.n + G - 1) / G;
-  for (int64_t wi = (int64_t)blockIdx.x * wpb + warp; wi < nw; wi += (int64_t)gridDim.x * wpb) {
+  // persistent CTAs (the factor is staged once per CTA); the trip count is the same for every
+  // warp so the staging barrier can sit after the first cross covariances (their latency
+  // overlaps the factor's loads)
+  const int64_t stride = (int64_t)gridDim.x * wpb;
+  const int64_t trips = (nw + stride - 1) / stride;
+  for (int64_t it = 0; it < trips; ++it) {
+    const int64_t wi = (int64_t)blockIdx.x * wpb + warp + it * stride;
     const int64_t i = wi * G + sub;
     bool live = i < a.n;
     const double x = live ? a.obs[2 * i] : a.px0, y = live ? a.obs[2 * i + 1] : a.py0;
@@ -415,37 +424,86 @@ __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
       v[s] = k[s];
     }
     if (bad) atomicOr(&a.err[2], 1);
-    // forward substitution L y = k, column oriented (y overwrites v)
+    if (it == 0) __syncthreads();   // factor staged
+    // forward substitution L y = k, column oriented (y overwrites v), four columns per step:
+    // every lane gathers the block's four entries (independent shuffles) and solves the 4 x 4
+    // diagonal block itself, then applies the four column updates to its rows with one 32-byte
+    // row read -- the same operations in the same order as one column at a time (bitwise
+    // identical), with a quarter of the dependent shuffle round trips
+    constexpr int W = LPO;
+    const int jm4 = sl & 3;
 #pragma unroll
     for (int s = 0; s < MPL; ++s) {
-      constexpr int W = LPO;
-      const int ncc = s == MPL - 1 ? M - s * 32 : 32;
-#pragma unroll 8
-      for (int cc = 0; cc < ncc; ++cc) {
-        const int c = s * 32 + cc;
-        const double yc = __shfl_sync(0xffffffffu, v[s], cc, W) * rd[c];
-        if (sl == cc) v[s] = yc;
+      const int ncc = s == MPL - 1 ? M - s * 32 : 32;   // a multiple of 4 (M = 4 L^2)
+#pragma unroll 2
+      for (int cb = 0; cb < ncc; cb += 4) {
+        const int c0 = s * 32 + cb;
+        double x0 = __shfl_sync(0xffffffffu, v[s], cb, W), x1 = __shfl_sync(0xffffffffu, v[s], cb + 1, W);
+        double x2 = __shfl_sync(0xffffffffu, v[s], cb + 2, W), x3 = __shfl_sync(0xffffffffu, v[s], cb + 3, W);
+        const double* B = LF + ((cb0(c0) * M + c0) * 4);   // B[4 i + j] = L[c0 + i][c0 + j]
+        const double y0 = x0 * rd[c0];
+        x1 = fma(-B[4], y0, x1);
+        const double y1 = x1 * rd[c0 + 1];
+        x2 = fma(-B[8], y0, x2);
+        x2 = fma(-B[9], y1, x2);
+        const double y2 = x2 * rd[c0 + 2];
+        x3 = fma(-B[12], y0, x3);
+        x3 = fma(-B[13], y1, x3);
+        x3 = fma(-B[14], y2, x3);
+        const double y3 = x3 * rd[c0 + 3];
+        {   // the lane's own entry: its position in the block is sl & 3 for every block
+          const double ym = jm4 == 0 ? y0 : jm4 == 1 ? y1 : jm4 == 2 ? y2 : y3;
+          if ((sl >> 2) == (cb >> 2)) v[s] = ym;
+        }
 #pragma unroll
         for (int s2 = s; s2 < MPL; ++s2) {
           const int r = s2 * 32 + sl;
-          if (r > c && r < M) v[s2] = fma(-Lc[c * M + r], yc, v[s2]);
+          if (r > c0 + 3 && r < M) {
+            const double2* q = reinterpret_cast<const double2*>(LF + (cb0(c0) * M + r) * 4);   // L[r][c0 .. c0 + 3]
+            const double2 a01 = q[0], a23 = q[1];
+            v[s2] = fma(-a01.x, y0, v[s2]);
+            v[s2] = fma(-a01.y, y1, v[s2]);
+            v[s2] = fma(-a23.x, y2, v[s2]);
+            v[s2] = fma(-a23.y, y3, v[s2]);
+          }
         }
       }
     }
-    // back substitution L' w = y
+    // back substitution L' w = y, four columns per step from the bottom
 #pragma unroll
     for (int s = MPL - 1; s >= 0; --s) {
-      constexpr int W = LPO;
       const int ncc = s == MPL - 1 ? M - s * 32 : 32;
-#pragma unroll 8
-      for (int cc = ncc - 1; cc >= 0; --cc) {
-        const int c = s * 32 + cc;
-        const double wc = __shfl_sync(0xffffffffu, v[s], cc, W) * rd[c];
-        if (sl == cc) v[s] = wc;
+#pragma unroll 2
+      for (int cb = ncc - 4; cb >= 0; cb -= 4) {
+        const int c0 = s * 32 + cb;
+        double x0 = __shfl_sync(0xffffffffu, v[s], cb, W), x1 = __shfl_sync(0xffffffffu, v[s], cb + 1, W);
+        double x2 = __shfl_sync(0xffffffffu, v[s], cb + 2, W), x3 = __shfl_sync(0xffffffffu, v[s], cb + 3, W);
+        const double* B = LF + ((cb0(c0) * M + c0) * 4);
+        const double w3 = x3 * rd[c0 + 3];
+        x2 = fma(-B[14], w3, x2);
+        const double w2 = x2 * rd[c0 + 2];
+        x1 = fma(-B[13], w3, x1);
+        x1 = fma(-B[9], w2, x1);
+        const double w1 = x1 * rd[c0 + 1];
+        x0 = fma(-B[12], w3, x0);
+        x0 = fma(-B[8], w2, x0);
+        x0 = fma(-B[4], w1, x0);
+        const double w0 = x0 * rd[c0];
+        {
+          const double wm = jm4 == 0 ? w0 : jm4 == 1 ? w1 : jm4 == 2 ? w2 : w3;
+          if ((sl >> 2) == (cb >> 2)) v[s] = wm;
+        }
 #pragma unroll
         for (int s2 = 0; s2 <= s; ++s2) {
           const int r = s2 * 32 + sl;
-          if (r < c) v[s2] = fma(-Lr[c * M + r], wc, v[s2]);
+          if (r < c0) {
+            const double2* q = reinterpret_cast<const double2*>(LB + (cb0(c0) * M + r) * 4);   // L[c0 .. c0 + 3][r]
+            const double2 a01 = q[0], a23 = q[1];
+            v[s2] = fma(-a23.y, w3, v[s2]);
+            v[s2] = fma(-a23.x, w2, v[s2]);
+            v[s2] = fma(-a01.y, w1, v[s2]);
+            v[s2] = fma(-a01.x, w0, v[s2]);
+          }
         }
       }
     }
@@ -797,7 +855,7 @@ static Status launch_weights(const rk_setup* s, int32_t* base, double* weights, 
   if (L <= 4 && !generic) {
     const size_t wsl = sizeof(double) * (2 * M * M + M);
     const int G = M <= 4 ? 8 : M <= 16 ? 2 : 1;
-    const int wbl = (int)std::min<int64_t>(ceil_div(ceil_div(n, G), 8), 148 * 16);
+    const int wbl = (int)std::min<int64_t>(ceil_div(ceil_div(n, G), 8), 148 * 3);   // resident: 3 per SM
     auto launch_l = [&](auto kern) -> Status {
       RK_TRY(set_smem_attr((const void*)kern, wsl));
       kern<<<wbl, 256, wsl, st>>>(wa);
