@@ -15,6 +15,10 @@
 
 namespace rk {
 
+// reciprocals of the Temme series' per-term divisors, tabulated on the host: the series
+// loop multiplies instead of dividing (a double division is a ~10-instruction dependent chain)
+constexpr int kTemmeTab = 24;
+
 struct MaternDev {
   double sigma2, alpha;
   int half_n;             // >= 0: closed form
@@ -23,6 +27,10 @@ struct MaternDev {
   double pref;
   int nl;
   double mu, gampl, gammi, gam1, gam2, fact, gamma_nu;
+  double rq[kTemmeTab];   // 1 / (i^2 - mu^2), i = 1 .. kTemmeTab
+  double ri[kTemmeTab];   // 1 / i
+  double rm[kTemmeTab];   // 1 / (i - mu)
+  double rp[kTemmeTab];   // 1 / (i + mu)
 };
 
 inline MaternDev make_matern_dev(const rk_model& m) {
@@ -41,6 +49,14 @@ inline MaternDev make_matern_dev(const rk_model& m) {
   d.gam2 = m.temme_gam2;
   d.fact = m.temme_fact;
   d.gamma_nu = m.gamma_nu;  // divisor in 2 r0 / Gamma(nu) (bessel.py:255)
+  const double mu2 = d.mu * d.mu;
+  for (int i = 1; i <= kTemmeTab; ++i) {
+    const double di = (double)i;
+    d.rq[i - 1] = 1.0 / (di * di - mu2);
+    d.ri[i - 1] = 1.0 / di;
+    d.rm[i - 1] = 1.0 / (di - d.mu);
+    d.rp[i - 1] = 1.0 / (di + d.mu);
+  }
   return d;
 }
 
@@ -61,10 +77,17 @@ __device__ inline bool kv_pair_series(const MaternDev& P, double x, double& k0, 
   const double mu2 = mu * mu;
   for (int i = 1; i <= 500; ++i) {
     const double di = (double)i;
-    f = (di * f + p + q) / (di * di - mu2);
-    c *= d / di;
-    p /= di - mu;
-    q /= di + mu;
+    if (i <= kTemmeTab) {
+      f = (di * f + p + q) * P.rq[i - 1];
+      c *= d * P.ri[i - 1];
+      p *= P.rm[i - 1];
+      q *= P.rp[i - 1];
+    } else {
+      f = (di * f + p + q) / (di * di - mu2);
+      c *= d / di;
+      p /= di - mu;
+      q /= di + mu;
+    }
     const double del = c * f;
     s0 += del;
     s1 += c * (p - di * f);
