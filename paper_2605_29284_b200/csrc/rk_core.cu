@@ -356,8 +356,13 @@ __global__ void __launch_bounds__(256) weights_kernel(WArgs a) {
 // generic kernel pays a division, runtime index arithmetic and the loop bounds.
 __device__ __forceinline__ int cb0(int c0) { return c0 >> 2; }   // 4-column block of column c0
 
-template <int L>
-__global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
+// HELP (L = 3, M = 36, Bessel-path Matern): the four cross covariances of each observation
+// beyond the warp's 32 lanes are evaluated by a ninth helper warp in parallel (one evaluation
+// per thread instead of two serial rounds), handed over through shared memory.  Only for the
+// latency-bound Bessel case: with the closed forms the extra barrier per trip costs more.
+template <int L, bool HELP = false>
+__global__ void __launch_bounds__(HELP ? 288 : 256, HELP ? 2 : 3) weights_kernel_l(WArgs a) {
+  static_assert(!HELP || L == 3, "helper warp layout is for M = 36");
   constexpr int BS = 2 * L, M = BS * BS;
   constexpr int LPO = M <= 4 ? 4 : M <= 16 ? 16 : 32;   // lanes per observation
   constexpr int G = 32 / LPO;                            // observations per warp
@@ -368,6 +373,7 @@ __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
   double* LF = wsm;                // LF[((c / 4) * M + r) * 4 + c % 4] = L[r][c]   (forward)
   double* LB = wsm + M * M;        // LB[((c / 4) * M + r) * 4 + c % 4] = L[c][r]   (backward)
   double* rd = wsm + 2 * M * M;    // 1 / L[c][c]
+  double* kx = rd + M;             // HELP: (8 observations, M - 32) helper-evaluated covariances
   for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
     const int r = e / M, c = e % M;
     const double v = a.chol[e];
@@ -378,7 +384,8 @@ __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPO, sl = lane - sub * LPO;
   const int warp = threadIdx.x >> 5;
-  const int wpb = blockDim.x >> 5;
+  const int wpb = HELP ? 8 : blockDim.x >> 5;   // observation warps per CTA
+  const bool helper = HELP && warp == 8;
   const int64_t nw = (a.n + G - 1) / G;
   // persistent CTAs (the factor is staged once per CTA); the trip count is the same for every
   // warp so the staging barrier can sit after the first cross covariances (their latency
@@ -386,7 +393,9 @@ __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
   const int64_t stride = (int64_t)gridDim.x * wpb;
   const int64_t trips = (nw + stride - 1) / stride;
   for (int64_t it = 0; it < trips; ++it) {
-    const int64_t wi = (int64_t)blockIdx.x * wpb + warp + it * stride;
+    // the helper's lane l serves observation warp l / 4, covariance 32 + l % 4
+    const int ow = helper ? lane >> 2 : warp;
+    const int64_t wi = (int64_t)blockIdx.x * wpb + ow + it * stride;
     const int64_t i = wi * G + sub;
     bool live = i < a.n;
     const double x = live ? a.obs[2 * i] : a.px0, y = live ? a.obs[2 * i + 1] : a.py0;
@@ -394,14 +403,14 @@ __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
     const double ty = __ddiv_rn(__dsub_rn(y, a.py0), a.hy);
     int cx = 0, cy = 0;
     if (live && !(tx >= -1.0e-9 && tx <= a.hix && ty >= -1.0e-9 && ty <= a.hiy)) {
-      if (sl == 0) atomicMin(&a.err[0], (int)i);
+      if (sl == 0 && !helper) atomicMin(&a.err[0], (int)i);
       live = false;
     }
     if (live) {
       cx = snap_cell(tx);
       cy = snap_cell(ty);
       if (cx - (L - 1) < 0 || cy - (L - 1) < 0 || cx + L > a.M1 - 1 || cy + L > a.M2 - 1) {
-        if (sl == 0) atomicMin(&a.err[1], (int)i);
+        if (sl == 0 && !helper) atomicMin(&a.err[1], (int)i);
         live = false;
       }
     }
@@ -412,9 +421,10 @@ __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
     int bad = 0;
 #pragma unroll
     for (int s = 0; s < MPL; ++s) {
-      const int m = s * 32 + sl;
+      // HELP: observation warps evaluate chunk 0 only; the helper lane evaluates entry 32 + l % 4
+      const int m = helper ? 32 + (lane & 3) : s * 32 + sl;
       k[s] = 0.0;
-      if (live && m < M) {
+      if (live && m < M && (!HELP || s == 0)) {
         const int r = m / BS, q = m % BS;
         const double nx = __dadd_rn(a.px0, __dmul_rn((double)(xlo + q), a.hx));
         const double ny = __dadd_rn(a.py0, __dmul_rn((double)(ylo + r), a.hy));
@@ -424,7 +434,16 @@ __global__ void __launch_bounds__(256, 3) weights_kernel_l(WArgs a) {
       v[s] = k[s];
     }
     if (bad) atomicOr(&a.err[2], 1);
-    if (it == 0) __syncthreads();   // factor staged
+    if (HELP) {
+      double* kb = kx + (it & 1) * 32;   // double-buffered: trip t + 2 reuses it after trip t + 1's barrier
+      if (helper) kb[lane] = k[0];
+      __syncthreads();   // helper results (and, on the first trip, the factor) staged
+      if (helper) continue;
+      k[1] = sl < M - 32 ? kb[warp * (M - 32) + sl] : 0.0;
+      v[1] = k[1];
+    } else if (it == 0) {
+      __syncthreads();   // factor staged
+    }
     // forward substitution L y = k, column oriented (y overwrites v), four columns per step:
     // every lane gathers the block's four entries (independent shuffles) and solves the 4 x 4
     // diagonal block itself, then applies the four column updates to its rows with one 32-byte
@@ -853,16 +872,18 @@ static Status launch_weights(const rk_setup* s, int32_t* base, double* weights, 
   };
   static const bool generic = getenv("RK_WEIGHTS_GENERIC") && atoi(getenv("RK_WEIGHTS_GENERIC"));
   if (L <= 4 && !generic) {
-    const size_t wsl = sizeof(double) * (2 * M * M + M);
+    const size_t wsl = sizeof(double) * (2 * M * M + M + 64);
     const int G = M <= 4 ? 8 : M <= 16 ? 2 : 1;
-    const int wbl = (int)std::min<int64_t>(ceil_div(ceil_div(n, G), 8), 148 * 3);   // resident: 3 per SM
+    const bool help = L == 3 && s->mat.half_n < 0;
+    const int wbl = (int)std::min<int64_t>(ceil_div(ceil_div(n, G), 8), 148 * (help ? 2 : 3));   // resident
     auto launch_l = [&](auto kern) -> Status {
       RK_TRY(set_smem_attr((const void*)kern, wsl));
-      kern<<<wbl, 256, wsl, st>>>(wa);
+      kern<<<wbl, help ? 288 : 256, wsl, st>>>(wa);
       return Status::ok();
     };
     if (L == 1) RK_TRY(launch_l(weights_kernel_l<1>));
     else if (L == 2) RK_TRY(launch_l(weights_kernel_l<2>));
+    else if (L == 3 && help) RK_TRY(launch_l(weights_kernel_l<3, true>));
     else if (L == 3) RK_TRY(launch_l(weights_kernel_l<3>));
     else RK_TRY(launch_l(weights_kernel_l<4>));
   } else if (mpl <= 1) {
