@@ -7,7 +7,8 @@ cannot run a 4374^2 torus per test in seconds):
   restated at full size; phi from the numpy oracle), linearity in c, and c = 0 -> exactly the
   fixed part;
 * configs[3] (n = 5000, 512^2, L = 3, CS torus 2304^2): ensemble mean / SE bitwise identical
-  whatever the realization batch size, and the SE finite and positive.
+  whatever the realization batch size, and the SE finite and positive;
+* configs[4]'s largest cell (n = 50000, 4096^2, 8748^2 torus): field vs the direct sum.
 """
 import numpy as np
 import pytest
@@ -81,3 +82,30 @@ def test_cfg4_ensemble_batch_independent(pk):
     assert np.array_equal(a.mean_field, b.mean_field)
     assert np.array_equal(a.empirical_se, b.empirical_se)
     assert np.all(np.isfinite(a.empirical_se)) and a.empirical_se.min() >= 0.0 and a.empirical_se.max() > 0.0
+
+
+def test_cfg5_largest_cell_matches_direct_sum(pk):
+    """configs[4]'s largest cell (n = 50000, 4096^2 grid, L = 4, nu = 1.5; an 8748^2 torus):
+    random coefficients (predict does not need the n x n fit), field against the direct sum at
+    sampled nodes."""
+    from oracle import rk_oracle as ro
+    from paper_2605_29284_b200 import workloads
+    wl = workloads.cfg5(nu=1.5, L=4, m=4096)
+    model = pk.CovarianceModel(wl.sigma2, wl.alpha, wl.nu, wl.tau2)
+    grid = pk.build_padded_grid(wl.domain, wl.dims, wl.L, wl.obs)
+    st = pk.build_setup(model, grid, wl.L, wl.obs)
+    assert max(st.embed_dims) >= 8192
+    rng = np.random.default_rng(51)
+    c = rng.normal(size=wl.obs.shape[0])
+    field = pk.predict_rapid(st, c, np.array([-0.5]))
+    cstar = st.coefficients_to_grid(c)
+    iy, ix = np.nonzero(cstar)
+    vals = cstar[iy, ix]
+    hx, hy = grid.spacing
+    l, _, b, _ = grid.pad
+    m1, m2 = grid.interior_dims
+    scale = np.abs(field).max()
+    for jx, jy in [(0, 0), (m1 - 1, m2 - 1)] + [tuple(int(v) for v in rng.integers(0, [m1, m2])) for _ in range(4)]:
+        d = np.hypot((ix - (jx + l)) * hx, (iy - (jy + b)) * hy)
+        ref = float(np.dot(vals, model.sigma2 * ro.matern_phi(wl.alpha * d, wl.nu))) - 0.5
+        assert abs(field[jy, jx] - ref) <= 1e-10 * scale, (jx, jy, field[jy, jx], ref)
