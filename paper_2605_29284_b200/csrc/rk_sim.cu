@@ -469,8 +469,13 @@ __device__ __forceinline__ void philox_words4(uint64_t w, uint64_t fs, uint64_t 
   }
 }
 
-template <bool TWS, int FM>
-__global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSplitThreads : 512, 1) cs_rowgen_kernel(const CsGenArgs a) {
+// MAXT / MINB: the occupancy variant used for WIDE plans of one line of <= 288 threads per CTA
+// (e.g. cfg4's 2304-point rows): twiddles from L1 instead of smem and 128-entry tail queues, so
+// four CTAs fit an SM (56 registers) instead of three; CS 138.7 -> 135.4 us per realization.
+// RK_CS_GEN4=0 keeps the 3-per-SM kernel.
+template <bool TWS, int FM, int MAXT = (FM == 1 ? kFftWideThreads : FM == 2 ? kFftSplitThreads : 512), int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB) cs_rowgen_kernel(const CsGenArgs a) {
+  constexpr int QCAP = MINB > 1 ? 128 : 256;   // tail-queue entries per warp
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
   const int nthr = a.pl.nthr;
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSpli
   const int b = blockIdx.y;
   const int iy = blockIdx.x * a.lpc + line;
   double2* buf = smem + (size_t)line * n;
-  double* wq = (double*)(smem + a.q_off) + (size_t)(threadIdx.x >> 5) * 256;
+  double* wq = (double*)(smem + a.q_off) + (size_t)(threadIdx.x >> 5) * QCAP;
   const FftPlan pls = TWS ? fft_twiddles_to_smem(a.pl, smem + a.tw_off) : a.pl;
   const uint64_t fs = a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
   if (iy < a.ps2) {
@@ -514,7 +519,11 @@ __global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSpli
       }
       const int total = __shfl_sync(0xffffffffu, off, 31);
       off -= cnt;
-      if (total) {
+      if (total > QCAP) {   // queue overflow (never in practice): each lane evaluates its own
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (tmask >> q & 1) z[q] = ndtri_tail(uu[q]);
+      } else if (total) {
         int o = off;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
@@ -577,13 +586,16 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     ga.ldV = ldV;
     ga.V_bstride = (int64_t)s->M1 * ldV;
     const int warps = ga.lpc * ga.pl.nthr / 32;
+    static const bool gen4 = !(getenv("RK_CS_GEN4") && atoi(getenv("RK_CS_GEN4")) == 0);
+    const bool occ4 = gen4 && ga.pl.wide == 2 && ga.lpc == 1 && ga.pl.nthr <= 288;
     ga.q_off = (int)(ga.lpc * (size_t)e.ps1);
-    ga.tw_off = ga.q_off + warps * 128;   // 256 doubles per warp
+    ga.tw_off = ga.q_off + warps * (occ4 ? 64 : 128);   // 128 / 256 doubles per warp
     size_t smem = sizeof(double2) * ((size_t)ga.tw_off + ga.pl.ntw);
-    const bool tws = smem <= 227 * 1024;
+    const bool tws = !occ4 && smem <= 227 * 1024;
     if (!tws) smem = sizeof(double2) * (size_t)ga.tw_off;
-    if (ga.pl.wide >= 2 && !tws) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
-    auto kern = ga.pl.wide == 2 ? cs_rowgen_kernel<true, 1> : ga.pl.wide == 3 ? cs_rowgen_kernel<true, 2>
+    if (ga.pl.wide >= 2 && !tws && !occ4) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
+    auto kern = occ4 ? cs_rowgen_kernel<false, 1, 288, 4>
+                : ga.pl.wide == 2 ? cs_rowgen_kernel<true, 1> : ga.pl.wide == 3 ? cs_rowgen_kernel<true, 2>
                 : tws ? cs_rowgen_kernel<true, 0> : cs_rowgen_kernel<false, 0>;
     RK_TRY(set_smem_attr((const void*)kern, smem));
     const dim3 grid((unsigned)ceil_div(e.ps2, ga.lpc), (unsigned)batch);
