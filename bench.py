@@ -409,7 +409,7 @@ def cpu_baseline_predict(case, wl, seconds=10.0, min_reps=5):
 
 
 # ------------------------------------------------------------------ CS
-def bench_cs(pk, steps, warmup, rank, world, R=1024, batch=32):
+def bench_cs(pk, steps, warmup, rank, world, R=1024, batch=64):
     import torch
     from paper_2605_29284_b200 import _native as N
     from paper_2605_29284_b200 import workloads
