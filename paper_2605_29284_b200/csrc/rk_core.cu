@@ -744,7 +744,7 @@ static Status build_sparse_gather(rk_setup* s) {
   RK_CUDA_TRY(cudaMalloc(&flag, sizeof(int32_t) * tot));
   RK_CUDA_TRY(cudaMalloc(&pos, sizeof(int32_t) * tot));
   RK_CUDA_TRY(cudaMalloc(&s->ent_w, sizeof(int32_t) * tot));
-  RK_CUDA_TRY(cudaMalloc(&s->ent_c, sizeof(int32_t) * tot));
+  RK_CUDA_TRY(cudaMalloc(&s->ent_c, sizeof(int32_t) * (tot + 4)));   // + slack: pass 1 bulk-copies 16-byte-rounded ranges
   const int grid = (int)std::min<int64_t>(ceil_div(tot, 256), 148 * 32);
   ent_gen_kernel<<<grid, 256>>>(s->bsort, s->n, s->M, s->bs, s->M1, key, val);
   count_launch();
@@ -769,8 +769,8 @@ static Status build_sparse_gather(rk_setup* s) {
   RK_CUDA_TRY(cudaMemcpy(&last_pos, pos + tot - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
   RK_CUDA_TRY(cudaMemcpy(&last_flag, flag + tot - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
   s->nnodes = (int64_t)last_pos + last_flag;
-  RK_CUDA_TRY(cudaMalloc(&s->node_q, sizeof(int32_t) * (s->nnodes + 1)));
-  RK_CUDA_TRY(cudaMalloc(&s->node_off, sizeof(int32_t) * (s->nnodes + 1)));
+  RK_CUDA_TRY(cudaMalloc(&s->node_q, sizeof(int32_t) * (s->nnodes + 5)));
+  RK_CUDA_TRY(cudaMalloc(&s->node_off, sizeof(int32_t) * (s->nnodes + 5)));
   RK_CUDA_TRY(cudaMalloc(&s->row_node, sizeof(int32_t) * (s->M2 + 1)));
   node_fill_kernel<<<grid, 256>>>(key2, flag, pos, tot, s->bs, s->node_q, s->node_off);
   count_launch();
@@ -798,7 +798,7 @@ static Status build_sparse_gather(rk_setup* s) {
     RK_CUDA_TRY(cudaMalloc(&s->pair_info, sizeof(int4) * pi.size()));
     RK_CUDA_TRY(cudaMemcpy(s->pair_info, pi.data(), sizeof(int4) * pi.size(), cudaMemcpyHostToDevice));
   }
-  RK_CUDA_TRY(cudaMalloc(&s->ent_wv, sizeof(double) * std::max<int64_t>(tot, 1)));
+  RK_CUDA_TRY(cudaMalloc(&s->ent_wv, sizeof(double) * (std::max<int64_t>(tot, 1) + 2)));
   ent_value_kernel<<<grid, 256>>>(s->ent_w, s->wsort, tot, s->ent_wv);
   count_launch();
   RK_LAUNCH_CHECK();
