@@ -802,6 +802,48 @@ static Status build_sparse_gather(rk_setup* s) {
   ent_value_kernel<<<grid, 256>>>(s->ent_w, s->wsort, tot, s->ent_wv);
   count_launch();
   RK_LAUNCH_CHECK();
+  {  // fixed-stride per-pair plan blocks for small plans (pass 1 of one-wave launches)
+    const int npairs = (s->M2 + 1) / 2;
+    const int cap = (int)((s->max_pair_ent + 1) & ~int64_t(1));
+    const int64_t stride = (16 + (int64_t)cap * 20 + 15) & ~int64_t(15);
+    if (cap > 0 && cap <= 2048 && stride * npairs <= (int64_t)64 << 20) {
+      std::vector<int4> pi(npairs + 1);
+      std::vector<int32_t> nq(s->nnodes + 1), no(s->nnodes + 1), ec(std::max<int64_t>(tot, 1));
+      std::vector<double> ew(std::max<int64_t>(tot, 1));
+      RK_CUDA_TRY(cudaMemcpy(pi.data(), s->pair_info, sizeof(int4) * pi.size(), cudaMemcpyDeviceToHost));
+      RK_CUDA_TRY(cudaMemcpy(nq.data(), s->node_q, sizeof(int32_t) * nq.size(), cudaMemcpyDeviceToHost));
+      RK_CUDA_TRY(cudaMemcpy(no.data(), s->node_off, sizeof(int32_t) * no.size(), cudaMemcpyDeviceToHost));
+      if (tot > 0) {
+        RK_CUDA_TRY(cudaMemcpy(ec.data(), s->ent_c, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
+        RK_CUDA_TRY(cudaMemcpy(ew.data(), s->ent_wv, sizeof(double) * tot, cudaMemcpyDeviceToHost));
+      }
+      std::vector<unsigned char> hb((size_t)stride * npairs, 0);
+      for (int p = 0; p < npairs; ++p) {
+        const int n0 = pi[p].x, n1 = pi[p].y, e0 = pi[p].z;
+        const int nn = pi[p + 1].x - n0, cnt = pi[p + 1].z - e0;
+        unsigned char* blk = hb.data() + (size_t)p * stride;
+        int32_t* hdr = reinterpret_cast<int32_t*>(blk);
+        hdr[0] = cnt;
+        hdr[1] = nn;
+        int2* rec = reinterpret_cast<int2*>(blk + 16);
+        double* wv = reinterpret_cast<double*>(blk + 16 + (size_t)cap * 8);
+        int32_t* ci = reinterpret_cast<int32_t*>(blk + 16 + (size_t)cap * 16);
+        const int rowq = 2 * p * s->M1;
+        for (int i = 0; i < nn; ++i) {   // as pass 1 forms it: end of products, 2 x + odd row
+          const int odd = n0 + i >= n1;
+          rec[i] = make_int2(no[n0 + i + 1] - e0, 2 * (nq[n0 + i] - rowq - odd * (int)s->M1) + odd);
+        }
+        for (int i = 0; i < cnt; ++i) {
+          wv[i] = ew[e0 + i];
+          ci[i] = ec[e0 + i];
+        }
+      }
+      RK_CUDA_TRY(cudaMalloc(&s->pblk, hb.size()));
+      RK_CUDA_TRY(cudaMemcpy(s->pblk, hb.data(), hb.size(), cudaMemcpyHostToDevice));
+      s->pblk_stride = stride;
+      s->pblk_cap = cap;
+    }
+  }
   cudaFree(tmp);
   cudaFree(key);
   cudaFree(key2);
@@ -830,6 +872,7 @@ static void free_setup(rk_setup* s) {
   cudaFree(s->ent_c);
   cudaFree(s->ent_wv);
   cudaFree(s->pair_info);
+  cudaFree(s->pblk);
   cudaFree(s->spec_q);
   cudaFree(s->kn_chol_dev);
   cudaFree(s->emb.root_q);

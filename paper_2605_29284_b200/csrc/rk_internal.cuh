@@ -123,6 +123,12 @@ struct rk_setup {
   int64_t max_pair_ent = 0;       // most contributions of one row pair (2k, 2k+1)
   double* ent_wv = nullptr;       // (n M) weight of each contribution (wsort[ent_w])
   int4* pair_info = nullptr;      // (ceil(M2/2) + 1) {node0, node of row 2p+1, contribution0, 0}
+  // per-row-pair plan blocks at a fixed stride (small plans only): {count, nodes, 0, 0}, then
+  // node records int2 {end of its products, 2 x + odd row} [cap], weights double [cap],
+  // observation indices int [cap] -- pass 1 fetches a pair's whole plan in one bulk copy
+  unsigned char* pblk = nullptr;
+  int64_t pblk_stride = 0;        // bytes (multiple of 16)
+  int pblk_cap = 0;
   double* spec_q = nullptr;     // (H1, Q2): Re fft2(filter)[ky, kx] / (p1 p2), ky <= p2/2
   double* kn_chol_dev = nullptr;  // (M, M) row-major lower
   std::vector<double> kn_chol, kn_inv;

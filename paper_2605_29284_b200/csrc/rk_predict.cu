@@ -100,8 +100,9 @@ struct RowFwdArgs {
                              // of the staged products w * c of the line's row pair
   int c_off, c_n;            // SRC_SPARSE, c_n > 0: the whole coefficient vector (c_n entries)
                              // is bulk-copied to smem at offset c_off (double2 units) up front
-  int pl_off, pl_cap;        // SRC_SPARSE, pl_cap > 0: each line's plan ranges (weights, obs
-                             // indices, node records) bulk-copied to smem at pl_off, pl_cap slots
+  const unsigned char* pblk;  // SRC_SPARSE (one-wave launches): the setup's per-pair plan blocks,
+  int64_t pblk_stride;       // fetched per line into smem at pl_off (double2 units)
+  int pblk_cap, pl_off;
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
 };
 
@@ -202,88 +203,74 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
       cl = cs;
       __syncthreads();   // barrier initialised before anyone waits on it
     }
-    int4 P0 = make_int4(0, 0, 0, 0), P1 = P0;
-    if (va) {
-      P0 = __ldg(&g.pair_info[pidx]);
-      P1 = __ldg(&g.pair_info[pidx + 1]);
-    }
-    const int n0 = P0.x, n1 = P0.y, e0 = P0.z;
-    const int nn = P1.x - n0, cnt = P1.z - e0;
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
-    const int rowq = ya * g.M1;
     bool cwait = cbar != nullptr;
-    // one pass issues the contribution loads and the node-record loads together; only the
-    // coefficient loads depend on them
-    constexpr int U = 4;
-    const int m = max(cnt, nn);
-    // one-wave launches: the pair's four plan ranges arrive by TMA bulk copies (16-byte-rounded,
-    // the buffers carry slack) -- one round trip for any pair size, so the most loaded row
-    // pair no longer takes a dependent round trip per U * nthr contributions
-    const double* __restrict__ pwv = g.ent_wv + e0;
-    const int* __restrict__ pci = g.ent_c + e0;
-    const int* __restrict__ pnq = g.node_q + n0;
-    const int* __restrict__ pne = g.node_off + n0 + 1;
-    if (FM != 1 && a.pl_cap > 0) {   // (never for the WIDE kernels: keeps their register budget)
-      const int cap = a.pl_cap;   // multiple of 4
-      // per line (stride (cap + 8) * 24 bytes): weights cap + 4 doubles, then three int ranges of
-      // cap + 8 each (a rounded-up copy never reaches the next range), then the barrier
-      double* wv_s = (double*)(smem + a.pl_off) + (size_t)line * (size_t)(cap + 8) * 3;
-      int* ci_s = (int*)(wv_s + cap + 4);
-      int* nq_s = ci_s + cap + 8;
-      int* ne_s = nq_s + cap + 8;
-      uint64_t* pbar = (uint64_t*)(ne_s + cap + 8);
+    int nn = 0;
+    const int2* nrp = nrec;   // the node records the sums below read
+    if (FM != 1 && a.pblk) {
+      // one-wave launches: the pair's whole plan (counts, node records, weights, observation
+      // indices) is one fixed-stride block fetched by ONE bulk copy -- a single global round
+      // trip for any pair size, where the most loaded pair of a clustered design otherwise
+      // takes a dependent round trip per 4 * nthr contributions and sets the pass's end
+      unsigned char* blk = reinterpret_cast<unsigned char*>(smem + a.pl_off) + (size_t)line * (a.pblk_stride + 16);
+      uint64_t* pbar = reinterpret_cast<uint64_t*>(blk + a.pblk_stride);
       if (tl == 0) mbar_init(pbar, 1);
       __syncthreads();
-      const int aw = e0 & 1, ac = e0 & 3, aq = n0 & 3, ae = (n0 + 1) & 3;
       if (tl == 0) {
-        const uint32_t bw = cnt ? (uint32_t)((cnt + aw) * 8 + 15) & ~15u : 0u;
-        const uint32_t bc = cnt ? (uint32_t)((cnt + ac) * 4 + 15) & ~15u : 0u;
-        const uint32_t bq = nn ? (uint32_t)((nn + aq) * 4 + 15) & ~15u : 0u;
-        const uint32_t be = nn ? (uint32_t)((nn + ae) * 4 + 15) & ~15u : 0u;
-        mbar_expect_tx(pbar, bw + bc + bq + be);
-        if (bw) bulk_g2s(wv_s, g.ent_wv + (e0 - aw), bw, pbar);
-        if (bc) bulk_g2s(ci_s, g.ent_c + (e0 - ac), bc, pbar);
-        if (bq) bulk_g2s(nq_s, g.node_q + (n0 - aq), bq, pbar);
-        if (be) bulk_g2s(ne_s, g.node_off + (n0 + 1 - ae), be, pbar);
+        mbar_expect_tx(pbar, va ? (uint32_t)a.pblk_stride : 0u);
+        if (va) bulk_g2s(blk, a.pblk + (int64_t)pidx * a.pblk_stride, (uint32_t)a.pblk_stride, pbar);
       }
       mbar_wait(pbar, 0);
-      pwv = wv_s + aw;
-      pci = ci_s + ac;
-      pnq = nq_s + aq;
-      pne = ne_s + ae;
-    }
-    for (int i0 = tl; i0 < m; i0 += U * nthr) {
-      double w[U];
-      int ci[U], nq[U], ne[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nthr;
-        if (FM == 1) {   // WIDE kernels: read-only cache path as before
-          w[u] = i < cnt ? __ldg(&pwv[i]) : 0.0;
-          ci[u] = i < cnt ? __ldg(&pci[i]) : 0;
-          nq[u] = i < nn ? __ldg(&pnq[i]) : 0;
-          ne[u] = i < nn ? __ldg(&pne[i]) : 0;
-        } else {
-          w[u] = i < cnt ? pwv[i] : 0.0;
-          ci[u] = i < cnt ? pci[i] : 0;
-          nq[u] = i < nn ? pnq[i] : 0;
-          ne[u] = i < nn ? pne[i] : 0;
-        }
-      }
-      if (cwait) {   // first use: the bulk copy (init ordered by the barrier above) has landed
+      const int cnt = va ? reinterpret_cast<const int*>(blk)[0] : 0;
+      nn = va ? reinterpret_cast<const int*>(blk)[1] : 0;
+      nrp = reinterpret_cast<const int2*>(blk + 16);
+      const double* wv = reinterpret_cast<const double*>(blk + 16 + (size_t)a.pblk_cap * 8);
+      const int* ci = reinterpret_cast<const int*>(blk + 16 + (size_t)a.pblk_cap * 16);
+      if (cwait) {
         mbar_wait(cbar, 0);
         cwait = false;
       }
-      double cv[U];
+      for (int i = tl; i < cnt; i += nthr) prod[i] = __dmul_rn(wv[i], cl[ci[i]]);
+    } else {
+      int4 P0 = make_int4(0, 0, 0, 0), P1 = P0;
+      if (va) {
+        P0 = __ldg(&g.pair_info[pidx]);
+        P1 = __ldg(&g.pair_info[pidx + 1]);
+      }
+      const int n0 = P0.x, n1 = P0.y, e0 = P0.z;
+      nn = P1.x - n0;
+      const int cnt = P1.z - e0;
+      const int rowq = ya * g.M1;
+      // one pass issues the contribution loads and the node-record loads together; only the
+      // coefficient loads depend on them
+      constexpr int U = 4;
+      const int m = max(cnt, nn);
+      for (int i0 = tl; i0 < m; i0 += U * nthr) {
+        double w[U];
+        int ci[U], nq[U], ne[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) cv[u] = i0 + u * nthr < cnt ? cl[ci[u]] : 0.0;
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * nthr;
+          w[u] = i < cnt ? __ldg(&g.ent_wv[e0 + i]) : 0.0;
+          ci[u] = i < cnt ? __ldg(&g.ent_c[e0 + i]) : 0;
+          nq[u] = i < nn ? __ldg(&g.node_q[n0 + i]) : 0;
+          ne[u] = i < nn ? __ldg(&g.node_off[n0 + i + 1]) : 0;
+        }
+        if (cwait) {   // first use: the bulk copy (init ordered by the barrier above) has landed
+          mbar_wait(cbar, 0);
+          cwait = false;
+        }
+        double cv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * nthr;
-        if (i < cnt) prod[i] = __dmul_rn(w[u], cv[u]);
-        if (i < nn) {   // node i: end of its products, its x | odd-row bit
-          const int odd = n0 + i >= n1;
-          nrec[i] = make_int2(ne[u] - e0, 2 * (nq[u] - rowq - odd * g.M1) + odd);
+        for (int u = 0; u < U; ++u) cv[u] = i0 + u * nthr < cnt ? cl[ci[u]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * nthr;
+          if (i < cnt) prod[i] = __dmul_rn(w[u], cv[u]);
+          if (i < nn) {   // node i: end of its products, its x | odd-row bit
+            const int odd = n0 + i >= n1;
+            nrec[i] = make_int2(ne[u] - e0, 2 * (nq[u] - rowq - odd * g.M1) + odd);
+          }
         }
       }
     }
@@ -292,8 +279,8 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
     RK_PHASE(0, 1);
     double* bd = (double*)buf;
     for (int k = tl; k < nn; k += nthr) {
-      const int s0 = k ? nrec[k - 1].x : 0;
-      const int2 r = nrec[k];
+      const int s0 = k ? nrp[k - 1].x : 0;
+      const int2 r = nrp[k];
       double acc = 0.0;
       for (int i = s0; i < r.x; ++i) acc = __dadd_rn(acc, prod[i]);   // (w * c) then add, as np.add.at
       bd[r.y] = acc;
@@ -583,9 +570,9 @@ static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStrea
   if (src == SRC_SPARSE) {
     a.prod_off = tw_slot(smem);
     smem = (size_t)a.prod_off * 16 + sizeof(double) * (size_t)a.lpc * 2 * a.prod_cap;
-    if (a.pl_cap > 0) {   // per line: weights, three int ranges and a barrier in (cap + 8) * 24 bytes
+    if (a.pblk) {   // per line: one plan block + its barrier
       a.pl_off = tw_slot(smem);
-      smem = (size_t)a.pl_off * 16 + (size_t)a.lpc * (size_t)(a.pl_cap + 8) * 24;
+      smem = (size_t)a.pl_off * 16 + (size_t)a.lpc * (size_t)(a.pblk_stride + 16);
     }
     if (a.c_n > 0) {   // whole c in smem only while it stays a small share of the CTA's budget
       const bool aligned = (reinterpret_cast<uintptr_t>(a.sp.c) & 15) == 0 && (a.sp.c_stride * 8) % 16 == 0;
@@ -823,9 +810,12 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     // plan ranges by TMA only for one-wave launches (spread / split plans): elsewhere the extra
     // shared memory would cost occupancy
     static const bool plan_tma = !(getenv("RK_PLAN_TMA") && atoi(getenv("RK_PLAN_TMA")) == 0);
-    const int cap4 = (int)((s->max_pair_ent + 3) & ~int64_t(3));
-    if (plan_tma && (ra.pl.wide == 1 || ra.pl.wide == 3) && (size_t)ra.lpc * (cap4 + 8) * 24 <= 48 * 1024)
-      ra.pl_cap = cap4;
+    if (plan_tma && s->pblk && (ra.pl.wide == 1 || ra.pl.wide == 3) &&
+        (size_t)ra.lpc * (size_t)(s->pblk_stride + 16) <= 64 * 1024) {
+      ra.pblk = s->pblk;
+      ra.pblk_stride = s->pblk_stride;
+      ra.pblk_cap = s->pblk_cap;
+    }
   }
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[1], st));
   RK_TRY(launch_row_fwd(sp ? SRC_SPARSE : SRC_ROWS, ra, batch, st));
