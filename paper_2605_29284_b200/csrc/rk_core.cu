@@ -806,7 +806,9 @@ static Status build_sparse_gather(rk_setup* s) {
     const int npairs = (s->M2 + 1) / 2;
     const int cap = (int)((s->max_pair_ent + 1) & ~int64_t(1));
     const int64_t stride = (16 + (int64_t)cap * 20 + 15) & ~int64_t(15);
-    if (cap > 0 && cap <= 2048 && stride * npairs <= (int64_t)64 << 20) {
+    // only where pass 1 can be a one-wave launch (a few row pairs per SM); large grids run
+    // the WIDE kernels, which keep the direct loads
+    if (cap > 0 && cap <= 2048 && npairs <= 148 * 4 && stride * npairs <= (int64_t)64 << 20) {
       std::vector<int4> pi(npairs + 1);
       std::vector<int32_t> nq(s->nnodes + 1), no(s->nnodes + 1), ec(std::max<int64_t>(tot, 1));
       std::vector<double> ew(std::max<int64_t>(tot, 1));
