@@ -137,6 +137,11 @@ rk_status rk_setup_time_weights(const rk_setup* s, void* stream, int32_t reps, f
 /* predict_rapid with per-kernel CUDA-event timing on `stream` (benchmark support):
  * ms_out[0..3] = gather (c* = A'c), pass 1 (row FFT), pass 2 (column filter),
  * pass 3 (row IFFT + epilogue) durations in milliseconds; synchronises the stream. */
+/* K1 alone into caller device buffers: base (n) int32, w (n, M), cv (n), err (4 int32,
+ * initialised by the caller to {INT_MAX, INT_MAX, 0, 0}); asynchronous on `stream`.  A predict
+ * step from observation coordinates is this + rk_predict_dev (SURVEY 8(d) T_predict). */
+rk_status rk_setup_weights_into(const rk_setup* s, int32_t* base_dev, double* w_dev, double* cv_dev,
+                                int32_t* err_dev, void* stream);
 rk_status rk_predict_profile(const rk_setup* s, const double* c_dev, const double* beta_dev,
                              int32_t p, const double* xg_dev, double* out_dev, void* stream,
                              float* ms_out);
@@ -195,19 +200,50 @@ rk_status rk_sim_unconditional_dev(rk_setup* s, uint64_t seed, double* field_dev
 rk_status rk_sim_obs_local_dev(const rk_setup* s, double tau2, const double* field_dev,
                                uint64_t seed, double* z_dev, void* stream);
 /* Ensemble slice (simulate.py:146-192): realizations j in [j0, j0+count) with
- * sub-seeds draw_seed(seed, j).  Adds, in j order and per pixel,
+ * sub-seeds draw_seed(seed, j).  Adds, per pixel,
  *   e_j = interior(g_j) - predict_rapid(c_sim_j, beta_sim_j)
- * into s1_dev += e, s2_dev += e*e (m2*m1 each, caller-zeroed per chunk).
- * draw_j = data_pred + e_j is written to draws_dev (count, m2, m1) if non-NULL.
- * xg_dev / p as in rk_predict_dev (p = fit's covariate count). */
+ * into the exact fixed-point moment accumulator acc_dev (int64, 6 * m2*m1, caller-zeroed):
+ * s1 = sum e, s2 = sum e^2 as trunc(v 2^64) in three signed 42-bit digits (v = e / 2^k, 2^k the
+ * power of two nearest sigma).  Integer sums are order-free: the result is bitwise the same
+ * for any batch size, split into slices, or number of GPUs.  draw_j = data_pred + e_j is
+ * written to draws_dev (count, m2, m1) if non-NULL.  xg_dev / p as in rk_predict_dev.
+ * RK_NUMERIC if a draw deviates by >= 2^20 sigma (outside the fixed-point range). */
 rk_status rk_ensemble_accumulate(rk_setup* s, const rk_fit* f, uint64_t seed, int64_t j0,
                                  int64_t count, const double* xg_dev,
-                                 const double* data_pred_dev, double* s1_dev, double* s2_dev,
+                                 const double* data_pred_dev, long long* acc_dev,
                                  double* draws_dev, int32_t batch, void* stream);
-/* mean = data_pred + s1/R ; se = sqrt((s2 - s1*s1/R)/(R-1)) (simulate.py:191-192) */
-rk_status rk_ensemble_finalize(int64_t n_pix, int64_t n_draws, const double* data_pred_dev,
-                               const double* s1_dev, const double* s2_dev, double* mean_dev,
-                               double* se_dev, void* stream);
+/* the fixed-point accumulation alone: acc_dev += moments of e_dev (count, n_pix) */
+rk_status rk_ensemble_accumulate_values(const double* e_dev, int32_t count, int64_t n_pix, double sigma2,
+                                        long long* acc_dev, void* stream);
+/* dst += src (two accumulators of n_pix pixels; exact) */
+rk_status rk_ensemble_combine(long long* dst_dev, const long long* src_dev, int64_t n_pix, void* stream);
+/* mean = data_pred + s1/R ; se = sqrt(max((s2 - s1*s1/R)/(R-1), 0)) (simulate.py:191-192);
+ * sigma2 = the model's (fixes the accumulator scale) */
+rk_status rk_ensemble_finalize(int64_t n_pix, int64_t n_draws, double sigma2,
+                               const double* data_pred_dev, const long long* acc_dev,
+                               double* mean_dev, double* se_dev, void* stream);
+/* build the fit's inverse factor L^-1 used by the batched refits now (otherwise on the
+ * first refit); cuSOLVER trtri -- setup, once per fit */
+rk_status rk_fit_prepare_refit(rk_fit* f, void* stream);
+/* kernel timing of the refit's two triangular panel products for S right-hand sides
+ * (CUDA events, mean of reps): ms_out[0] = L^-1 Z, ms_out[1] = L^-T H */
+rk_status rk_refit_profile(rk_fit* f, int64_t S, int32_t reps, void* stream, float* ms_out);
+
+/* ---- moving setups / fits between GPUs (ensemble sharding, rk_replicate.cu) ---- */
+/* copy onto `device` peer to peer (one process, several GPUs) */
+rk_status rk_setup_replicate(const rk_setup* src, int32_t device, rk_setup** out);
+rk_status rk_fit_replicate(const rk_fit* src, int32_t device, rk_fit** out);
+/* setup as one device blob (for a broadcast between processes): size, export into a
+ * caller buffer on the setup's device, import on the current device */
+rk_status rk_setup_blob_bytes(const rk_setup* s, int64_t* bytes);
+rk_status rk_setup_export(const rk_setup* s, void* blob_dev, void* stream);
+rk_status rk_setup_import(const void* blob_dev, int64_t bytes, rk_setup** out);
+/* fit arrays broadcast in place: an empty fit on the current device, its 7 array pointers /
+ * sizes (U, X, B, beta, c, obs, U^-1; NULL / 0 if absent), and the p x p Gram LU + pivots */
+rk_status rk_fit_shell(const rk_model* model, int64_t n, int32_t p, int32_t with_uinv, rk_fit** out);
+rk_status rk_fit_fields(const rk_fit* f, void** ptrs, int64_t* bytes);
+rk_status rk_fit_get_gram(const rk_fit* f, double* lu, int32_t* piv);
+rk_status rk_fit_set_gram(rk_fit* f, const double* lu, const int32_t* piv);
 
 #ifdef __cplusplus
 }

@@ -414,12 +414,10 @@ class Setup:
     ridge_applied: bool = False
 
 
-def rapid_setup(model: Model, grid: Grid, L: int, obs) -> Setup:
-    """rapid.py:177-230."""
+def rapid_weights(model: Model, grid: Grid, L: int, obs, chol):
+    """rapid.py:200-225 -- the per-observation part of build_setup (stencil indices, weights by
+    cho_solve against the K_N factor, conditional variances, on-node rows, clamp)."""
     obs = np.asarray(obs, dtype=float).reshape(-1, 2)
-    if obs.shape[0] == 0:
-        raise OracleDomainError("no observations")
-    chol, ridged = kn_factor(model, kn_matrix(model, grid, L), L)
     M1 = grid.total_dims[0]
     base, offs = stencils(grid, obs, L)
     idx = expand_indices(base, M1, L)
@@ -436,6 +434,16 @@ def rapid_setup(model: Model, grid: Grid, L: int, obs) -> Setup:
         w[node, (L - 1) * 2 * L + (L - 1)] = 1.0
         cv[node] = 0.0
     cv = np.where((cv < 0) & (cv > -1.0e-10 * model.sigma2), 0.0, cv)
+    return base, idx, w, cv
+
+
+def rapid_setup(model: Model, grid: Grid, L: int, obs) -> Setup:
+    """rapid.py:177-230."""
+    obs = np.asarray(obs, dtype=float).reshape(-1, 2)
+    if obs.shape[0] == 0:
+        raise OracleDomainError("no observations")
+    chol, ridged = kn_factor(model, kn_matrix(model, grid, L), L)
+    base, idx, w, cv = rapid_weights(model, grid, L, obs, chol)
     dims, spec = filter_spectrum(model, grid)
     return Setup(model, grid, L, chol, base, idx, w, cv, dims, spec, ridged)
 

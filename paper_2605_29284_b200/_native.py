@@ -65,6 +65,7 @@ _PROTOS = {
     "rk_predict_profile": (_i32, [_vp, _dp, _dp, _i32, _dp, _dp, _vp, C.POINTER(C.c_float * 4)]),
     "rk_predict_traffic": (_i32, [_vp, _i32, C.POINTER(C.c_double * 4)]),
     "rk_setup_time_weights": (_i32, [_vp, _vp, _i32, C.POINTER(C.c_float)]),
+    "rk_setup_weights_into": (_i32, [_vp, _dp, _dp, _dp, _dp, _vp]),
     "rk_fit_create": (_i32, [C.POINTER(RkModel), _dp, _i64, _dp, _dp, _i32, C.POINTER(_vp),
                              C.POINTER(_i32)]),
     "rk_fit_import": (_i32, [C.POINTER(RkModel), _dp, _i64, _dp, _i32, _dp, _dp, _dp,
@@ -81,9 +82,21 @@ _PROTOS = {
     "rk_setup_embedding": (_i32, [_vp, C.POINTER(_i32 * 2), C.POINTER(_i32)]),
     "rk_sim_unconditional_dev": (_i32, [_vp, _u64, _dp, _vp]),
     "rk_sim_obs_local_dev": (_i32, [_vp, C.c_double, _dp, _u64, _dp, _vp]),
-    "rk_ensemble_accumulate": (_i32, [_vp, _vp, _u64, _i64, _i64, _dp, _dp, _dp, _dp, _dp,
-                                      _i32, _vp]),
-    "rk_ensemble_finalize": (_i32, [_i64, _i64, _dp, _dp, _dp, _dp, _dp, _vp]),
+    "rk_ensemble_accumulate": (_i32, [_vp, _vp, _u64, _i64, _i64, _dp, _dp, _dp, _dp, _i32, _vp]),
+    "rk_ensemble_accumulate_values": (_i32, [_dp, _i32, _i64, C.c_double, _dp, _vp]),
+    "rk_ensemble_combine": (_i32, [_dp, _dp, _i64, _vp]),
+    "rk_ensemble_finalize": (_i32, [_i64, _i64, C.c_double, _dp, _dp, _dp, _dp, _vp]),
+    "rk_fit_prepare_refit": (_i32, [_vp, _vp]),
+    "rk_setup_replicate": (_i32, [_vp, _i32, C.POINTER(_vp)]),
+    "rk_fit_replicate": (_i32, [_vp, _i32, C.POINTER(_vp)]),
+    "rk_setup_blob_bytes": (_i32, [_vp, C.POINTER(_i64)]),
+    "rk_setup_export": (_i32, [_vp, _dp, _vp]),
+    "rk_setup_import": (_i32, [_dp, _i64, C.POINTER(_vp)]),
+    "rk_fit_shell": (_i32, [C.POINTER(RkModel), _i64, _i32, _i32, C.POINTER(_vp)]),
+    "rk_fit_fields": (_i32, [_vp, C.POINTER(_vp * 7), C.POINTER(_i64 * 7)]),
+    "rk_fit_get_gram": (_i32, [_vp, _dp, _dp]),
+    "rk_fit_set_gram": (_i32, [_vp, _dp, _dp]),
+    "rk_refit_profile": (_i32, [_vp, _i64, _i32, _vp, C.POINTER(C.c_float * 2)]),
 }
 
 _lock = threading.Lock()

@@ -8,7 +8,9 @@
 //   build_setup         rapid.py:177-230      -> rk_build_setup (weights_kernel + sort +
 //                                                spectrum_quarter)
 #include <algorithm>
+#include <atomic>
 #include <climits>
+#include <set>
 #include <cmath>
 #include <map>
 #include <memory>
@@ -26,7 +28,7 @@ namespace rk {
 namespace {
 thread_local std::string g_err;
 thread_local int g_code = RK_OK;
-thread_local int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};   // process-wide: ensemble shards launch from worker threads
 }  // namespace
 
 void set_error(int code, const std::string& msg) {
@@ -154,16 +156,20 @@ Status set_smem_attr(const void* fn, size_t bytes) {
 }
 
 Status scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
-  static bool pool_cfg = false;
-  if (!pool_cfg) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  static std::mutex mu;
+  static std::set<int> configured;   // per device: keep freed blocks cached in its pool
+  int dev = 0;
+  RK_CUDA_TRY(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!configured.count(dev)) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      configured.insert(dev);
     }
-    pool_cfg = true;
   }
   RK_CUDA_TRY(cudaMallocAsync(p, bytes ? bytes : 16, st));
   return Status::ok();
@@ -856,8 +862,10 @@ static Status build_sparse_gather(rk_setup* s) {
   return Status::ok();
 }
 
-static void free_setup(rk_setup* s) {
+void free_setup(rk_setup* s) {
   if (!s) return;
+  int cur = 0;
+  const bool swap = cudaGetDevice(&cur) == cudaSuccess && cur != s->device && cudaSetDevice(s->device) == cudaSuccess;
   free_workspaces(s);
   cudaFree(s->obs);
   cudaFree(s->base);
@@ -879,6 +887,7 @@ static void free_setup(rk_setup* s) {
   cudaFree(s->kn_chol_dev);
   cudaFree(s->emb.root_q);
   delete s;
+  if (swap) cudaSetDevice(cur);
 }
 
 // weights + stencil base + cond_var for every observation of the setup (rapid.py:202-225);
@@ -1099,7 +1108,7 @@ extern "C" {
 
 const char* rk_last_error(void) { return rk::g_err.c_str(); }
 int32_t rk_version(void) { return 1; }
-int64_t rk_launch_count(void) { return rk::g_launches; }
+int64_t rk_launch_count(void) { return rk::g_launches.load(); }
 
 rk_status rk_matern_cov(const rk_model* model, const double* d_dev, double* out_dev, int64_t n,
                         void* stream) {
@@ -1241,6 +1250,18 @@ rk_status rk_setup_time_weights(const rk_setup* s, void* stream, int32_t reps, f
     scratch_free(err, st);
     RK_CUDA_TRY(cudaStreamSynchronize(st));
     return Status::ok();
+  };
+  return (rk_status)finish(run());
+}
+
+// K1 of a predict step (SURVEY 8(d) T_predict = K1 + T_apply): stencil bases, weights and
+// conditional variances of the setup's observations, recomputed into caller device buffers
+// (base (n) int32, w (n, M), cv (n)) on `stream`; no host synchronisation
+rk_status rk_setup_weights_into(const rk_setup* s, int32_t* base_dev, double* w_dev, double* cv_dev,
+                                int32_t* err_dev, void* stream) {
+  auto run = [&]() -> Status {
+    if (!s || s->n <= 0) return Status::err(RK_DOMAIN, "weights need a setup with observations");
+    return launch_weights(s, base_dev, w_dev, cv_dev, err_dev, (cudaStream_t)stream);
   };
   return (rk_status)finish(run());
 }

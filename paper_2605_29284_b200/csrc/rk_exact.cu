@@ -173,37 +173,38 @@ static Status gls_trsm(const rk_fit* f, const double* Z, int64_t batch, double* 
 }
 
 
-// Batched refit (exact.py:108-113) with the precomputed inverse factor: two FP64
-// tensor-core GEMMs per batch instead of three triangular solves.
+// Batched refit (exact.py:108-113) with the precomputed inverse factor, on our own FP64
+// tensor-core kernels (rk_refit.cu) -- no cuBLAS on the ensemble path:
 //   A = L^-1 Z ; beta = (B'B)^-1 B'A ; H = A - B beta (= L^-1 (Z - X beta)) ; C = L^-T H
 Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C,
-                        cudaStream_t st) {
-  cublasHandle_t h;
-  RK_TRY(blas_for(const_cast<rk_fit*>(f), st, &h));
-  const int n = (int)f->n, p = f->p, nb = (int)batch;
-  const double one = 1.0, zero = 0.0;
-  RK_TRY(ensure_uinv(const_cast<rk_fit*>(f), st));
+                 cudaStream_t st) {
+  const int64_t n = f->n;
+  const int p = f->p;
+  if (!f->Uinv) return Status::err(RK_INTERNAL, "refit without the inverse factor (call ensure_uinv first)");
   double *A = nullptr, *H = nullptr;
-  RK_TRY(scratch_alloc((void**)&A, sizeof(double) * (size_t)n * nb, st));
-  RK_TRY(scratch_alloc((void**)&H, sizeof(double) * (size_t)n * nb, st));
-  // L^-1 = U^-T
-  RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, n, nb, n, &one, f->Uinv, n, Z, n, &zero, A, n));
-  RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, nb, n, &one, f->B, n, A, n, &zero, beta, p));
-  gram_solve_kernel<<<(nb + 127) / 128, 128, 0, st>>>(gram_args(f), beta, nb);
-  count_launch();
-  resid_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)n * nb, 256), 148 * 32), 256, 0, st>>>(
-      A, f->B, n, p, beta, nb, H);
+  RK_TRY(scratch_alloc((void**)&A, sizeof(double) * (size_t)n * batch, st));
+  RK_TRY(scratch_alloc((void**)&H, sizeof(double) * (size_t)n * batch, st));
+  RK_TRY(trmm_linv(f, false, Z, n, batch, A, n, st));
+  RK_TRY(bta(f, A, n, batch, beta, st));
+  for (int64_t b0 = 0; b0 < batch; b0 += 1 << 20) {
+    const int nb = (int)std::min<int64_t>(batch - b0, 1 << 20);
+    gram_solve_kernel<<<(nb + 127) / 128, 128, 0, st>>>(gram_args(f), beta + b0 * p, nb);
+    count_launch();
+  }
+  resid_kernel<<<(int)std::min<int64_t>(ceil_div(n * batch, 256), 148 * 32), 256, 0, st>>>(
+      A, f->B, n, p, beta, (int)batch, H);
   count_launch();
   RK_LAUNCH_CHECK();
-  // L^-T = U^-1
-  RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, n, nb, n, &one, f->Uinv, n, H, n, &zero, C, n));
+  RK_TRY(trmm_linv(f, true, H, n, batch, C, n, st));
   scratch_free(A, st);
   scratch_free(H, st);
   return Status::ok();
 }
 
-static void free_fit(rk_fit* f) {
+void free_fit(rk_fit* f) {
   if (!f) return;
+  int cur = 0;
+  const bool swap = cudaGetDevice(&cur) == cudaSuccess && cur != f->device && cudaSetDevice(f->device) == cudaSuccess;
   cudaFree(f->Uinv);
   cudaFree(f->obs);
   cudaFree(f->U);
@@ -214,6 +215,7 @@ static void free_fit(rk_fit* f) {
   if (f->cublas) cublasDestroy((cublasHandle_t)f->cublas);
   for (auto& kv : f->blas_by_stream) cublasDestroy((cublasHandle_t)kv.second);
   delete f;
+  if (swap) cudaSetDevice(cur);
 }
 
 // common tail: X upload, B = L^-1 X, gram LU
@@ -302,6 +304,7 @@ static Status inv_upper(cusolverDnHandle_t sh, cublasHandle_t bh, double* U, int
 }
 
 Status ensure_uinv(rk_fit* f, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(f->uinv_mu);   // concurrent first refits build it once
   if (f->Uinv) return Status::ok();
   const int64_t n = f->n;
   double* Ui = nullptr;
@@ -482,7 +485,15 @@ rk_status rk_fit_copy_out(const rk_fit* f, double* beta_host, double* c_host, do
 
 rk_status rk_refit_dev(const rk_fit* f, const double* z_dev, int64_t batch, double* beta_dev,
                        double* c_dev, void* stream) {
-  return (rk_status)finish_exact(gls_batch(f, z_dev, batch, beta_dev, c_dev, (cudaStream_t)stream));
+  auto run = [&]() -> Status {
+    RK_TRY(ensure_uinv(const_cast<rk_fit*>(f), (cudaStream_t)stream));
+    return gls_batch(f, z_dev, batch, beta_dev, c_dev, (cudaStream_t)stream);
+  };
+  return (rk_status)finish_exact(run());
+}
+
+rk_status rk_fit_prepare_refit(rk_fit* f, void* stream) {
+  return (rk_status)finish_exact(ensure_uinv(f, (cudaStream_t)stream));
 }
 
 }  // extern "C"
@@ -677,9 +688,6 @@ rk_status rk_kriging_se_exact(rk_fit* f, const double* targets_dev, int64_t nt, 
     unsigned long long zero_bits;
     memcpy(&zero_bits, &zero_d, sizeof zero_bits);
     RK_CUDA_TRY(cudaMemcpyAsync(minv, &zero_bits, sizeof zero_bits, cudaMemcpyHostToDevice, st));
-    cublasHandle_t h;
-    RK_TRY(blas_for(const_cast<rk_fit*>(f), st, &h));
-    const double one = 1.0, zer = 0.0;
     const GramLU g = gram_args(f);
     for (int64_t j0 = 0; j0 < nt; j0 += tc) {
       const int64_t m = std::min<int64_t>(tc, nt - j0);
@@ -687,14 +695,12 @@ rk_status rk_kriging_se_exact(rk_fit* f, const double* targets_dev, int64_t nt, 
           f->mat, f->obs, n, targets_dev + 2 * j0, m, K, bad);
       count_launch();
       RK_LAUNCH_CHECK();
-      // u = L^-1 K = (U^-1)' K
-      RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)n, (int)m, (int)n, &one, f->Uinv, (int)n, K,
-                                (int)n, &zer, U, (int)n));
+      // u = L^-1 K (DMMA triangular panel product, rk_refit.cu)
+      RK_TRY(trmm_linv(f, false, K, n, m, U, n, st));
       colsq_kernel<<<(unsigned)ceil_div(m, 8), 256, 0, st>>>(U, n, m, f->model.sigma2, var);
       count_launch();
-      // B'u (p x m)
-      RK_CUBLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, (int)m, (int)n, &one, f->B, (int)n, U, (int)n,
-                                &zer, BtU, p));
+      // B'u (p x m), fixed-order per target
+      RK_TRY(bta(f, U, n, m, BtU, st));
       se_finish_kernel<<<(unsigned)ceil_div(m, 128), 128, 0, st>>>(g, BtU, xt_dev ? xt_dev + j0 * p : nullptr, x00,
                                                                    m, var, out_dev + j0, minv);
       count_launch();

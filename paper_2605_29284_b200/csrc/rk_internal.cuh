@@ -158,9 +158,14 @@ struct rk_fit {
   void* cublas = nullptr;                    // handle of the creating thread / default stream
   std::mutex blas_mu;
   std::map<cudaStream_t, void*> blas_by_stream;   // one handle per stream (own workspace)
+  std::mutex uinv_mu;                             // serialises the lazy U^-1 build
 };
 
 namespace rk {
+
+// destructors (device-aware: free on the object's own device)
+void free_setup(rk_setup* s);
+void free_fit(rk_fit* f);
 
 // predict pipeline pieces (rk_predict.cu), used by the ensemble driver
 enum EpiMode { EPI_PLAIN = 0, EPI_SCALAR = 1, EPI_COV = 2 };
@@ -186,5 +191,10 @@ Status ensure_embedding(rk_setup* s, cudaStream_t st);
 // batched refit: Z (n x batch, column-major) -> beta (p x batch), C (n x batch)
 Status gls_batch(const rk_fit* f, const double* Z, int64_t batch, double* beta, double* C, cudaStream_t st);
 Status ensure_uinv(rk_fit* f, cudaStream_t st);   // U^-1 for the batched refits, built once
+// refit products with the inverse factor (rk_refit.cu): out = L^-1 X (trans = false) or
+// L^-T X (trans = true), X / out (n x S) column-major; rhs (S, p) = (B' A) per column
+Status trmm_linv(const rk_fit* f, bool trans, const double* X, int64_t ldx, int64_t S, double* out, int64_t ldo,
+                 cudaStream_t st);
+Status bta(const rk_fit* f, const double* A, int64_t lda, int64_t S, double* rhs, cudaStream_t st);
 
 }  // namespace rk

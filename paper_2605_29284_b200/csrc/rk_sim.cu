@@ -158,32 +158,91 @@ __global__ void obs_local_kernel(const ObsArgs a) {
   }
 }
 
-__global__ void accumulate_kernel(const double* __restrict__ E, int batch, int64_t npix,
-                                  const double* __restrict__ dp, double* s1, double* s2,
-                                  double* draws) {
+// ----------------------------------------------------- exact (order-free) ensemble moments
+// Per pixel, the moments s1 = sum e_j and s2 = sum e_j^2 of e_j = draw_j - data_pred are kept
+// as fixed-point INTEGERS: each term v (scaled by the power of two 2^-k nearest sigma, exact) is
+// converted to trunc(v 2^64) and added as three signed 42-bit digits into three int64 limbs.
+// Integer addition is associative, so the moments -- and mean / SE -- are bitwise the same
+// whatever the order, batching, chunking or GPU count (one all-reduce of int64 limbs combines
+// ranks), and they are the exactly rounded sums of the terms (the reference's two-pass
+// std(ddof=1), simulate.py:191-192, is matched to ~1e-16 instead of one-pass roundoff).
+// Range: |v| < 2^20 sigma per term and < 2^21 terms per limb (checked; RK_NUMERIC beyond).
+constexpr int kFxFrac = 64;
+constexpr double kFxMaxTerm = 1048576.0;   // 2^20
+
+__device__ __forceinline__ void fx_digits(double v, long long d[3]) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const int ex = (int)((bits >> 52) & 0x7ff);
+  unsigned long long m = bits & ((1ULL << 52) - 1);
+  if (ex) m |= 1ULL << 52;
+  const int sh = (ex ? ex : 1) - 1075 + kFxFrac;   // |v| 2^64 = m 2^sh
+  unsigned __int128 M = 0;
+  if (sh >= 0) M = (unsigned __int128)m << sh;       // sh <= 72 under the range check
+  else if (sh > -64) M = m >> (-sh);                  // truncation toward zero
+  const unsigned long long mask = (1ULL << 42) - 1;
+  long long d0 = (long long)((unsigned long long)M & mask);
+  long long d1 = (long long)((unsigned long long)(M >> 42) & mask);
+  long long d2 = (long long)(unsigned long long)(M >> 84);
+  if (bits >> 63) { d0 = -d0; d1 = -d1; d2 = -d2; }
+  d[0] = d0; d[1] = d1; d[2] = d2;
+}
+
+__global__ void accumulate_fx_kernel(const double* __restrict__ E, int batch, int64_t npix,
+                                     const double* __restrict__ dp, double inv_scale,
+                                     long long* __restrict__ acc, double* __restrict__ draws,
+                                     int* __restrict__ bad) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
        p += (int64_t)gridDim.x * blockDim.x) {
-    double a1 = s1[p], a2 = s2[p];
+    long long a[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) a[q] = acc[q * npix + p];
     const double d = dp[p];
+    bool oob = false;
     for (int b = 0; b < batch; ++b) {
       const double e = E[(int64_t)b * npix + p];
-      a1 += e;
-      a2 = fma(e, e, a2);
+      const double v = e * inv_scale;   // exact: a power of two
+      if (!(fabs(v) < kFxMaxTerm)) oob = true;   // also NaN / inf
+      long long t[3];
+      fx_digits(oob ? 0.0 : v, t);
+      a[0] += t[0]; a[1] += t[1]; a[2] += t[2];
+      fx_digits(oob ? 0.0 : v * v, t);
+      a[3] += t[0]; a[4] += t[1]; a[5] += t[2];
       if (draws) draws[(int64_t)b * npix + p] = d + e;
     }
-    s1[p] = a1;
-    s2[p] = a2;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) acc[q * npix + p] = a[q];
+    if (oob) atomicOr(bad, 1);
   }
 }
 
-__global__ void finalize_kernel(int64_t npix, double R, const double* dp, const double* s1,
-                                const double* s2, double* mean, double* se) {
+__global__ void acc_add_kernel(long long* __restrict__ dst, const long long* __restrict__ src, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
+__device__ __forceinline__ double fx_value(long long d0, long long d1, long long d2) {
+  const __int128 S = ((__int128)d2 << 84) + ((__int128)d1 << 42) + (__int128)d0;
+  const long long hi = (long long)(S >> 64);
+  const unsigned long long lo = (unsigned long long)S;
+  return fma((double)hi, 18446744073709551616.0, (double)lo) * 0x1.0p-64;
+}
+
+__global__ void finalize_fx_kernel(int64_t npix, double R, double scale, const double* dp,
+                                   const long long* __restrict__ acc, double* mean, double* se) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
        p += (int64_t)gridDim.x * blockDim.x) {
-    const double m = s1[p] / R;
+    const double s1 = fx_value(acc[p], acc[npix + p], acc[2 * npix + p]) * scale;
+    const double s2 = fx_value(acc[3 * npix + p], acc[4 * npix + p], acc[5 * npix + p]) * (scale * scale);
+    const double m = s1 / R;
     if (mean) mean[p] = dp[p] + m;
-    if (se) se[p] = sqrt(fmax((s2[p] - s1[p] * m) / (R - 1.0), 0.0));
+    if (se) se[p] = sqrt(fmax((s2 - s1 * m) / (R - 1.0), 0.0));
   }
+}
+
+// the power of two nearest sigma (exact rescaling of the moments)
+static double fx_scale(double sigma2) {
+  if (!(sigma2 > 0.0) || !std::isfinite(sigma2)) return 1.0;
+  return std::ldexp(1.0, (int)std::floor(0.5 * std::log2(sigma2)));
 }
 
 __global__ void root_q_kernel(const double* __restrict__ lam_q, int hs1, int qs2, double scale,
@@ -446,6 +505,8 @@ struct CsGenArgs {
   double2* V;
   int64_t ldV, V_bstride;
   int tw_off, q_off;         // smem offsets (double2 units): twiddles, tail queues
+  int qcap;                  // tail-queue entries per warp actually used (<= the kernel's QCAP;
+                             // smaller only to exercise the overflow path: RK_CS_QCAP)
 };
 
 // words w .. w+3 of the (fs, 0) Philox stream; two blocks when w is not block aligned
@@ -519,7 +580,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cs_rowgen_kernel(const CsGenArgs a
       }
       const int total = __shfl_sync(0xffffffffu, off, 31);
       off -= cnt;
-      if (total > QCAP) {   // queue overflow (never in practice): each lane evaluates its own
+      if (total > min(QCAP, a.qcap)) {   // queue overflow (rare): each lane evaluates its own
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           if (tmask >> q & 1) z[q] = ndtri_tail(uu[q]);
@@ -585,6 +646,8 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     ga.V = V;
     ga.ldV = ldV;
     ga.V_bstride = (int64_t)s->M1 * ldV;
+    static const int qcap_env = getenv("RK_CS_QCAP") ? atoi(getenv("RK_CS_QCAP")) : 1 << 30;
+    ga.qcap = std::max(0, qcap_env);
     const int warps = ga.lpc * ga.pl.nthr / 32;
     static const bool gen4 = !(getenv("RK_CS_GEN4") && atoi(getenv("RK_CS_GEN4")) == 0);
     const bool occ4 = gen4 && ga.pl.wide == 2 && ga.lpc == 1 && ga.pl.nthr <= 288;
@@ -761,31 +824,37 @@ rk_status rk_sim_obs_local_dev(const rk_setup* s, double tau2, const double* fie
 }
 
 rk_status rk_ensemble_accumulate(rk_setup* s, const rk_fit* f, uint64_t seed, int64_t j0, int64_t count,
-                                 const double* xg_dev, const double* data_pred_dev, double* s1_dev,
-                                 double* s2_dev, double* draws_dev, int32_t batch, void* stream) {
+                                 const double* xg_dev, const double* data_pred_dev, long long* acc_dev,
+                                 double* draws_dev, int32_t batch, void* stream) {
   auto run = [&]() -> Status {
     cudaStream_t st = (cudaStream_t)stream;
     if (f->n != s->n) return Status::err(RK_DOMAIN, "fit and setup disagree on the number of observations");
     if (!xg_dev && f->p != 1)
       return Status::err(RK_DOMAIN, "grid covariates are required when beta_hat has more than one entry");
+    if (count <= 0) return Status::ok();
+    if (count > (int64_t)1 << 21)
+      return Status::err(RK_DOMAIN, "at most 2^21 realizations per accumulator");
     RK_TRY(ensure_embedding(s, st));
-    // Realizations per field pass (B) are capped so the per-pass FFT scratch (Z, V, T, U, e)
-    // stays within ~8 GB (a 8748^2 torus needs ~1.2 GB of Z per realization).  The refit,
-    // whose cost is reading the n x n inverse factor twice, runs once per super-batch of up to
-    // `count` realizations: their unconditional fields are kept (up to ~16 GB) between the
-    // simulation passes and the prediction passes.
-    const double per_real = 16.0 * ((double)s->emb.ps1 * s->emb.ps2 + (double)s->M1 * s->emb.ps2 +
-                                    2.0 * s->H1 * s->M2) + 8.0 * (double)s->m1 * s->m2;
+    RK_TRY(ensure_uinv(const_cast<rk_fit*>(f), st));
+    // Realizations per field pass (B) are capped so the per-pass FFT scratch (V, T, U, e)
+    // stays within ~8 GB.  The refit, whose cost is reading the n x n inverse factor twice,
+    // runs once per super-batch of up to `count` realizations: their unconditional fields
+    // are kept (up to ~16 GB) between the simulation passes and the prediction passes.
+    const double per_real = 16.0 * ((double)s->M1 * s->emb.ps2 + 2.0 * s->H1 * s->M2) + 8.0 * (double)s->m1 * s->m2;
     const int B = std::max(1, std::min((int)batch, (int)(8.0e9 / per_real)));
     const int64_t gsz = (int64_t)s->M1 * s->M2;
     const int64_t S = std::max<int64_t>(B, std::min<int64_t>(count, (int64_t)(16.0e9 / (8.0 * gsz))));
     const int64_t npix = (int64_t)s->m1 * s->m2;
+    const double scale = fx_scale(f->model.sigma2);
     double *G = nullptr, *Z = nullptr, *C = nullptr, *BT = nullptr, *E = nullptr;
+    int* bad = nullptr;
     RK_TRY(scratch_alloc((void**)&G, sizeof(double) * (size_t)gsz * S, st));
     RK_TRY(scratch_alloc((void**)&Z, sizeof(double) * (size_t)s->n * S, st));
     RK_TRY(scratch_alloc((void**)&C, sizeof(double) * (size_t)s->n * S, st));
     RK_TRY(scratch_alloc((void**)&BT, sizeof(double) * (size_t)f->p * S, st));
     RK_TRY(scratch_alloc((void**)&E, sizeof(double) * (size_t)npix * B, st));
+    RK_TRY(scratch_alloc((void**)&bad, sizeof(int), st));
+    RK_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
     for (int64_t js = j0; js < j0 + count; js += S) {
       const int64_t sc = std::min<int64_t>(S, j0 + count - js);
       for (int64_t k = 0; k < sc; k += B) {   // unconditional fields + simulated observations
@@ -806,30 +875,72 @@ rk_status rk_ensemble_accumulate(rk_setup* s, const rk_fit* f, uint64_t seed, in
         pb.g = G + k * gsz;
         pb.out = E;
         RK_TRY(predict_batch(s, pb, st));
-        accumulate_kernel<<<(int)std::min<int64_t>(ceil_div(npix, 256), 148 * 16), 256, 0, st>>>(
-            E, bc, npix, data_pred_dev, s1_dev, s2_dev, draws_dev ? draws_dev + (js + k - j0) * npix : nullptr);
+        accumulate_fx_kernel<<<(int)std::min<int64_t>(ceil_div(npix, 256), 148 * 16), 256, 0, st>>>(
+            E, bc, npix, data_pred_dev, 1.0 / scale, acc_dev,
+            draws_dev ? draws_dev + (js + k - j0) * npix : nullptr, bad);
         count_launch();
         RK_LAUNCH_CHECK();
       }
     }
+    int hb = 0;
+    RK_CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
     scratch_free(G, st);
     scratch_free(Z, st);
     scratch_free(C, st);
     scratch_free(BT, st);
     scratch_free(E, st);
+    scratch_free(bad, st);
+    RK_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hb)
+      return Status::err(RK_NUMERIC, "conditional draw deviates from the data prediction by more than 2^20 sigma "
+                                     "(or is not finite)");
     return Status::ok();
   };
   return (rk_status)finish_sim(run());
 }
 
-rk_status rk_ensemble_finalize(int64_t n_pix, int64_t n_draws, const double* data_pred_dev,
-                               const double* s1_dev, const double* s2_dev, double* mean_dev,
-                               double* se_dev, void* stream) {
+// the fixed-point accumulation alone, on caller values: acc += moments of e_dev (count, n_pix)
+// (tests pin the integer arithmetic against exact host sums)
+rk_status rk_ensemble_accumulate_values(const double* e_dev, int32_t count, int64_t n_pix, double sigma2,
+                                        long long* acc_dev, void* stream) {
+  auto run = [&]() -> Status {
+    cudaStream_t st = (cudaStream_t)stream;
+    int* bad = nullptr;
+    RK_TRY(scratch_alloc((void**)&bad, sizeof(int), st));
+    RK_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    accumulate_fx_kernel<<<(int)std::min<int64_t>(ceil_div(n_pix, 256), 148 * 16), 256, 0, st>>>(
+        e_dev, count, n_pix, e_dev, 1.0 / fx_scale(sigma2), acc_dev, nullptr, bad);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    int hb = 0;
+    RK_CUDA_TRY(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    scratch_free(bad, st);
+    RK_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hb) return Status::err(RK_NUMERIC, "value outside the fixed-point range (>= 2^20 sigma or not finite)");
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_ensemble_combine(long long* dst_dev, const long long* src_dev, int64_t n_pix, void* stream) {
+  auto run = [&]() -> Status {
+    const int64_t n = 6 * n_pix;
+    acc_add_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+        dst_dev, src_dev, n);
+    count_launch();
+    RK_LAUNCH_CHECK();
+    return Status::ok();
+  };
+  return (rk_status)finish_sim(run());
+}
+
+rk_status rk_ensemble_finalize(int64_t n_pix, int64_t n_draws, double sigma2, const double* data_pred_dev,
+                               const long long* acc_dev, double* mean_dev, double* se_dev, void* stream) {
   auto run = [&]() -> Status {
     if (n_draws < 2) return Status::err(RK_DOMAIN, "need at least 2 draws, got " + std::to_string(n_draws));
-    finalize_kernel<<<(int)std::min<int64_t>(ceil_div(n_pix, 256), 148 * 16), 256, 0,
-                      (cudaStream_t)stream>>>(n_pix, (double)n_draws, data_pred_dev, s1_dev, s2_dev,
-                                              mean_dev, se_dev);
+    finalize_fx_kernel<<<(int)std::min<int64_t>(ceil_div(n_pix, 256), 148 * 16), 256, 0,
+                         (cudaStream_t)stream>>>(n_pix, (double)n_draws, fx_scale(sigma2), data_pred_dev, acc_dev,
+                                                 mean_dev, se_dev);
     count_launch();
     RK_LAUNCH_CHECK();
     return Status::ok();

@@ -37,7 +37,7 @@ class _FitHandle:
 class KrigingFit:
     """Device-resident fit; attribute names follow exact.py:40-56."""
 
-    def __init__(self, model, obs_locs, X, beta_hat, c, handle, chol_host=None):
+    def __init__(self, model, obs_locs, X, beta_hat, c, handle, chol_host=None, device=None):
         self.model = model
         self.obs_locs = obs_locs
         self.X = X
@@ -45,6 +45,25 @@ class KrigingFit:
         self.c = c
         self._h = handle
         self._chol = chol_host
+        self.device = D.torch().cuda.current_device() if device is None else int(device)
+        self._replicas = {}
+
+    def prepare_refit(self, stream=None):
+        """Build the inverse factor the batched refits use now (else on the first refit)."""
+        N.call("rk_fit_prepare_refit", self.handle, N.stream_ptr(stream))
+
+    def replica(self, device: int) -> "KrigingFit":
+        """This fit on another GPU of the process: every device array copied peer to peer
+        (bitwise), cached per device."""
+        device = int(device)
+        if device == self.device:
+            return self
+        if device not in self._replicas:
+            h = N.C.c_void_p()
+            N.call("rk_fit_replicate", self.handle, device, N.C.byref(h))
+            self._replicas[device] = KrigingFit(self.model, self.obs_locs, self.X, self.beta_hat, self.c,
+                                                _FitHandle(h), chol_host=self._chol, device=device)
+        return self._replicas[device]
 
     @property
     def handle(self):

@@ -92,7 +92,7 @@ class FilterSpectrum:
 class RapidSetup:
     """Immutable device-resident setup (reference rapid.py:138-174)."""
 
-    def __init__(self, model, grid, L, handle, ridge_applied=False):
+    def __init__(self, model, grid, L, handle, ridge_applied=False, device=None):
         self.model = model
         self.grid = grid
         self.L = int(L)
@@ -103,6 +103,21 @@ class RapidSetup:
         self.embed_dims = emb
         self._total = tot
         self._cache = {}
+        self.device = D.torch().cuda.current_device() if device is None else int(device)
+        self._replicas = {}
+
+    def replica(self, device: int) -> "RapidSetup":
+        """This setup on another GPU of the process: every device array (incl. the simulation
+        embedding, if built) copied peer to peer, bitwise; cached per device."""
+        device = int(device)
+        if device == self.device:
+            return self
+        if device not in self._replicas:
+            h = N.C.c_void_p()
+            N.call("rk_setup_replicate", self.handle, device, N.C.byref(h))
+            self._replicas[device] = RapidSetup(self.model, self.grid, self.L, _Handle(h), self.ridge_applied,
+                                                device=device)
+        return self._replicas[device]
 
     @property
     def handle(self):

@@ -7,11 +7,13 @@ counter) and inverse-CDF normals, so draws match the reference to roundoff.
 
 ``generate_ensemble`` runs realizations in batches through one fused device
 pipeline (rk_ensemble_accumulate): Philox+normal+sqrt(lambda) fused into the
-row IFFT pass, column IFFT, local observation simulation, batched GLS refit,
-the rapid predict passes with the draw epilogue, and in-order per-pixel moment
-accumulation.  Moments are kept per fixed chunk of realizations (independent
-of how many GPUs run them) and combined in chunk order, so the ensemble is
-bitwise identical on 1, 2, 4 or 8 GPUs (see distributed.py).
+row IFFT pass, column IFFT, local observation simulation, batched GLS refit
+(FP64 tensor cores), the rapid predict passes with the draw epilogue, and
+per-pixel moments accumulated as exact fixed-point integers.  Integer sums do
+not depend on order, so the ensemble is bitwise identical however the
+realizations are batched or split over GPUs -- within one process
+(``devices="all"``, setup and fit copied peer to peer) or over
+torch.distributed ranks (distributed.py, one int64 all-reduce).
 """
 
 from __future__ import annotations
@@ -27,10 +29,10 @@ from .exact import as_device_fit, refit_coefficients
 from .rapid import GRID_SETUPS, _fixed_inputs, predict_rapid
 
 __all__ = ["Ensemble", "RNG_ALGORITHM", "draw_seed", "std_normals", "sim_unconditional_grid", "sim_obs_local",
-           "conditional_draw", "generate_ensemble", "ensemble_chunks", "ENSEMBLE_CHUNKS"]
+           "conditional_draw", "generate_ensemble", "shard_ranges", "new_accumulator", "accumulate",
+           "combine", "finalize"]
 
 RNG_ALGORITHM = "philox4x64-10"
-ENSEMBLE_CHUNKS = 8
 _M64 = (1 << 64) - 1
 
 
@@ -121,11 +123,11 @@ def conditional_draw(krig, setup, seed: int, grid_covariates=None, data_predicti
     return draw.cpu().numpy()
 
 
-def ensemble_chunks(n_draws: int, n_chunks: int = ENSEMBLE_CHUNKS):
-    """Fixed chunk boundaries [j0, j1) of the realization index range."""
-    k = max(1, min(n_chunks, n_draws))
+def shard_ranges(n_draws: int, n_shards: int):
+    """Contiguous realization blocks [j0, j1) of ``n_shards`` workers (empty blocks dropped)."""
+    k = max(1, int(n_shards))
     b = [(i * n_draws) // k for i in range(k + 1)]
-    return [(b[i], b[i + 1]) for i in range(k) if b[i + 1] > b[i]]
+    return [(b[i], b[i + 1]) for i in range(k)]
 
 
 def _prepare(krig, setup, grid_covariates):
@@ -136,54 +138,119 @@ def _prepare(krig, setup, grid_covariates):
     return f, xd, dp
 
 
-def accumulate_chunk(setup, f, seed, j0, j1, xd, dp, draws=None, batch=32, stream=None):
-    """Per-chunk partial moments (s1, s2) of e_j = draw_j - data_pred, j in [j0, j1)."""
+def new_accumulator(setup):
+    """Exact fixed-point moment accumulator of one ensemble (int64, 6 x m2 x m1), zeroed."""
     m1, m2 = setup.grid.interior_dims
-    s1 = D.zeros((m2, m1))
-    s2 = D.zeros((m2, m1))
+    return D.zeros((6, m2, m1), dtype=D.torch().int64)
+
+
+def accumulate(setup, f, seed, j0, j1, xd, dp, acc, draws=None, batch=64, stream=None):
+    """Adds the moments of e_j = draw_j - data_pred, j in [j0, j1), into ``acc`` (exact
+    integer sums: the result does not depend on how the range is split or batched)."""
+    if j1 <= j0:
+        return acc
     N.call("rk_ensemble_accumulate", setup.handle, f.handle, int(seed) & _M64, int(j0), int(j1 - j0),
-           N.ptr(xd), N.ptr(dp), N.ptr(s1), N.ptr(s2), N.ptr(draws), int(batch),
-           N.stream_ptr(stream))
-    return s1, s2
+           N.ptr(xd), N.ptr(dp), N.ptr(acc), N.ptr(draws), int(batch), N.stream_ptr(stream))
+    return acc
 
 
-def combine_chunks(partials):
-    """Chunk partials summed in chunk order (deterministic, GPU-count independent)."""
-    s1 = partials[0][0].clone()
-    s2 = partials[0][1].clone()
-    for a, b in partials[1:]:
-        s1 += a
-        s2 += b
-    return s1, s2
+def combine(dst, src, stream=None):
+    """dst += src for two accumulators on the same device (exact)."""
+    N.call("rk_ensemble_combine", N.ptr(dst), N.ptr(src), dst.shape[1] * dst.shape[2], N.stream_ptr(stream))
+    return dst
 
 
-def finalize(dp, s1, s2, n_draws):
+def finalize(dp, acc, n_draws, sigma2):
     mean = D.empty(dp.shape)
     se = D.empty(dp.shape)
-    N.call("rk_ensemble_finalize", dp.numel(), int(n_draws), N.ptr(dp), N.ptr(s1), N.ptr(s2),
+    N.call("rk_ensemble_finalize", dp.numel(), int(n_draws), float(sigma2), N.ptr(dp), N.ptr(acc),
            N.ptr(mean), N.ptr(se), N.stream_ptr())
     return mean, se
 
 
+def _devices(devices):
+    """None: every visible GPU of this process -- unless torch.distributed runs one process per
+    GPU, where each rank keeps to its own (use distributed.generate_ensemble_sharded there)."""
+    torch = D.torch()
+    if devices is None:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            return [torch.cuda.current_device()]
+        cur = torch.cuda.current_device()
+        return [cur] + [d for d in range(torch.cuda.device_count()) if d != cur]
+    if devices == "all":
+        return list(range(torch.cuda.device_count()))
+    return [int(d) for d in devices]
+
+
+def _ensemble_multi(setup, f, seed, n_draws, xd, dp, devs, draws, batch):
+    """Realization blocks on several GPUs of this process (setup / fit replicated peer to peer),
+    one thread per GPU; accumulators summed exactly on the first GPU."""
+    import threading
+    torch = D.torch()
+    ranges = shard_ranges(n_draws, len(devs))
+    embedding_dims(setup.model, setup)   # simulation embedding and inverse factor built once,
+    f.prepare_refit()                    # then copied with the replicas
+    accs = [None] * len(devs)
+    errs = []
+
+    def work(i, d):
+        try:
+            with torch.cuda.device(d):
+                st = setup.replica(d)
+                fr = f.replica(d)
+                s = torch.cuda.Stream(d)
+                with torch.cuda.stream(s):
+                    x = None if xd is None else xd.to(d)
+                    p = dp.to(d)
+                    acc = new_accumulator(setup)
+                    j0, j1 = ranges[i]
+                    dv = None
+                    if draws is not None:
+                        dv = draws[j0:j1] if d == draws.device.index else torch.empty(
+                            (j1 - j0,) + tuple(dp.shape), dtype=torch.float64, device=d)
+                    accumulate(st, fr, seed, j0, j1, x, p, acc, dv, batch, stream=s)
+                    if draws is not None and dv.device != draws.device:
+                        draws[j0:j1].copy_(dv)
+                s.synchronize()
+                accs[i] = acc
+        except BaseException as e:   # re-raised on the calling thread
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i, d)) for i, d in enumerate(devs)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    total = accs[0] if accs[0].device == dp.device else accs[0].to(dp.device)
+    for a in accs[1:]:
+        combine(total, a.to(dp.device))
+    return total
+
+
 def generate_ensemble(krig, setup, n_draws: int, seed: int, grid_covariates=None, *,
-                      keep_draws: bool = True, batch: int = 32, device: bool = False):
+                      keep_draws: bool = True, batch: int = 64, device: bool = False, devices=None):
     """n_draws conditional draws; draw j uses sub-seed draw_seed(seed, j) (simulate.py:174-192).
 
-    ``keep_draws=False`` skips materialising the (n_draws, m2, m1) stack (the
-    reference always returns it; at 4096^2 x 256 it is 34 GB) — mean and SE
-    are accumulated on the fly either way.
+    ``devices``: None (every visible GPU of this process, the current one first; one GPU per
+    rank under torch.distributed), "all" or a list of device indices; realizations are split into contiguous blocks, one per GPU, and the moments
+    are combined exactly, so mean / SE are bitwise identical for any GPU count.
+    ``keep_draws=False`` skips materialising the (n_draws, m2, m1) stack (the reference always
+    returns it; at 4096^2 x 256 it is 34 GB) -- mean and SE are accumulated on the fly either way.
     """
     if n_draws < 2:
         raise DomainError(f"need at least 2 draws, got {n_draws}")
     f, xd, dp = _prepare(krig, setup, grid_covariates)
     m1, m2 = setup.grid.interior_dims
     draws = D.empty((n_draws, m2, m1)) if keep_draws else None
-    parts = []
-    for j0, j1 in ensemble_chunks(n_draws):
-        dv = None if draws is None else draws[j0:j1]
-        parts.append(accumulate_chunk(setup, f, seed, j0, j1, xd, dp, dv, batch))
-    s1, s2 = combine_chunks(parts)
-    mean, se = finalize(dp, s1, s2, n_draws)
+    devs = _devices(devices)
+    if len(devs) > 1:
+        acc = _ensemble_multi(setup, f, seed, n_draws, xd, dp, devs, draws, batch)
+    else:
+        acc = accumulate(setup, f, seed, 0, n_draws, xd, dp, new_accumulator(setup), draws, batch)
+    mean, se = finalize(dp, acc, n_draws, f.model.sigma2)
     if device:
         return Ensemble(draws, int(seed), int(n_draws), mean, se)
     return Ensemble(None if draws is None else draws.cpu().numpy(), int(seed), int(n_draws),

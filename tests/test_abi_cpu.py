@@ -73,16 +73,19 @@ def test_model_constants_match_reference_arithmetic():
         assert m.gamma_nu == math.gamma(nu)
 
 
-def test_next_fft_len_and_chunks():
+@pytest.mark.parametrize("n_draws", [2, 3, 7, 256, 1001, 1024])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8, 16])
+def test_next_fft_len_and_shards(n_draws, world):
     from paper_2605_29284_b200.rapid import next_fft_len
-    from paper_2605_29284_b200.simulate import ensemble_chunks
+    from paper_2605_29284_b200.simulate import shard_ranges
     g = load_golden("fft_len")
     assert [next_fft_len(int(k)) for k in g["n"]] == list(g["p"])
-    ch = ensemble_chunks(1024)
-    assert len(ch) == 8 and ch[0] == (0, 128) and ch[-1] == (896, 1024)
-    assert ensemble_chunks(3) == [(0, 1), (1, 2), (2, 3)]
-    flat = [j for a, b in ensemble_chunks(1001) for j in range(a, b)]
-    assert flat == list(range(1001))
+    sh = shard_ranges(n_draws, world)
+    assert len(sh) == world
+    flat = [j for a, b in sh for j in range(a, b)]
+    assert flat == list(range(n_draws))
+    sizes = [b - a for a, b in sh]
+    assert max(sizes) - min(sizes) <= 1
 
 
 def test_draw_seed_host():
