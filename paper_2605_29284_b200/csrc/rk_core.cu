@@ -87,6 +87,81 @@ Status plan_set(int n, PlanSet* out) {
   return Status::ok();
 }
 
+Status split_table(int P, SplitTw* out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, SplitTw> cache;
+  int dev = 0;
+  RK_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, P});
+  if (it != cache.end()) {
+    *out = it->second;
+    return Status::ok();
+  }
+  const int H = P / 2, nhi = (H + 127) / 128;
+  std::vector<double2> t(128 + nhi);
+  const long double PI_L = 3.141592653589793238462643383279502884L;
+  for (int i = 0; i < 128 + nhi; ++i) {
+    const long long e = i < 128 ? i : 128LL * (i - 128);
+    const long double ang = 2.0L * PI_L * (long double)e / (long double)P;
+    t[i] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+  }
+  double2* d = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&d, sizeof(double2) * t.size()));
+  RK_CUDA_TRY(cudaMemcpy(d, t.data(), sizeof(double2) * t.size(), cudaMemcpyHostToDevice));
+  SplitTw w;
+  w.lo = d;
+  w.hi = d + 128;
+  w.nhi = nhi;
+  cache[{dev, P}] = w;
+  *out = w;
+  return Status::ok();
+}
+
+// a length-P pass splits into two length-P/2 transforms when P is even and larger than the
+// lengths with WIDE plans (the half has one), see rk_predict.cu
+static bool split_len(int P) {
+  static const bool allow = !(getenv("RK_SPLIT") && atoi(getenv("RK_SPLIT")) == 0);
+  return allow && P % 2 == 0 && P > 4608 && P / 2 <= 4608;
+}
+
+Status setup_plans(rk_setup* s) {
+  RK_TRY(plan_for(s->p1, &s->pl1));
+  RK_TRY(plan_for(s->p2, &s->pl2));
+  RK_TRY(plan_set(s->p1, &s->pl1v));
+  RK_TRY(plan_set(s->p2, &s->pl2v));
+  s->h1v = PlanSet{};
+  s->h2v = PlanSet{};
+  if (split_len(s->p1) && s->M1 <= s->p1 / 2) {
+    RK_TRY(plan_set(s->p1 / 2, &s->h1v));
+    RK_TRY(split_table(s->p1, &s->sw1));
+  }
+  if (split_len(s->p2) && s->M2 <= s->p2 / 2) {
+    RK_TRY(plan_set(s->p2 / 2, &s->h2v));
+    RK_TRY(split_table(s->p2, &s->sw2));
+  }
+  return Status::ok();
+}
+
+Status embedding_plans(rk_setup* s) {
+  Embedding& e = s->emb;
+  RK_TRY(plan_for(e.ps1, &e.pl1));
+  RK_TRY(plan_for(e.ps2, &e.pl2));
+  RK_TRY(plan_set(e.ps1, &e.ps1v));
+  RK_TRY(plan_set(e.ps2, &e.ps2v));
+  e.hs1v = PlanSet{};
+  e.hs2v = PlanSet{};
+  if (split_len(e.ps1) && s->M1 <= e.ps1 / 2) {   // kept columns of the row pass < ps1 / 2
+    RK_TRY(plan_set(e.ps1 / 2, &e.hs1v));
+    RK_TRY(split_table(e.ps1, &e.sws1));
+  }
+  if (split_len(e.ps2) && s->M2 <= e.ps2 / 2) {   // kept rows of the column pass < ps2 / 2
+    RK_TRY(plan_set(e.ps2 / 2, &e.hs2v));
+    RK_TRY(split_table(e.ps2, &e.sws2));
+  }
+  return Status::ok();
+}
+
 const FftPlan& plan_pick(const PlanSet& ps, int64_t lines) {
   // RK_WIDE: 0 normal only, 1 auto, 2 spread, 3 wide, 4 split (where available)
   static const int mode = getenv("RK_WIDE") ? atoi(getenv("RK_WIDE")) : 1;
@@ -554,6 +629,202 @@ __global__ void __launch_bounds__(HELP ? 288 : 256, HELP ? 2 : 3) weights_kernel
   }
 }
 
+// M = 36 / 64 (L = 3 / 4), one lane per stencil entry: OB observations per warp, their
+// substitution chains interleaved step by step.  One observation's chain is a dependent
+// shuffle -> multiply -> FMA sequence (latency bound: ~15 % issue with one chain per warp);
+// OB independent chains per warp hide each other's latency, and each factor entry read from
+// shared memory serves all OB observations.  Per observation the operations and their order
+// are exactly those of weights_kernel_l (bitwise identical weights).
+template <int L, int OB>
+__global__ void __launch_bounds__(256, 2) weights_kernel_ob(WArgs a) {
+  constexpr int BS = 2 * L, M = BS * BS;
+  static_assert(M > 16, "sub-warp layouts use weights_kernel_l");
+  constexpr int MPL = (M + 31) / 32;
+  extern __shared__ double wsm[];
+  double* LF = wsm;                // LF[((c / 4) * M + r) * 4 + c % 4] = L[r][c]   (forward)
+  double* LB = wsm + M * M;        // LB[((c / 4) * M + r) * 4 + c % 4] = L[c][r]   (backward)
+  double* rd = wsm + 2 * M * M;    // 1 / L[c][c]
+  for (int e = threadIdx.x; e < M * M; e += blockDim.x) {
+    const int r = e / M, c = e % M;
+    const double v = a.chol[e];
+    LF[((c >> 2) * M + r) * 4 + (c & 3)] = v;
+    LB[((r >> 2) * M + c) * 4 + (r & 3)] = v;
+  }
+  for (int c = threadIdx.x; c < M; c += blockDim.x) rd[c] = 1.0 / a.chol[c * M + c];
+  const int sl = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  const int64_t nw = (a.n + OB - 1) / OB;
+  const int64_t stride = (int64_t)gridDim.x * wpb;
+  const int64_t trips = (nw + stride - 1) / stride;
+  const int jm4 = sl & 3;
+  for (int64_t it = 0; it < trips; ++it) {
+    const int64_t wi = (int64_t)blockIdx.x * wpb + warp + it * stride;
+    bool live[OB], on_node[OB];
+    int xlo[OB], ylo[OB];
+    double xs[OB], ys[OB];
+    double k[OB][MPL], v[OB][MPL];
+    int bad = 0;
+#pragma unroll
+    for (int o = 0; o < OB; ++o) {
+      const int64_t i = wi * OB + o;
+      live[o] = i < a.n;
+      const double x = live[o] ? a.obs[2 * i] : a.px0, y = live[o] ? a.obs[2 * i + 1] : a.py0;
+      xs[o] = x;
+      ys[o] = y;
+      const double tx = __ddiv_rn(__dsub_rn(x, a.px0), a.hx);
+      const double ty = __ddiv_rn(__dsub_rn(y, a.py0), a.hy);
+      int cx = 0, cy = 0;
+      if (live[o] && !(tx >= -1.0e-9 && tx <= a.hix && ty >= -1.0e-9 && ty <= a.hiy)) {
+        if (sl == 0) atomicMin(&a.err[0], (int)i);
+        live[o] = false;
+      }
+      if (live[o]) {
+        cx = snap_cell(tx);
+        cy = snap_cell(ty);
+        if (cx - (L - 1) < 0 || cy - (L - 1) < 0 || cx + L > a.M1 - 1 || cy + L > a.M2 - 1) {
+          if (sl == 0) atomicMin(&a.err[1], (int)i);
+          live[o] = false;
+        }
+      }
+      xlo[o] = cx - (L - 1);
+      ylo[o] = cy - (L - 1);
+      const double ox = __dsub_rn(tx, (double)cx), oy = __dsub_rn(ty, (double)cy);
+      on_node[o] = fabs(ox) <= 1.0e-9 && fabs(oy) <= 1.0e-9;
+    }
+#pragma unroll
+    for (int s = 0; s < MPL; ++s)
+#pragma unroll
+      for (int o = 0; o < OB; ++o) {
+        const int m = s * 32 + sl;
+        k[o][s] = 0.0;
+        if (live[o] && m < M) {
+          const int r = m / BS, q = m % BS;
+          const double nx = __dadd_rn(a.px0, __dmul_rn((double)(xlo[o] + q), a.hx));
+          const double ny = __dadd_rn(a.py0, __dmul_rn((double)(ylo[o] + r), a.hy));
+          const double dist = hypot(__dsub_rn(nx, xs[o]), __dsub_rn(ny, ys[o]));
+          k[o][s] = matern_cov(a.P, dist, &bad);
+        }
+        v[o][s] = k[o][s];
+      }
+    if (bad) atomicOr(&a.err[2], 1);
+    if (it == 0) __syncthreads();   // factor staged
+    // forward substitution L y = k, four columns per step (as weights_kernel_l)
+#pragma unroll
+    for (int s = 0; s < MPL; ++s) {
+      const int ncc = s == MPL - 1 ? M - s * 32 : 32;
+#pragma unroll 2
+      for (int cb = 0; cb < ncc; cb += 4) {
+        const int c0 = s * 32 + cb;
+        const double* B = LF + ((cb0(c0) * M + c0) * 4);
+        const double b4 = B[4], b8 = B[8], b9 = B[9], b12 = B[12], b13 = B[13], b14 = B[14];
+        const double r0 = rd[c0], r1 = rd[c0 + 1], r2 = rd[c0 + 2], r3 = rd[c0 + 3];
+        double y0[OB], y1[OB], y2[OB], y3[OB];
+#pragma unroll
+        for (int o = 0; o < OB; ++o) {
+          double x0 = __shfl_sync(0xffffffffu, v[o][s], cb), x1 = __shfl_sync(0xffffffffu, v[o][s], cb + 1);
+          double x2 = __shfl_sync(0xffffffffu, v[o][s], cb + 2), x3 = __shfl_sync(0xffffffffu, v[o][s], cb + 3);
+          y0[o] = x0 * r0;
+          x1 = fma(-b4, y0[o], x1);
+          y1[o] = x1 * r1;
+          x2 = fma(-b8, y0[o], x2);
+          x2 = fma(-b9, y1[o], x2);
+          y2[o] = x2 * r2;
+          x3 = fma(-b12, y0[o], x3);
+          x3 = fma(-b13, y1[o], x3);
+          x3 = fma(-b14, y2[o], x3);
+          y3[o] = x3 * r3;
+          const double ym = jm4 == 0 ? y0[o] : jm4 == 1 ? y1[o] : jm4 == 2 ? y2[o] : y3[o];
+          if ((sl >> 2) == (cb >> 2)) v[o][s] = ym;
+        }
+#pragma unroll
+        for (int s2 = s; s2 < MPL; ++s2) {
+          const int r = s2 * 32 + sl;
+          if (r > c0 + 3 && r < M) {
+            const double2* q = reinterpret_cast<const double2*>(LF + (cb0(c0) * M + r) * 4);
+            const double2 a01 = q[0], a23 = q[1];
+#pragma unroll
+            for (int o = 0; o < OB; ++o) {
+              v[o][s2] = fma(-a01.x, y0[o], v[o][s2]);
+              v[o][s2] = fma(-a01.y, y1[o], v[o][s2]);
+              v[o][s2] = fma(-a23.x, y2[o], v[o][s2]);
+              v[o][s2] = fma(-a23.y, y3[o], v[o][s2]);
+            }
+          }
+        }
+      }
+    }
+    // back substitution L' w = y
+#pragma unroll
+    for (int s = MPL - 1; s >= 0; --s) {
+      const int ncc = s == MPL - 1 ? M - s * 32 : 32;
+#pragma unroll 2
+      for (int cb = ncc - 4; cb >= 0; cb -= 4) {
+        const int c0 = s * 32 + cb;
+        const double* B = LF + ((cb0(c0) * M + c0) * 4);
+        const double b4 = B[4], b8 = B[8], b9 = B[9], b12 = B[12], b13 = B[13], b14 = B[14];
+        const double r0 = rd[c0], r1 = rd[c0 + 1], r2 = rd[c0 + 2], r3 = rd[c0 + 3];
+        double w0[OB], w1[OB], w2[OB], w3[OB];
+#pragma unroll
+        for (int o = 0; o < OB; ++o) {
+          double x0 = __shfl_sync(0xffffffffu, v[o][s], cb), x1 = __shfl_sync(0xffffffffu, v[o][s], cb + 1);
+          double x2 = __shfl_sync(0xffffffffu, v[o][s], cb + 2), x3 = __shfl_sync(0xffffffffu, v[o][s], cb + 3);
+          w3[o] = x3 * r3;
+          x2 = fma(-b14, w3[o], x2);
+          w2[o] = x2 * r2;
+          x1 = fma(-b13, w3[o], x1);
+          x1 = fma(-b9, w2[o], x1);
+          w1[o] = x1 * r1;
+          x0 = fma(-b12, w3[o], x0);
+          x0 = fma(-b8, w2[o], x0);
+          x0 = fma(-b4, w1[o], x0);
+          w0[o] = x0 * r0;
+          const double wm = jm4 == 0 ? w0[o] : jm4 == 1 ? w1[o] : jm4 == 2 ? w2[o] : w3[o];
+          if ((sl >> 2) == (cb >> 2)) v[o][s] = wm;
+        }
+#pragma unroll
+        for (int s2 = 0; s2 <= s; ++s2) {
+          const int r = s2 * 32 + sl;
+          if (r < c0) {
+            const double2* q = reinterpret_cast<const double2*>(LB + (cb0(c0) * M + r) * 4);
+            const double2 a01 = q[0], a23 = q[1];
+#pragma unroll
+            for (int o = 0; o < OB; ++o) {
+              v[o][s2] = fma(-a23.y, w3[o], v[o][s2]);
+              v[o][s2] = fma(-a23.x, w2[o], v[o][s2]);
+              v[o][s2] = fma(-a01.y, w1[o], v[o][s2]);
+              v[o][s2] = fma(-a01.x, w0[o], v[o][s2]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < OB; ++o) {
+      double part = 0.0;
+#pragma unroll
+      for (int s = 0; s < MPL; ++s) part = fma(v[o][s], k[o][s], part);
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+      if (!live[o]) continue;
+      const int64_t i = wi * OB + o;
+      double cv = a.P.sigma2 - part;
+      constexpr int corner = (L - 1) * BS + (L - 1);
+#pragma unroll
+      for (int s = 0; s < MPL; ++s) {
+        const int m = s * 32 + sl;
+        if (m < M) a.weights[i * M + m] = on_node[o] ? (m == corner ? 1.0 : 0.0) : v[o][s];
+      }
+      if (on_node[o]) cv = 0.0;
+      if (cv < 0.0 && cv > -1.0e-10 * a.P.sigma2) cv = 0.0;
+      if (sl == 0) {
+        a.cond_var[i] = cv;
+        a.base[i] = ylo[o] * a.M1 + xlo[o];
+      }
+    }
+  }
+}
+
 // cell_start[b] = lower_bound(sorted keys, b) for b in [0, nb]
 __global__ void cell_start_kernel(const int32_t* __restrict__ keys, int64_t n, int32_t* cs,
                                   int64_t nb) {
@@ -935,8 +1206,21 @@ static Status launch_weights(const rk_setup* s, int32_t* base, double* weights, 
       kern<<<wbl, help ? 288 : 256, wsl, st>>>(wa);
       return Status::ok();
     };
+    // RK_WEIGHTS_OB: observations per warp of the interleaved kernel for L = 3 / 4 (0 = the
+    // one-observation kernels)
+    static const int ob = getenv("RK_WEIGHTS_OB") ? atoi(getenv("RK_WEIGHTS_OB")) : 4;
+    auto launch_ob = [&](auto kern, int obs_per_warp) -> Status {
+      RK_TRY(set_smem_attr((const void*)kern, wsl));
+      const int nb = (int)std::min<int64_t>(ceil_div(ceil_div(n, obs_per_warp), 8), 148 * 2);
+      kern<<<nb, 256, wsl, st>>>(wa);
+      return Status::ok();
+    };
     if (L == 1) RK_TRY(launch_l(weights_kernel_l<1>));
     else if (L == 2) RK_TRY(launch_l(weights_kernel_l<2>));
+    else if (L >= 3 && ob >= 2) {
+      if (L == 3) RK_TRY(ob >= 4 ? launch_ob(weights_kernel_ob<3, 4>, 4) : launch_ob(weights_kernel_ob<3, 2>, 2));
+      else RK_TRY(ob >= 4 ? launch_ob(weights_kernel_ob<4, 4>, 4) : launch_ob(weights_kernel_ob<4, 2>, 2));
+    }
     else if (L == 3 && help) RK_TRY(launch_l(weights_kernel_l<3, true>));
     else if (L == 3) RK_TRY(launch_l(weights_kernel_l<3>));
     else RK_TRY(launch_l(weights_kernel_l<4>));
@@ -1088,10 +1372,7 @@ spectrum:
   s->p2 = (int)next_fft_len(2 * (int64_t)s->M2 - 1);
   s->H1 = s->p1 / 2 + 1;
   s->Q2 = quarter_ld(s->p2);
-  RK_TRY(plan_for(s->p1, &s->pl1));
-  RK_TRY(plan_for(s->p2, &s->pl2));
-  RK_TRY(plan_set(s->p1, &s->pl1v));
-  RK_TRY(plan_set(s->p2, &s->pl2v));
+  RK_TRY(setup_plans(s));
   RK_CUDA_TRY(cudaMalloc(&s->spec_q, sizeof(double) * (size_t)s->H1 * s->Q2));
   RK_TRY(spectrum_quarter(s->mat, grid->hx, grid->hy, s->p1, s->p2,
                           1.0 / ((double)s->p1 * (double)s->p2), s->spec_q, s->Q2, 0));

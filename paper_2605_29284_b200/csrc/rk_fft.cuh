@@ -246,9 +246,17 @@ __device__ __forceinline__ int mod_magic(int j, int Ns, uint32_t m) {
   return Ns == 1 ? 0 : m == 0 ? j % Ns : j - Ns * (int)__umulhi((uint32_t)j, m);
 }
 
+// Barrier of the threads working on one line: the whole CTA (id 0) or, when a CTA holds several
+// independent lines, a named barrier per line (id 1 + line, count = the line's threads) so the
+// lines' stages drift apart and one line's arithmetic overlaps another's shared-memory phases.
+__device__ __forceinline__ void group_sync(int id, int count) {
+  if (id == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 template <int R, bool INV, bool TWS = false, bool WIDE = false>
 __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
-                                          const double2* __restrict__ tw, uint32_t nsm) {
+                                          const double2* __restrict__ tw, uint32_t nsm, int bid = 0) {
   constexpr int K = WIDE ? fft_kmax_wide(R) : fft_kmax(R);
   const int nb = n / R;
   double2 a[K][R];
@@ -280,7 +288,7 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
       outb[q] = (j - jm) * R + jm;
     }
   }
-  __syncthreads();
+  group_sync(bid, nthr);
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     if (outb[q] >= 0) {
@@ -288,7 +296,7 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
       for (int k = 0; k < R; ++k) buf[outb[q] + k * Ns] = a[q][k];
     }
   }
-  __syncthreads();
+  group_sync(bid, nthr);
 }
 
 // Radix-9 stage with each butterfly split over three lanes (the 3 x 3 form of Dft<9>): lane r
@@ -300,8 +308,8 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
 // what changes is the serial FP64 work per thread (~72 instead of ~148 instructions), which
 // is what a radix-9 stage of a latency-bound line waits on.
 template <bool INV, bool TWS>
-__device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int n, int Ns, int t,
-                                                 const double2* __restrict__ tw, uint32_t nsm) {
+__device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
+                                                 const double2* __restrict__ tw, uint32_t nsm, int bid = 0) {
   const double C1 = 7.66044443118978013452e-01, S1 = 6.42787609686539362919e-01;
   const double C2 = 1.73648177666930358942e-01, S2 = 9.84807753012208020316e-01;
   const double C4 = -9.39692620785908427905e-01, S4 = 3.42020143325668712908e-01;
@@ -355,21 +363,21 @@ __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int 
     else d2 = got;
   }
   if (valid) dft3<INV>(d0, d1, d2);
-  __syncthreads();
+  group_sync(bid, nthr);
   if (valid) {
     const int ob = (j - jm) * 9 + jm;
     buf[ob + r * Ns] = d0;
     buf[ob + (r + 3) * Ns] = d1;
     buf[ob + (r + 6) * Ns] = d2;
   }
-  __syncthreads();
+  group_sync(bid, nthr);
 }
 
 // Full transform of the line at `buf` by thread t (0 <= t < pl.nthr or idle beyond).
 // Must be called by every thread of the CTA (contains barriers).  FM (FFT mode): 0 normal /
 // spread plans, 1 WIDE (64-register kernels), 2 split radix-9 stages.
 template <bool INV, bool TWS = false, int FM = 0, bool MAG = true>   // MAG: magic-divisor modulo
-__device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t) {
+__device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t, int bid = 0) {
   constexpr bool WIDE = FM >= 1;   // split plans also keep the small register footprint elsewhere
   const int n = pl.n, nthr = pl.nthr;
   const double2* tw = pl.tw;   // stage 1 (Ns = 1) needs no twiddles and has no block
@@ -377,36 +385,36 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
   int Ns = 1, si = 0;   // si: stage index (magic divisors)
 #pragma unroll 1
   for (int s = 0; s < pl.n9; ++s) {
-    if (FM == 2) fft_stage9_split<INV, TWS>(buf, n, Ns, t, tw, MAG ? mg[si] : 0u);
-    else fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
+    if (FM == 2) fft_stage9_split<INV, TWS>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
+    else fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     if (Ns > 1) tw += Ns;
     Ns *= 9;
     ++si;
   }
   if (pl.r3 == 6) {
-    fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
+    fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     if (Ns > 1) tw += Ns;
     Ns *= 6;
     ++si;
   } else if (pl.r3 == 3) {
-    fft_stage<3, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
+    fft_stage<3, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     if (Ns > 1) tw += Ns;
     Ns *= 3;
     ++si;
   }
 #pragma unroll 1
   for (int s = 0; s < pl.n8; ++s) {
-    fft_stage<8, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
+    fft_stage<8, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     if (Ns > 1) tw += Ns;
     Ns *= 8;
     ++si;
   }
   if (pl.r2 == 2) {
-    fft_stage<2, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
+    fft_stage<2, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
   } else if (pl.r2 >= 4) {
 #pragma unroll 1
     for (int s = 0; s < (pl.r2 == 16 ? 2 : 1); ++s) {
-      fft_stage<4, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u);
+      fft_stage<4, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
       if (Ns > 1) tw += Ns;
       Ns *= 4;
       ++si;

@@ -19,6 +19,21 @@ Status plan_for(int n, FftPlan* out, int wide = 0);   // cached per (device, n, 
 struct PlanSet {
   FftPlan v[4] = {};
 };
+// w_P^n = hi[n >> 7] * lo[n & 127] for 0 <= n < P / 2 (split-length passes, rk_predict.cu)
+struct SplitTw {
+  const double2* lo = nullptr;   // 128 entries
+  const double2* hi = nullptr;   // nhi entries
+  int nhi = 0;
+  int off = 0;                   // smem offset (double2 units) where a kernel stages them
+};
+Status split_table(int P, SplitTw* out);   // cached per (device, P)
+__device__ __forceinline__ const double2* stage_split_tw(const SplitTw& t, double2* dst) {
+  for (int i = threadIdx.x; i < 128 + t.nhi; i += blockDim.x) dst[i] = i < 128 ? __ldg(&t.lo[i]) : __ldg(&t.hi[i - 128]);
+  return dst;
+}
+__device__ __forceinline__ double2 split_w(const double2* tw, int n) {   // w_P^n (staged tables)
+  return cmul(tw[128 + (n >> 7)], tw[n & 127]);
+}
 Status plan_set(int n, PlanSet* out);
 // spread while the launch's CTAs are all resident at once (latency-bound small grids), else
 // wide (64-register kernels, twice the resident warps), else normal
@@ -39,6 +54,8 @@ struct Embedding {
   int hs1 = 0, qs2 = 0;          // ps1/2+1, ps2/2+1
   FftPlan pl1{}, pl2{};
   PlanSet ps1v, ps2v;            // all plan variants of ps1 / ps2
+  PlanSet hs1v, hs2v;            // half-length plans of split-length passes (n = 0 if unused)
+  SplitTw sws1, sws2;            // w_P^n tables for P = ps1, ps2
   double* root_q = nullptr;      // (qs2, hs1) row-major: sqrt(clip(lambda,0)) * sqrt(P)/P
 };
 
@@ -103,6 +120,8 @@ struct rk_setup {
   int p1 = 0, p2 = 0, H1 = 0, Q2 = 0;
   rk::FftPlan pl1{}, pl2{};
   rk::PlanSet pl1v, pl2v;       // all plan variants of p1 / p2, see plan_pick
+  rk::PlanSet h1v, h2v;         // plan variants of p1 / 2, p2 / 2 (split-length passes; n = 0 if unused)
+  rk::SplitTw sw1, sw2;         // w_P^n tables for P = p1, p2
   // device arrays
   double* obs = nullptr;        // (n, 2)
   int32_t* base = nullptr;      // (n) flat padded index of block entry 0
@@ -162,6 +181,12 @@ struct rk_fit {
 };
 
 namespace rk {
+
+// all FFT plans of a setup from its p1 / p2: full lengths, half lengths + w_P tables where a
+// split-length pass applies (rk_core.cu)
+Status setup_plans(rk_setup* s);
+// the embedding's plans from its ps1 / ps2 (same rules)
+Status embedding_plans(rk_setup* s);
 
 // destructors (device-aware: free on the object's own device)
 void free_setup(rk_setup* s);

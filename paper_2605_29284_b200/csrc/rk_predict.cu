@@ -104,6 +104,7 @@ struct RowFwdArgs {
   int64_t pblk_stride;       // fetched per line into smem at pl_off (double2 units)
   int pblk_cap, pl_off;
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
+  SplitTw sw;                // split-length kernels: w_P^n tables (staged at sw.off)
 };
 
 // FFT kernels: WIDE instantiations run 64-register threads (fft_kmax_wide butterflies each)
@@ -296,7 +297,8 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
   const FftPlan pls = TWS ? twiddles_commit(a.pl, twp, smem + a.tw_off) : a.pl;
   __syncthreads();
   RK_PHASE(0, 2);
-  fft_line<false, TWS, FM>(buf, pls, tl);
+  fft_line<false, TWS, FM>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+  if (a.lpc > 1) __syncthreads();   // the split below reads every line
   RK_PHASE(0, 3);
   pdl_trigger();   // the column pass may start staging while the split rows are stored
   // split Z = FFT(u + i v) into U = (Z + conj Z[-k]) / 2, V = (Z - conj Z[-k]) / 2i
@@ -335,6 +337,7 @@ struct ColArgs {
   double* out_q;             // spectrum mode: out_q[kx * ldq + ky] = Re * scale, ky <= p2/2
   double scale;
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
+  SplitTw sw;                // split-length kernel: w_P^n tables
 };
 
 template <int MODE, bool TWS, int FM>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
@@ -379,13 +382,13 @@ __global__ void RK_FFT_BOUNDS(FM) col_kernel(const ColArgs a) {
   mbar_wait(bar, 0);
   __syncthreads();
   RK_PHASE(1, 1);
-  fft_line<false, TWS, FM>(buf, pls, tl);
+  fft_line<false, TWS, FM>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
   RK_PHASE(1, 2);
   if (MODE == 0) {
     const double* S = specs + (size_t)line * a.ldq;
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
-    __syncthreads();
-    fft_line<true, TWS, FM>(buf, pls, tl);
+    group_sync(a.lpc > 1 ? 1 + line : 0, nthr);
+    fft_line<true, TWS, FM>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
     RK_PHASE(1, 3);
     pdl_trigger();
     // TMA bulk store of the kept rows
@@ -430,6 +433,7 @@ struct RowInvArgs {
   int ep_off;                // smem offset (double2 units) of the prefetched epilogue operands
   int ep_smem;               // 1: epilogue operands prefetched to smem, 0: read from global
   int xg_bulk;               // X_g is 16-byte aligned: one TMA bulk copy per CTA
+  SplitTw sw;                // split-length kernel: w_P^n tables
 };
 
 template <bool TWS, int FM>
@@ -516,7 +520,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
   __syncthreads();
   RK_PHASE(2, 2);
   double2* buf = smem + (size_t)line * n;
-  fft_line<true, TWS, FM>(buf, pls, tl);
+  fft_line<true, TWS, FM>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
   if (xwait) mbar_wait(bar, 0);   // init is ordered by the barrier above
   RK_PHASE(2, 3);
   const int ya = 2 * (blockIdx.x * a.lpc + line);
@@ -542,6 +546,263 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
     out[(int64_t)y * a.ldo + x] = v;
   }
   RK_PHASE(2, 4);
+}
+
+// ----------------------------------------------------------------- split-length passes
+// For a transform length P = 2H whose input is zero beyond H (the M nonzero rows / columns of
+// the padded grid: P >= 2M - 1 and P even give M <= H) and whose kept outputs lie below H (the
+// interior), one length-P transform is two independent length-H transforms:
+//   X[2m] = F_H(x)[m],  X[2m+1] = F_H(x w_P^n)[m]                     (forward, x[n >= H] = 0)
+//   y[n]  = F_H^-1(Y_e)[n] + w_P^-n F_H^-1(Y_o)[n],  n < H            (inverse, Y_e[m] = Y[2m])
+// (w_P = exp(-2 pi i / P), transforms unnormalised).  For the large tori (8748 = 2 x 4374) the
+// half length has a WIDE plan (64-register kernels, 1024 FFT threads per SM) and a twiddle
+// table that fits in shared memory next to the lines; the full length has neither.  The
+// w_P^n factors come from two staged tables, w_P^n = hi[n / 128] lo[n % 128] (one complex
+// product), built on the host in long double.
+
+// pass 1, sparse gather: row pair -> even / odd half lines -> T rows kx (kx parity = half)
+__global__ void __launch_bounds__(kFftWideThreads, 1) row_fwd_split_kernel(const RowFwdArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int H = a.pl.n, P = 2 * H;
+  const int nthr = a.pl.nthr;
+  const int line = threadIdx.x / nthr;
+  const int tl = threadIdx.x - line * nthr;
+  const int pl_ = line >> 1, half = line & 1;
+  const int t2 = tl + half * nthr, n2 = 2 * nthr;   // the pair's threads
+  const int b = blockIdx.y;
+  double2* be = smem + (size_t)(2 * pl_) * H;
+  double2* bo = be + H;
+  double2* buf = half ? bo : be;
+  const int pidx = blockIdx.x * a.lpc + pl_;
+  const int ya = 2 * pidx;
+  const bool va = ya < a.nrows;
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
+  pdl_wait();
+  const SparseSrc& g = a.sp;
+  const double* __restrict__ cb = g.c + (int64_t)b * g.c_stride;
+  double* __restrict__ prod = (double*)(smem + a.prod_off) + (size_t)pl_ * 2 * a.prod_cap;
+  int2* __restrict__ nrec = (int2*)(prod + a.prod_cap);
+  for (int x = tl; x < H; x += nthr) buf[x] = make_double2(0.0, 0.0);
+  int4 P0 = make_int4(0, 0, 0, 0), P1 = P0;
+  if (va) {
+    P0 = __ldg(&g.pair_info[pidx]);
+    P1 = __ldg(&g.pair_info[pidx + 1]);
+  }
+  const int n0 = P0.x, n1 = P0.y, e0 = P0.z;
+  const int nn = P1.x - n0;
+  const int cnt = P1.z - e0;
+  const int rowq = ya * g.M1;
+  constexpr int U = 4;
+  const int m = max(cnt, nn);
+  for (int i0 = t2; i0 < m; i0 += U * n2) {
+    double w[U];
+    int ci[U], nq[U], ne[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * n2;
+      w[u] = i < cnt ? __ldg(&g.ent_wv[e0 + i]) : 0.0;
+      ci[u] = i < cnt ? __ldg(&g.ent_c[e0 + i]) : 0;
+      nq[u] = i < nn ? __ldg(&g.node_q[n0 + i]) : 0;
+      ne[u] = i < nn ? __ldg(&g.node_off[n0 + i + 1]) : 0;
+    }
+    double cv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cv[u] = i0 + u * n2 < cnt ? __ldg(&cb[ci[u]]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * n2;
+      if (i < cnt) prod[i] = __dmul_rn(w[u], cv[u]);
+      if (i < nn) {
+        const int odd = n0 + i >= n1;
+        nrec[i] = make_int2(ne[u] - e0, 2 * (nq[u] - rowq - odd * g.M1) + odd);
+      }
+    }
+  }
+  __syncthreads();
+  double* bd = (double*)be;
+  for (int k = t2; k < nn; k += n2) {
+    const int s0 = k ? nrec[k - 1].x : 0;
+    const int2 r = nrec[k];
+    double acc = 0.0;
+    for (int i = s0; i < r.x; ++i) acc = __dadd_rn(acc, prod[i]);   // (w * c) then add, as np.add.at
+    bd[r.y] = acc;
+  }
+  __syncthreads();
+  if (half)
+    for (int x = tl; x < a.ncols; x += nthr) bo[x] = cmul(be[x], split_w(wt, x));
+  __syncthreads();
+  fft_line<false, true, 1>(buf, pls, tl, 1 + (threadIdx.x / nthr));
+  __syncthreads();   // both halves
+  pdl_trigger();
+  // Z[k] of the full transform: k even -> be[k / 2], k odd -> bo[(k - 1) / 2]; U / V split as
+  // in row_fwd_kernel with conj Z[P - k] from the same half
+  const int nr = 2 * a.lpc;
+  const int Hf = H + 1;
+  double2* T = a.T + (int64_t)b * a.T_bstride;
+  for (int idx = threadIdx.x; idx < Hf * nr; idx += blockDim.x) {
+    const int r = idx % nr, kx = idx / nr;
+    const int l = r >> 1;
+    const int row = 2 * (blockIdx.x * a.lpc + l) + (r & 1);
+    if (row >= a.nrows) continue;
+    const double2* le = smem + (size_t)(2 * l) * H;
+    double2 z, zc;
+    if ((kx & 1) == 0) {
+      const int mm = kx >> 1;
+      z = le[mm];
+      zc = le[mm ? H - mm : 0];
+    } else {
+      const int mm = (kx - 1) >> 1;
+      z = le[H + mm];
+      zc = le[H + (H - 1 - mm)];
+    }
+    double2 o;
+    if ((r & 1) == 0) o = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+    else o = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+    T[(int64_t)kx * a.ldT + row] = o;
+  }
+  (void)P;
+}
+
+// pass 2: column kx -> even / odd halves -> x real-even spectrum -> inverse halves -> combine
+// the kept rows -> TMA bulk store
+__global__ void __launch_bounds__(kFftWideThreads, 1) col_split_kernel(const ColArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int H = a.pl.n, P = 2 * H;
+  const int nthr = a.pl.nthr;
+  const int half = threadIdx.x / nthr;
+  const int tl = threadIdx.x - half * nthr;
+  const int b = blockIdx.y;
+  const int kx = blockIdx.x;
+  double2* be = smem;
+  double2* bo = smem + H;
+  double2* buf = half ? bo : be;
+  double* specs = (double*)(smem + 2 * (size_t)H);
+  uint64_t* bar = (uint64_t*)(specs + a.ldq);
+  const double2* Tb = a.T + (int64_t)b * a.T_bstride;
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  const uint32_t colb = (uint32_t)a.nin * 16u, specb = (uint32_t)a.ldq * 8u;
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(bar, colb + specb);
+    bulk_g2s(specs, a.spec_q + (int64_t)kx * a.ldq, specb, bar);
+  }
+  pdl_wait();
+  if (threadIdx.x == 0) bulk_g2s(be, Tb + (int64_t)kx * a.ldT, colb, bar);
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
+  for (int y = a.nin + tl; y < H; y += nthr) buf[y] = make_double2(0.0, 0.0);
+  mbar_wait(bar, 0);
+  __syncthreads();   // staged twiddle tables visible
+  if (half)
+    for (int y = tl; y < a.nin; y += nthr) bo[y] = cmul(be[y], split_w(wt, y));
+  __syncthreads();
+  fft_line<false, true, 1>(buf, pls, tl, 1 + (threadIdx.x / nthr));
+  // spectrum: S[k] = specs[min(k, P - k)], k = 2m + half
+  for (int mm = tl; mm < H; mm += nthr) {
+    const int k = 2 * mm + half;
+    buf[mm] = cscale(buf[mm], specs[min(k, P - k)]);
+  }
+  group_sync(1 + half, nthr);
+  fft_line<true, true, 1>(buf, pls, tl, 1 + (threadIdx.x / nthr));
+  __syncthreads();   // both halves
+  pdl_trigger();
+  for (int y = a.row0 + threadIdx.x; y < a.row0 + a.nout; y += blockDim.x) {
+    const double2 w = split_w(wt, y);
+    be[y] = cadd(be[y], cmulc(bo[y], w));   // + w^-y (inverse half)
+  }
+  fence_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bulk_s2g(a.U + (int64_t)b * a.U_bstride + (int64_t)kx * a.ldU, be + a.row0, (uint32_t)a.nout * 16u);
+    bulk_commit();
+    bulk_wait_read0();
+  }
+  __syncthreads();
+}
+
+// pass 3: Hermitian pair of interior rows -> even / odd half spectra -> inverse halves ->
+// combine the kept columns -> fixed-part / draw epilogue
+__global__ void __launch_bounds__(kFftWideThreads, 1) row_inv_split_kernel(const RowInvArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int H = a.pl.n;
+  const int nthr = a.pl.nthr;
+  const int line = threadIdx.x / nthr;
+  const int tl = threadIdx.x - line * nthr;
+  const int pl_ = line >> 1, half = line & 1;
+  const int t2 = tl + half * nthr, n2 = 2 * nthr;
+  const int b = blockIdx.y;
+  const int Hf = H + 1;
+  const double2* U = a.U + (int64_t)b * a.U_bstride;
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
+  pdl_wait();
+  // gather: Z[k] = A[k] + i B[k] (k < Hf) and its Hermitian mirror Z[P - k]; even k -> be, odd -> bo
+  const int tot = a.lpc * Hf;
+  constexpr int D = 8;
+  for (int base = threadIdx.x; base < tot; base += D * blockDim.x) {
+    double2 A[D], B[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int idx = base + d * blockDim.x;
+      A[d] = B[d] = make_double2(0.0, 0.0);
+      if (idx < tot) {
+        const int l = idx % a.lpc, k = idx / a.lpc;
+        const int ya = 2 * (blockIdx.x * a.lpc + l);
+        const double2* u = U + (int64_t)k * a.ldU + ya;
+        if (ya < a.nrows) A[d] = u[0];
+        if (ya + 1 < a.nrows) B[d] = u[1];
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int idx = base + d * blockDim.x;
+      if (idx < tot) {
+        const int l = idx % a.lpc, k = idx / a.lpc;
+        double2* le = smem + (size_t)(2 * l) * H;
+        const double2 z = make_double2(A[d].x - B[d].y, A[d].y + B[d].x);
+        const double2 zc = make_double2(A[d].x + B[d].y, B[d].x - A[d].y);
+        if ((k & 1) == 0) {
+          le[k >> 1] = z;
+          if (k >= 2 && k <= H - 1) le[H - (k >> 1)] = zc;
+        } else {
+          const int mm = (k - 1) >> 1;
+          le[H + mm] = z;
+          if (k <= H - 1) le[H + (H - 1 - mm)] = zc;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double2* buf = smem + (size_t)line * H;
+  fft_line<true, true, 1>(buf, pls, tl, 1 + (threadIdx.x / nthr));
+  __syncthreads();   // both halves
+  const double2* be = smem + (size_t)(2 * pl_) * H;
+  const double2* bo = be + H;
+  const int ya = 2 * (blockIdx.x * a.lpc + pl_);
+  const double* beta = a.beta ? a.beta + (int64_t)b * a.p : nullptr;
+  const double* gb = a.g ? a.g + (int64_t)b * a.g_bstride : nullptr;
+  const int pc = a.epi == EPI_COV ? a.p : 0;
+  double* out = a.out + (int64_t)b * a.out_bstride;
+  for (int e = t2; e < 2 * a.ncols; e += n2) {
+    const int which = e >= a.ncols;
+    const int x = e - which * a.ncols;
+    const int y = ya + which;
+    if (y >= a.nrows) continue;
+    const int nn = a.col0 + x;
+    const double2 z = cadd(be[nn], cmulc(bo[nn], split_w(wt, nn)));
+    double v = which ? z.y : z.x;
+    if (a.epi == EPI_SCALAR) {
+      v = v + beta[0];
+    } else if (a.epi == EPI_COV) {
+      const double* xr = a.xg + ((int64_t)y * a.ncols + x) * pc;
+      double fx = 0.0;
+      for (int q = 0; q < pc; ++q) fx = fma(xr[q], beta[q], fx);
+      v = v + fx;
+    }
+    if (gb) v = gb[(int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + x] - v;
+    out[(int64_t)y * a.ldo + x] = v;
+  }
 }
 
 // ----------------------------------------------------------------- launches
@@ -649,6 +910,67 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
   RK_CUDA_TRY(launch_pdl(kern, grid, dim3(a.lpc * a.pl.nthr), smem, st, a));
   count_launch();
   RK_LAUNCH_CHECK();
+  return Status::ok();
+}
+
+// split-length launches (see row_fwd_split_kernel); false when the layout does not fit
+static inline size_t split_tail(size_t bytes, const FftPlan& pl, SplitTw* sw, int* tw_off) {
+  *tw_off = tw_slot(bytes);
+  bytes = (size_t)*tw_off * 16 + (size_t)pl.ntw * 16;
+  sw->off = tw_slot(bytes);
+  return (size_t)sw->off * 16 + (size_t)(128 + sw->nhi) * 16;
+}
+
+static Status launch_row_fwd_split(const RowFwdArgs& a0, int batch, cudaStream_t st, bool* done) {
+  RowFwdArgs a = a0;
+  *done = false;
+  a.lpc = 1;
+  if (2 * a.pl.nthr > kFftWideThreads) return Status::ok();
+  size_t smem = sizeof(double2) * 2 * (size_t)a.pl.n;
+  a.prod_off = tw_slot(smem);
+  smem = (size_t)a.prod_off * 16 + sizeof(double) * 2 * (size_t)a.prod_cap;
+  smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
+  if (smem > kSmemMax) return Status::ok();
+  RK_TRY(set_smem_attr((const void*)row_fwd_split_kernel, smem));
+  const dim3 grid((unsigned)((a.nrows + 1) / 2), (unsigned)batch);
+  RK_CUDA_TRY(launch_pdl(row_fwd_split_kernel, grid, dim3(2 * a.pl.nthr), smem, st, a));
+  count_launch();
+  RK_LAUNCH_CHECK();
+  *done = true;
+  return Status::ok();
+}
+
+static Status launch_col_split(const ColArgs& a0, int batch, cudaStream_t st, bool* done) {
+  ColArgs a = a0;
+  *done = false;
+  a.lpc = 1;
+  if (2 * a.pl.nthr > kFftWideThreads) return Status::ok();
+  size_t smem = sizeof(double2) * 2 * (size_t)a.pl.n + sizeof(double) * (size_t)a.ldq + 16;
+  smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
+  if (smem > kSmemMax) return Status::ok();
+  RK_TRY(set_smem_attr((const void*)col_split_kernel, smem));
+  const dim3 grid((unsigned)a.ncols, (unsigned)batch);
+  RK_CUDA_TRY(launch_pdl(col_split_kernel, grid, dim3(2 * a.pl.nthr), smem, st, a));
+  count_launch();
+  RK_LAUNCH_CHECK();
+  *done = true;
+  return Status::ok();
+}
+
+static Status launch_row_inv_split(const RowInvArgs& a0, int batch, cudaStream_t st, bool* done) {
+  RowInvArgs a = a0;
+  *done = false;
+  a.lpc = 1;
+  if (2 * a.pl.nthr > kFftWideThreads) return Status::ok();
+  size_t smem = sizeof(double2) * 2 * (size_t)a.pl.n;
+  smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
+  if (smem > kSmemMax) return Status::ok();
+  RK_TRY(set_smem_attr((const void*)row_inv_split_kernel, smem));
+  const dim3 grid((unsigned)((a.nrows + 1) / 2), (unsigned)batch);
+  RK_CUDA_TRY(launch_pdl(row_inv_split_kernel, grid, dim3(2 * a.pl.nthr), smem, st, a));
+  count_launch();
+  RK_LAUNCH_CHECK();
+  *done = true;
   return Status::ok();
 }
 
@@ -818,7 +1140,14 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     }
   }
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[1], st));
-  RK_TRY(launch_row_fwd(sp ? SRC_SPARSE : SRC_ROWS, ra, batch, st));
+  bool done = false;
+  if (sp && s->h1v.v[2].n) {   // split-length row pass (p1 = 2 H, the M1 nonzero columns < H)
+    RowFwdArgs rs = ra;
+    rs.pl = s->h1v.v[2];
+    rs.sw = s->sw1;
+    RK_TRY(launch_row_fwd_split(rs, batch, st, &done));
+  }
+  if (!done) RK_TRY(launch_row_fwd(sp ? SRC_SPARSE : SRC_ROWS, ra, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[2], st));
   ColArgs ca{};
   ca.pl = plan_pick(s->pl2v, (int64_t)s->H1 * batch);
@@ -835,7 +1164,14 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   ca.U = U;
   ca.ldU = ldU;
   ca.U_bstride = (int64_t)s->H1 * ldU;
-  RK_TRY(launch_col(0, ca, batch, st));
+  done = false;
+  if (s->h2v.v[2].n && row0 + nout <= s->p2 / 2) {   // split-length column pass
+    ColArgs cs = ca;
+    cs.pl = s->h2v.v[2];
+    cs.sw = s->sw2;
+    RK_TRY(launch_col_split(cs, batch, st, &done));
+  }
+  if (!done) RK_TRY(launch_col(0, ca, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
   RowInvArgs ia = epi;
   ia.pl = plan_pick(s->pl1v, (int64_t)((nout + 1) / 2) * batch);
@@ -846,8 +1182,16 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   ia.U_bstride = ca.U_bstride;
   ia.col0 = col0;
   ia.ncols = ncols;
+  const bool split3 = s->h1v.v[2].n && col0 + ncols <= s->p1 / 2;
   if (!hio) {
-    RK_TRY(launch_row_inv(ia, batch, st));
+    done = false;
+    if (split3) {   // split-length inverse row pass
+      RowInvArgs is = ia;
+      is.pl = s->h1v.v[2];
+      is.sw = s->sw1;
+      RK_TRY(launch_row_inv_split(is, batch, st, &done));
+    }
+    if (!done) RK_TRY(launch_row_inv(ia, batch, st));
   } else {   // batch == 1: row blocks, each followed by its device -> host copy
     const int per = chunk_rows(nout, hio->chunks);
     for (int k = 0, r0 = 0; r0 < nout; ++k, r0 += per) {
@@ -860,7 +1204,14 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
       ck.g_row0 = ia.g_row0 + r0;
       ck.lpc = pick_lpc(ck.pl, 4, (int64_t)((ck.nrows + 1) / 2));
       if (hio->xev) RK_CUDA_TRY(cudaStreamWaitEvent(st, hio->xev[k], 0));
-      RK_TRY(launch_row_inv(ck, 1, st));
+      done = false;
+      if (split3) {
+        RowInvArgs is = ck;
+        is.pl = s->h1v.v[2];
+        is.sw = s->sw1;
+        RK_TRY(launch_row_inv_split(is, 1, st, &done));
+      }
+      if (!done) RK_TRY(launch_row_inv(ck, 1, st));
       if (hio->out_host)
         RK_CUDA_TRY(cudaMemcpyAsync(hio->out_host + (int64_t)r0 * ia.ldo, ck.out,
                                     sizeof(double) * (size_t)(r1 - r0) * ia.ldo, cudaMemcpyDeviceToHost, st));
@@ -1074,10 +1425,7 @@ rk_status rk_convolve_spectrum(const double* spec_q_dev, int32_t p1, int32_t p2,
     t.H1 = p1 / 2 + 1;
     t.Q2 = quarter_ld(p2);
     t.spec_q = const_cast<double*>(spec_q_dev);
-    RK_TRY(plan_for(p1, &t.pl1));
-    RK_TRY(plan_for(p2, &t.pl2));
-    RK_TRY(plan_set(p1, &t.pl1v));
-    RK_TRY(plan_set(p2, &t.pl2v));
+    RK_TRY(setup_plans(&t));
     RowInvArgs e{};
     e.out = out_dev;
     e.ldo = M1;

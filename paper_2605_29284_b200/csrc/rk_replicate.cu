@@ -110,18 +110,10 @@ Status setup_from_header(const SetupHdr& h, rk_setup* s) {
   s->p1 = h.p1; s->p2 = h.p2; s->H1 = h.H1; s->Q2 = h.Q2; s->pblk_cap = h.pblk_cap;
   s->n = h.n; s->nnodes = h.nnodes; s->max_pair_ent = h.max_pair_ent; s->pblk_stride = h.pblk_stride;
   s->px0 = h.px0; s->py0 = h.py0; s->cond_var_min = h.cond_var_min;
-  RK_TRY(plan_for(s->p1, &s->pl1));
-  RK_TRY(plan_for(s->p2, &s->pl2));
-  RK_TRY(plan_set(s->p1, &s->pl1v));
-  RK_TRY(plan_set(s->p2, &s->pl2v));
+  RK_TRY(setup_plans(s));
   Embedding& e = s->emb;
   e.ps1 = h.ps1; e.ps2 = h.ps2; e.doubled = h.doubled; e.hs1 = h.hs1; e.qs2 = h.qs2;
-  if (h.emb_ready) {
-    RK_TRY(plan_for(e.ps1, &e.pl1));
-    RK_TRY(plan_for(e.ps2, &e.pl2));
-    RK_TRY(plan_set(e.ps1, &e.ps1v));
-    RK_TRY(plan_set(e.ps2, &e.ps2v));
-  }
+  if (h.emb_ready) RK_TRY(embedding_plans(s));
   return Status::ok();
 }
 

@@ -88,6 +88,7 @@ struct CsColArgs {
   double* g;                 // (batch, M2, M1)
   int64_t g_bstride;
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
+  SplitTw sw;                // split-length kernel: w_P^n tables
 };
 
 template <bool TWS, int FM>
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSpli
     buf[y] = make_double2(0.5 * ((A.x + Am.x) - (B.y - Bm.y)), 0.5 * ((A.y - Am.y) + (B.x + Bm.x)));
   }
   __syncthreads();
-  fft_line<true, TWS, FM>(buf, pls, tl);
+  fft_line<true, TWS, FM>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+  if (a.lpc > 1) __syncthreads();   // the stores below read every line
   double* g = a.g + (int64_t)b * a.g_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, y = idx / a.lpc;
@@ -290,10 +292,7 @@ Status ensure_embedding(rk_setup* s, cudaStream_t st) {
       e.doubled = attempt;
       e.hs1 = hs1;
       e.qs2 = qs2;
-      RK_TRY(plan_for(e.ps1, &e.pl1));
-      RK_TRY(plan_for(e.ps2, &e.pl2));
-      RK_TRY(plan_set(e.ps1, &e.ps1v));
-      RK_TRY(plan_set(e.ps2, &e.ps2v));
+      RK_TRY(embedding_plans(s));
       RK_CUDA_TRY(cudaMalloc(&e.root_q, sizeof(double) * (size_t)hs1 * qs2));
       const double P = (double)p1 * (double)p2;
       root_q_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)hs1 * qs2, 256), 148 * 32), 256, 0, st>>>(
@@ -479,7 +478,8 @@ __global__ void __launch_bounds__(FM == 1 ? kFftWideThreads : FM == 2 ? kFftSpli
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
-  fft_line<true, TWS, FM>(buf, pls, tl);
+  fft_line<true, TWS, FM>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+  if (a.lpc > 1) __syncthreads();   // the stores below read every line
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, ix = idx / a.lpc;
@@ -507,6 +507,7 @@ struct CsGenArgs {
   int tw_off, q_off;         // smem offsets (double2 units): twiddles, tail queues
   int qcap;                  // tail-queue entries per warp actually used (<= the kernel's QCAP;
                              // smaller only to exercise the overflow path: RK_CS_QCAP)
+  SplitTw sw;                // split-length kernel: w_P^n tables
 };
 
 // words w .. w+3 of the (fs, 0) Philox stream; two blocks when w is not block aligned
@@ -613,12 +614,137 @@ __global__ void __launch_bounds__(MAXT, MINB) cs_rowgen_kernel(const CsGenArgs a
     for (int x = tl; x < n; x += nthr) buf[x] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  fft_line<true, TWS, FM, false>(buf, pls, tl);
+  fft_line<true, TWS, FM, false>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+  if (a.lpc > 1) __syncthreads();   // the stores below read every line
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int idx = threadIdx.x; idx < a.lpc * a.keep; idx += blockDim.x) {
     const int l = idx % a.lpc, ix = idx / a.lpc;
     const int row = blockIdx.x * a.lpc + l;
     if (row < a.ps2) V[(int64_t)ix * a.ldV + row] = smem[(size_t)l * n + ix];
+  }
+}
+
+// Split-length versions of the two field passes for the large tori (ps = 2 H above the
+// WIDE-plan lengths; rk_predict.cu explains the identity).  Only the OUTPUT is pruned here (kept
+// columns / rows < H; the random input fills the whole torus), so each length-ps inverse
+// transform is the two length-H inverse transforms of its even- and odd-indexed inputs,
+// combined as y[n] = e[n] + w^-n o[n] for the kept n.
+constexpr int kSplitQcap = 128;   // tail-queue entries per warp
+
+__global__ void __launch_bounds__(kFftWideThreads, 1) cs_rowgen_split_kernel(const CsGenArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int H = a.pl.n;
+  const int nthr = a.pl.nthr;
+  const int half = threadIdx.x / nthr;
+  const int tl = threadIdx.x - half * nthr;
+  const int t2 = threadIdx.x, n2 = 2 * nthr;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const int iy = blockIdx.x;
+  double2* be = smem;
+  double2* bo = smem + H;
+  double* wq = (double*)(smem + a.q_off) + (size_t)(threadIdx.x >> 5) * kSplitQcap;
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
+  const uint64_t fs = a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
+  const uint64_t Ps = (uint64_t)a.ps1 * (uint64_t)a.ps2;
+  const uint64_t wre = (uint64_t)iy * a.ps1, wim = Ps + wre;   // simulate.py:114-115
+  const double* rq = a.root_q + (int64_t)min(iy, a.ps2 - iy) * a.rq_ld;
+  const int ng = (a.ps1 + 3) / 4;
+  for (int g0 = t2 - lane; g0 < ng; g0 += n2) {   // warp-uniform
+    const int g = g0 + lane;
+    const int x0 = 4 * g;
+    uint64_t re[4], im[4];
+    philox_words4(wre + x0, fs, re);
+    philox_words4(wim + x0, fs, im);
+    double uu[8], z[8];
+    unsigned tmask = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uu[q] = word_uniform(q < 4 ? re[q] : im[q - 4]);
+      if (g < ng && x0 + (q & 3) < a.ps1 && ndtri_is_tail(uu[q])) tmask |= 1u << q;
+    }
+    ndtri_central_n<8>(uu, z);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (tmask >> q & 1) z[q] = uu[q];
+    const int cnt = __popc(tmask);
+    int off = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;
+    if (total > min(kSplitQcap, a.qcap)) {   // queue overflow (rare): each lane evaluates its own
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) z[q] = ndtri_tail(uu[q]);
+    } else if (total) {
+      int o = off;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) wq[o++] = z[q];
+      __syncwarp();
+      for (int k = lane; k < total; k += 32) wq[k] = ndtri_tail(wq[k]);
+      __syncwarp();
+      o = off;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) z[q] = wq[o++];
+      __syncwarp();
+    }
+    if (g < ng) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int x = x0 + q;
+        if (x < a.ps1) {
+          const double r = __ldg(&rq[min(x, a.ps1 - x)]);
+          (x & 1 ? bo : be)[x >> 1] = make_double2(r * z[q], r * z[4 + q]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  fft_line<true, true, 1>(half ? bo : be, pls, tl, 1 + half);
+  __syncthreads();   // both halves
+  double2* V = a.V + (int64_t)b * a.V_bstride;
+  for (int ix = threadIdx.x; ix < a.keep; ix += blockDim.x)
+    V[(int64_t)ix * a.ldV + iy] = cadd(be[ix], cmulc(bo[ix], split_w(wt, ix)));
+}
+
+__global__ void __launch_bounds__(kFftWideThreads, 1) cs_col_split_kernel(const CsColArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int H = a.pl.n, P = 2 * H;
+  const int nthr = a.pl.nthr;
+  const int half = threadIdx.x / nthr;
+  const int tl = threadIdx.x - half * nthr;
+  const int b = blockIdx.y;
+  const int ca = 2 * blockIdx.x, cb = ca + 1;
+  double2* be = smem;
+  double2* bo = smem + H;
+  const double2* Va = a.V + (int64_t)b * a.V_bstride + (int64_t)ca * a.ldV;
+  const double2* Vb = Va + a.ldV;
+  const bool va = ca < a.ncols, vb = cb < a.ncols;
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
+  pdl_wait();
+  for (int y = threadIdx.x; y < P; y += blockDim.x) {   // Hermitian parts, as cs_col_kernel
+    const int m = y ? P - y : 0;
+    const double2 A = va ? Va[y] : make_double2(0.0, 0.0), Am = va ? Va[m] : make_double2(0.0, 0.0);
+    const double2 B = vb ? Vb[y] : make_double2(0.0, 0.0), Bm = vb ? Vb[m] : make_double2(0.0, 0.0);
+    (y & 1 ? bo : be)[y >> 1] =
+        make_double2(0.5 * ((A.x + Am.x) - (B.y - Bm.y)), 0.5 * ((A.y - Am.y) + (B.x + Bm.x)));
+  }
+  __syncthreads();
+  fft_line<true, true, 1>(half ? bo : be, pls, tl, 1 + half);
+  __syncthreads();   // both halves
+  double* g = a.g + (int64_t)b * a.g_bstride;
+  for (int y = threadIdx.x; y < a.keep; y += blockDim.x) {
+    const double2 v = cadd(be[y], cmulc(bo[y], split_w(wt, y)));
+    if (va) g[(int64_t)y * a.ncols + ca] = v.x;
+    if (vb) g[(int64_t)y * a.ncols + cb] = v.y;
   }
 }
 
@@ -631,7 +757,43 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
   RK_TRY(scratch_alloc((void**)&V, sizeof(double2) * (size_t)s->M1 * ldV * batch, st));
   double2* Zs = nullptr;   // freed after the column pass so the two FFT kernels stay adjacent
   static const bool fused = !(getenv("RK_CS_FUSED") && atoi(getenv("RK_CS_FUSED")) == 0);
-  if (fused) {
+  bool gen_done = false;
+  if (fused && e.hs1v.v[2].n && 2 * e.hs1v.v[2].nthr <= kFftWideThreads) {   // split-length row pass
+    CsGenArgs ga{};
+    ga.pl = e.hs1v.v[2];
+    ga.lpc = 1;
+    ga.seed = seed;
+    ga.j0 = j0;
+    ga.direct = direct;
+    ga.ps1 = e.ps1;
+    ga.ps2 = e.ps2;
+    ga.root_q = e.root_q;
+    ga.rq_ld = e.hs1;
+    ga.keep = s->M1;
+    ga.V = V;
+    ga.ldV = ldV;
+    ga.V_bstride = (int64_t)s->M1 * ldV;
+    static const int qcap_env2 = getenv("RK_CS_QCAP") ? atoi(getenv("RK_CS_QCAP")) : 1 << 30;
+    ga.qcap = std::max(0, qcap_env2);
+    ga.sw = e.sws1;
+    const int threads = 2 * ga.pl.nthr;
+    size_t by = sizeof(double2) * 2 * (size_t)ga.pl.n;
+    ga.q_off = (int)((by + 15) / 16);
+    by = (size_t)ga.q_off * 16 + sizeof(double) * (size_t)(threads / 32) * kSplitQcap;
+    ga.tw_off = (int)((by + 15) / 16);
+    by = (size_t)ga.tw_off * 16 + sizeof(double2) * (size_t)ga.pl.ntw;
+    ga.sw.off = (int)((by + 15) / 16);
+    by = (size_t)ga.sw.off * 16 + sizeof(double2) * (size_t)(128 + ga.sw.nhi);
+    if (by <= 227 * 1024) {
+      RK_TRY(set_smem_attr((const void*)cs_rowgen_split_kernel, by));
+      cs_rowgen_split_kernel<<<dim3((unsigned)e.ps2, (unsigned)batch), threads, by, st>>>(ga);
+      count_launch();
+      RK_LAUNCH_CHECK();
+      gen_done = true;
+    }
+  }
+  if (gen_done) {
+  } else if (fused) {
     CsGenArgs ga{};
     ga.pl = plan_pick(e.ps1v, (int64_t)e.ps2 * batch);
     ga.lpc = pick_lpc(ga.pl, 4, (int64_t)e.ps2 * batch);
@@ -707,8 +869,35 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     count_launch();
     Zs = Z;
   }
-  CsColArgs ca{};
   const int64_t cpairs = (s->M1 + 1) / 2;   // two columns per line
+  if (e.hs2v.v[2].n && 2 * e.hs2v.v[2].nthr <= kFftWideThreads) {   // split-length column pass
+    CsColArgs cs{};
+    cs.pl = e.hs2v.v[2];
+    cs.lpc = 1;
+    cs.ncols = s->M1;
+    cs.keep = s->M2;
+    cs.V = V;
+    cs.ldV = ldV;
+    cs.V_bstride = (int64_t)s->M1 * ldV;
+    cs.g = g;
+    cs.g_bstride = (int64_t)s->M1 * s->M2;
+    cs.sw = e.sws2;
+    size_t by = sizeof(double2) * 2 * (size_t)cs.pl.n;
+    cs.tw_off = (int)((by + 15) / 16);
+    by = (size_t)cs.tw_off * 16 + sizeof(double2) * (size_t)cs.pl.ntw;
+    cs.sw.off = (int)((by + 15) / 16);
+    by = (size_t)cs.sw.off * 16 + sizeof(double2) * (size_t)(128 + cs.sw.nhi);
+    if (by <= 227 * 1024) {
+      RK_TRY(set_smem_attr((const void*)cs_col_split_kernel, by));
+      RK_CUDA_TRY(launch_pdl(cs_col_split_kernel, dim3((unsigned)cpairs, (unsigned)batch), dim3(2 * cs.pl.nthr), by,
+                             st, cs));
+      count_launch();
+      scratch_free(Zs, st);
+      scratch_free(V, st);
+      return Status::ok();
+    }
+  }
+  CsColArgs ca{};
   ca.pl = plan_pick(e.ps2v, cpairs * batch);
   ca.lpc = pick_lpc(ca.pl, 4, cpairs * batch);
   ca.ncols = s->M1;

@@ -1,0 +1,64 @@
+"""Kernel variants that must agree: each run in a subprocess with its switch set, on the same
+inputs, compared with the default path.
+
+* RK_SPLIT=0: the full-length FFT passes instead of the split-length ones (for tori above the
+  WIDE-plan lengths, P = 2 H with the nonzero rows / kept outputs below H): equal to 1e-13;
+* RK_WEIGHTS_OB=0 / 2: the one-observation-per-warp weights kernels instead of the 4-per-warp
+  interleaved one: bitwise identical weights and fields (same operations, same order).
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from rk_testutil import ROOT, has_gpu, rel_err
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+CODE = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2605_29284_b200 as pk
+rng = np.random.default_rng(11)
+n, L, dims, nu = {n}, {L}, {dims}, {nu}
+obs = rng.uniform(0, 1, size=(n, 2))
+model = pk.CovarianceModel(1.0, 12.0, nu, 0.01)
+grid = pk.build_padded_grid((0, 1, 0, 1), dims, L, obs)
+st = pk.build_setup(model, grid, L, obs)
+c = rng.normal(size=n)
+field = pk.predict_rapid(st, c, np.array([0.25]))
+cstar = st.coefficients_to_grid(c)
+conv = pk.convolve_filter(st.filter_spectrum, st.embed_dims, cstar)
+np.savez({out!r}, field=field, w=st.weights, conv=conv, embed=np.array(st.embed_dims))
+"""
+
+
+def _run(tmp_path, tag, env_extra, **kw):
+    out = str(tmp_path / f"{tag}.npz")
+    code = CODE.format(root=ROOT, out=out, **kw)
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env_extra), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return dict(np.load(out))
+
+
+@pytest.mark.parametrize("dims", [(2600, 2500), (4096, 4096)])
+def test_split_length_passes_match_full_length(tmp_path, dims):
+    kw = dict(n=6000, L=2, dims=dims, nu=1.5)
+    a = _run(tmp_path, "split", {}, **kw)
+    b = _run(tmp_path, "full", {"RK_SPLIT": "0"}, **kw)
+    assert max(a["embed"]) > 4608   # a split-length torus
+    assert rel_err(a["field"], b["field"]) < 1e-13
+    assert rel_err(a["conv"], b["conv"]) < 1e-13
+
+
+@pytest.mark.parametrize("L,nu", [(3, 1.5), (4, 2.5), (3, 1.0)])
+def test_weights_kernel_variants_bitwise(tmp_path, L, nu):
+    kw = dict(n=5000, L=L, dims=(300, 280), nu=nu)
+    a = _run(tmp_path, "ob4", {}, **kw)
+    for v in ("0", "2"):
+        b = _run(tmp_path, "ob" + v, {"RK_WEIGHTS_OB": v}, **kw)
+        assert np.array_equal(a["w"], b["w"]), v
+        assert np.array_equal(a["field"], b["field"]), v
