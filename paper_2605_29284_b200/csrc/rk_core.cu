@@ -1208,7 +1208,10 @@ static Status launch_weights(const rk_setup* s, int32_t* base, double* weights, 
     };
     // RK_WEIGHTS_OB: observations per warp of the interleaved kernel for L = 3 / 4 (0 = the
     // one-observation kernels)
-    static const int ob = getenv("RK_WEIGHTS_OB") ? atoi(getenv("RK_WEIGHTS_OB")) : 4;
+    // measured (tools/weights_sweep.py): 2 per warp for L = 4 (cfg5 0.233 -> 0.204 ms, cfg3 0.099 ->
+    // 0.096 ms); for L = 3 the one-observation kernels are as fast or faster (cfg2 Bessel: 0.016 vs 0.025)
+    static const int ob_env = getenv("RK_WEIGHTS_OB") ? atoi(getenv("RK_WEIGHTS_OB")) : -1;
+    const int ob = ob_env >= 0 ? ob_env : (L == 4 ? 2 : 0);
     auto launch_ob = [&](auto kern, int obs_per_warp) -> Status {
       RK_TRY(set_smem_attr((const void*)kern, wsl));
       const int nb = (int)std::min<int64_t>(ceil_div(ceil_div(n, obs_per_warp), 8), 148 * 2);

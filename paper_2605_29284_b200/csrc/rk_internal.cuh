@@ -75,6 +75,7 @@ struct GraphKey {
 };
 
 struct Workspace {
+  uint64_t serial = 0;          // creation order (eviction of the oldest, rk_predict.cu get_ws)
   double2* T = nullptr;         // (H1, ldT)
   double2* U = nullptr;         // (H1, ldU)
   double* c_in = nullptr;       // host-path staging: c, then beta at an even offset

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 
 #include "rk_internal.cuh"
@@ -1263,6 +1264,29 @@ Status predict_batch(const rk_setup* s, const PredictBatch& pb, cudaStream_t st,
 }
 
 // ------------------------------------------------- persistent workspace + graph replay
+static void free_ws(Workspace* w) {
+  if (!w) return;
+  for (auto& g : w->graphs) cudaGraphExecDestroy(g.second);
+  for (auto& g : w->hgraphs) cudaGraphExecDestroy(g.second);
+  if (w->aux) cudaStreamDestroy(w->aux);
+  if (w->fork) cudaEventDestroy(w->fork);
+  for (auto& e : w->xev)
+    if (e) cudaEventDestroy(e);
+  cudaFreeHost(w->cb_h);
+  cudaFree(w->T);
+  cudaFree(w->U);
+  cudaFree(w->c_in);   // beta_in lives in the same allocation
+  cudaFree(w->xg_in);
+  cudaFree(w->out);
+  if (w->cap) cudaStreamDestroy(w->cap);
+  delete w;
+}
+
+// at most this many per-stream workspaces per setup: a caller cycling through streams evicts
+// the least recently created one (after a device synchronisation, since its stream may be
+// gone) instead of growing without bound
+static constexpr size_t kMaxWorkspaces = 8;
+
 static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
   std::lock_guard<std::mutex> lk(s->ws_mu);
   auto it = s->ws.find(st);
@@ -1270,7 +1294,17 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
     *out = it->second;
     return Status::ok();
   }
-  Workspace* w = new Workspace();
+  if (s->ws.size() >= kMaxWorkspaces) {
+    auto victim = s->ws.begin();
+    for (auto jt = s->ws.begin(); jt != s->ws.end(); ++jt)
+      if (jt->second->serial < victim->second->serial) victim = jt;
+    RK_CUDA_TRY(cudaDeviceSynchronize());
+    free_ws(victim->second);
+    s->ws.erase(victim);
+  }
+  std::unique_ptr<Workspace, void (*)(Workspace*)> w(new Workspace(), free_ws);   // freed on any failure below
+  static uint64_t serial = 0;
+  w->serial = ++serial;
   const int64_t ldT = round_even(s->M2), ldU = round_even(s->m2);
   RK_CUDA_TRY(cudaMalloc(&w->T, sizeof(double2) * (size_t)s->H1 * ldT));
   RK_CUDA_TRY(cudaMalloc(&w->U, sizeof(double2) * (size_t)s->H1 * ldU));
@@ -1284,8 +1318,8 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
   RK_CUDA_TRY(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
   for (auto& e : w->xev) RK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   RK_CUDA_TRY(cudaMallocHost(&w->cb_h, sizeof(double) * (boff + 16)));
-  s->ws[st] = w;
-  *out = w;
+  *out = w.get();
+  s->ws[st] = w.release();
   return Status::ok();
 }
 
@@ -1294,25 +1328,12 @@ void free_workspaces(rk_setup* s) {
     cudaStreamDestroy(s->host_st);
     s->host_st = nullptr;
   }
-  for (auto& kv : s->ws) {
-    Workspace* w = kv.second;
-    for (auto& g : w->graphs) cudaGraphExecDestroy(g.second);
-    for (auto& g : w->hgraphs) cudaGraphExecDestroy(g.second);
-    if (w->aux) cudaStreamDestroy(w->aux);
-    if (w->fork) cudaEventDestroy(w->fork);
-    for (auto& e : w->xev)
-      if (e) cudaEventDestroy(e);
-    cudaFreeHost(w->cb_h);
-    cudaFree(w->T);
-    cudaFree(w->U);
-    cudaFree(w->c_in);   // beta_in lives in the same allocation
-    cudaFree(w->xg_in);
-    cudaFree(w->out);
-    if (w->cap) cudaStreamDestroy(w->cap);
-    delete w;
-  }
+  for (auto& kv : s->ws) free_ws(kv.second);
   s->ws.clear();
 }
+
+// graph bookkeeping per workspace stays bounded: pointer sets seen once are forgotten in bulk
+static constexpr size_t kMaxSeen = 256;
 
 // Predict of one field through the workspace: direct launches the first time a pointer
 // set is seen, a CUDA graph (captured on the workspace's private stream, replayed on
@@ -1328,7 +1349,10 @@ static Status predict_graphed(rk_setup* s, Workspace* w, const PredictBatch& pb,
     std::lock_guard<std::mutex> lk(s->ws_mu);
     auto it = w->graphs.find(key);
     if (it != w->graphs.end()) exec = it->second;
-    else capture = (++w->seen[key] >= 2) && w->graphs.size() < 64;
+    else {
+      if (w->seen.size() >= kMaxSeen) w->seen.clear();
+      capture = (++w->seen[key] >= 2) && w->graphs.size() < 64;
+    }
   }
   static const bool use_graph = !(getenv("RK_DEV_GRAPH") && atoi(getenv("RK_DEV_GRAPH")) == 0);
   if (!use_graph) return predict_batch(s, pb, st, nullptr, w);
@@ -1599,7 +1623,10 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
       std::lock_guard<std::mutex> lk(ms->ws_mu);
       auto it = w->hgraphs.find(key);
       if (it != w->hgraphs.end()) exec = it->second;
-      else capture = graph_env && (++w->hseen[key] >= 2) && w->hgraphs.size() < 64;
+      else {
+        if (w->hseen.size() >= kMaxSeen) w->hseen.clear();
+        capture = graph_env && (++w->hseen[key] >= 2) && w->hgraphs.size() < 64;
+      }
     }
     const int nk = kPredictKernels + (K - 1);
     if (!exec && !capture) {

@@ -221,6 +221,30 @@ def _fixed_inputs(setup: RapidSetup, beta_hat, grid_covariates):
     return beta, xg
 
 
+def _device_f64(t):
+    """Contiguous float64 CUDA tensor on the current device (converted if needed)."""
+    torch = D.torch()
+    if (D.is_device_tensor(t) and t.dtype == torch.float64 and t.is_contiguous()
+            and t.device.index == torch.cuda.current_device()):
+        return t
+    return D.to_device(t)
+
+
+def _check_out(out, shape, device: bool):
+    """``out`` must be a C-contiguous float64 (m2, m1) buffer: a CUDA tensor on the current
+    device for device inputs, a host array otherwise."""
+    torch = D.torch()
+    if device:
+        ok = (D.is_device_tensor(out) and out.dtype == torch.float64 and out.is_contiguous()
+              and tuple(out.shape) == shape and out.device.index == torch.cuda.current_device())
+    else:
+        ok = (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.c_contiguous
+              and out.shape == shape and out.flags.writeable)
+    if not ok:
+        kind = "CUDA tensor on the current device" if device else "writeable numpy array"
+        raise DomainError(f"out must be a C-contiguous float64 {kind} of shape {shape}")
+
+
 def predict_rapid(setup: RapidSetup, c, beta_hat=None, grid_covariates=None, *, out=None):
     """(m2, m1) interior field: FFT convolution of A'c with the covariance filter + X_g beta.
 
@@ -235,19 +259,28 @@ def predict_rapid(setup: RapidSetup, c, beta_hat=None, grid_covariates=None, *, 
             cd = cd.to(dtype=D.torch().float64).contiguous()
         if cd.shape[0] != setup.n_obs:
             raise DomainError(f"coefficient vector has {cd.shape[0]} entries for {setup.n_obs} observations")
-        bd = None if beta is None else (beta if D.is_device_tensor(beta) else D.to_device(beta))
-        xd = None if xg is None else (xg if D.is_device_tensor(xg) and xg.is_contiguous()
-                                      and xg.dtype == D.torch().float64 else D.to_device(xg))
-        res = D.empty((m2, m1)) if out is None else out
+        # every buffer the library reads / writes as raw float64 must be contiguous float64 on
+        # this device (a strided or float32 tensor would be misread / overrun)
+        bd = None if beta is None else _device_f64(beta)
+        xd = None if xg is None else _device_f64(xg)
+        if out is None:
+            res = D.empty((m2, m1))
+        else:
+            _check_out(out, (m2, m1), device=True)
+            res = out
         N.call("rk_predict_dev", setup.handle, N.ptr(cd), N.ptr(bd), p, N.ptr(xd), N.ptr(res),
                N.stream_ptr())
         return res
     ch = D.host_f64(c).ravel()
     if ch.shape[0] != setup.n_obs:
         raise DomainError(f"coefficient vector has {ch.shape[0]} entries for {setup.n_obs} observations")
-    bh = None if beta is None else (beta.cpu().numpy() if D.is_device_tensor(beta) else beta)
-    xh = None if xg is None else (xg.cpu().numpy() if D.is_device_tensor(xg) else D.host_f64(xg))
-    res = np.empty((m2, m1)) if out is None else out
+    bh = None if beta is None else D.host_f64(beta.cpu().numpy() if D.is_device_tensor(beta) else beta)
+    xh = None if xg is None else D.host_f64(xg.cpu().numpy() if D.is_device_tensor(xg) else xg)
+    if out is None:
+        res = np.empty((m2, m1))
+    else:
+        _check_out(out, (m2, m1), device=False)
+        res = out
     # synchronous host-buffer call: on the setup's own stream (no torch stream lookup)
     N.call("rk_predict_host", setup.handle, N.ptr(ch), N.ptr(bh), p, N.ptr(xh), N.ptr(res), None)
     return res

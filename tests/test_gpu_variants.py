@@ -62,3 +62,60 @@ def test_weights_kernel_variants_bitwise(tmp_path, L, nu):
         b = _run(tmp_path, "ob" + v, {"RK_WEIGHTS_OB": v}, **kw)
         assert np.array_equal(a["w"], b["w"]), v
         assert np.array_equal(a["field"], b["field"]), v
+
+
+CFG2 = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2605_29284_b200 as pk
+from paper_2605_29284_b200 import workloads
+wl = workloads.cfg2()
+model = pk.CovarianceModel(wl.sigma2, wl.alpha, wl.nu, wl.tau2)
+grid = pk.build_padded_grid(wl.domain, wl.dims, wl.L, wl.obs)
+st = pk.build_setup(model, grid, wl.L, wl.obs)
+xg = workloads.grid_covariates_for(grid.interior_nodes(), wl.grid_covariates)
+c = np.random.default_rng(5).normal(size=wl.obs.shape[0])
+np.save({out!r}, pk.predict_rapid(st, c, np.array([0.5, 1.0, -1.0]), xg))
+"""
+
+
+def test_plan_block_staging_bitwise(tmp_path):
+    """Pass 1 fetching each row pair's plan by one TMA bulk copy (RK_PLAN_TMA=1, one-wave
+    launches) vs the direct plan loads (0) on cfg2's clustered design: bitwise equal."""
+    res = {}
+    for v in ("1", "0"):
+        out = str(tmp_path / f"p{v}.npy")
+        r = subprocess.run([sys.executable, "-c", CFG2.format(root=ROOT, out=out)],
+                           env=dict(os.environ, RK_PLAN_TMA=v), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[v] = np.load(out)
+    assert np.array_equal(res["1"], res["0"])
+
+
+def test_out_buffer_validation_and_many_streams():
+    import torch
+    import paper_2605_29284_b200 as pk
+    from paper_2605_29284_b200.errors import DomainError
+    rng = np.random.default_rng(3)
+    obs = rng.uniform(0, 1, size=(200, 2))
+    model = pk.CovarianceModel(1.0, 8.0, 1.5, 0.01)
+    st = pk.build_setup(model, pk.build_padded_grid((0, 1, 0, 1), (40, 30), 2, obs), 2, obs)
+    c = torch.as_tensor(rng.normal(size=200), device="cuda")
+    ref = pk.predict_rapid(st, c, np.array([1.0]))
+    for bad in (torch.empty((30, 40), dtype=torch.float32, device="cuda"),
+                torch.empty((40, 30), dtype=torch.float64, device="cuda"),
+                torch.empty((30, 80), dtype=torch.float64, device="cuda")[:, ::2]):
+        with pytest.raises(DomainError):
+            pk.predict_rapid(st, c, np.array([1.0]), out=bad)
+    with pytest.raises(DomainError):
+        pk.predict_rapid(st, c.cpu().numpy(), np.array([1.0]), out=np.empty((30, 40), dtype=np.float32))
+    # float32 / strided beta on the device is converted, not misread
+    b32 = torch.tensor([1.0, 7.0], dtype=torch.float32, device="cuda")[:1]
+    assert torch.equal(pk.predict_rapid(st, c, b32), ref)
+    # more streams than the workspace cap (8): oldest workspaces are evicted, results unchanged
+    for k in range(12):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            out = pk.predict_rapid(st, c, torch.tensor([1.0], dtype=torch.float64, device="cuda"))
+        s.synchronize()
+        assert torch.equal(out, ref), k
