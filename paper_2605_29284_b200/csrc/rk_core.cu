@@ -143,6 +143,33 @@ Status setup_plans(rk_setup* s) {
   return Status::ok();
 }
 
+__global__ void spec_split_kernel(const double* __restrict__ q, int Q2, int H1, int H, int ldh,
+                                  double* __restrict__ out) {
+  const int64_t tot = (int64_t)H1 * 2 * ldh;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % ldh), h = (int)((e / ldh) % 2);
+    const int64_t kx = e / (2 * ldh);
+    const int k = 2 * j + h;
+    out[e] = k <= H ? q[kx * Q2 + k] : 0.0;
+  }
+}
+
+Status build_spec_split(rk_setup* s, cudaStream_t st) {
+  cudaFree(s->spec_s);
+  s->spec_s = nullptr;
+  s->ldh = 0;
+  if (!s->h2v.v[2].n || !s->spec_q) return Status::ok();
+  const int H = s->p2 / 2;
+  s->ldh = ((H / 2 + 1) + 1) & ~1;   // even: 16-byte rows for the bulk copy
+  RK_CUDA_TRY(cudaMalloc(&s->spec_s, sizeof(double) * (size_t)s->H1 * 2 * s->ldh));
+  const int64_t tot = (int64_t)s->H1 * 2 * s->ldh;
+  spec_split_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 148 * 32), 256, 0, st>>>(s->spec_q, s->Q2, s->H1, H,
+                                                                                           s->ldh, s->spec_s);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  return Status::ok();
+}
+
 Status embedding_plans(rk_setup* s) {
   Embedding& e = s->emb;
   RK_TRY(plan_for(e.ps1, &e.pl1));
@@ -1062,8 +1089,13 @@ static Status build_sparse_gather(rk_setup* s) {
     RK_CUDA_TRY(cudaMemcpy(rn.data(), s->row_node, sizeof(int32_t) * rn.size(), cudaMemcpyDeviceToHost));
     RK_CUDA_TRY(cudaMemcpy(no.data(), s->node_off, sizeof(int32_t) * no.size(), cudaMemcpyDeviceToHost));
     s->max_pair_ent = 0;
-    for (int y = 0; y < s->M2; y += 2)
-      s->max_pair_ent = std::max<int64_t>(s->max_pair_ent, no[rn[std::min(y + 2, s->M2)]] - no[rn[y]]);
+    s->max_half_ent = 0;
+    for (int y = 0; y < s->M2; y += 2) {
+      const int a0 = rn[y], a1 = rn[std::min(y + 2, s->M2)];
+      const int am = a0 + (a1 - a0 + 1) / 2;   // the split-length pass 1 gives each CTA half the nodes
+      s->max_pair_ent = std::max<int64_t>(s->max_pair_ent, no[a1] - no[a0]);
+      s->max_half_ent = std::max<int64_t>(s->max_half_ent, std::max(no[am] - no[a0], no[a1] - no[am]));
+    }
     // per row pair p: {first node, first node of row 2p+1, first contribution}; entry
     // npairs is the end sentinel, so a pair reads two adjacent records in one round trip
     const int npairs = (s->M2 + 1) / 2;
@@ -1155,6 +1187,7 @@ void free_setup(rk_setup* s) {
   cudaFree(s->pair_info);
   cudaFree(s->pblk);
   cudaFree(s->spec_q);
+  cudaFree(s->spec_s);
   cudaFree(s->kn_chol_dev);
   cudaFree(s->emb.root_q);
   delete s;
@@ -1379,6 +1412,7 @@ spectrum:
   RK_CUDA_TRY(cudaMalloc(&s->spec_q, sizeof(double) * (size_t)s->H1 * s->Q2));
   RK_TRY(spectrum_quarter(s->mat, grid->hx, grid->hy, s->p1, s->p2,
                           1.0 / ((double)s->p1 * (double)s->p2), s->spec_q, s->Q2, 0));
+  RK_TRY(build_spec_split(s, 0));
   RK_CUDA_TRY(cudaDeviceSynchronize());
   *out = guard.release();
   return Status::ok();

@@ -141,6 +141,7 @@ struct rk_setup {
   int32_t* ent_w = nullptr;       // (n M) index into wsort
   int32_t* ent_c = nullptr;       // (n M) original observation index (into c)
   int64_t max_pair_ent = 0;       // most contributions of one row pair (2k, 2k+1)
+  int64_t max_half_ent = 0;       // most contributions of half a row pair's nodes (split pass 1)
   double* ent_wv = nullptr;       // (n M) weight of each contribution (wsort[ent_w])
   int4* pair_info = nullptr;      // (ceil(M2/2) + 1) {node0, node of row 2p+1, contribution0, 0}
   // per-row-pair plan blocks at a fixed stride (small plans only): {count, nodes, 0, 0}, then
@@ -150,6 +151,8 @@ struct rk_setup {
   int64_t pblk_stride = 0;        // bytes (multiple of 16)
   int pblk_cap = 0;
   double* spec_q = nullptr;     // (H1, Q2): Re fft2(filter)[ky, kx] / (p1 p2), ky <= p2/2
+  double* spec_s = nullptr;     // split-length column pass: (H1, 2, ldh) spec_q[kx][2 j + h], j <= p2/4
+  int ldh = 0;
   double* kn_chol_dev = nullptr;  // (M, M) row-major lower
   std::vector<double> kn_chol, kn_inv;
   double cond_var_min = 0;
@@ -186,6 +189,8 @@ namespace rk {
 // all FFT plans of a setup from its p1 / p2: full lengths, half lengths + w_P tables where a
 // split-length pass applies (rk_core.cu)
 Status setup_plans(rk_setup* s);
+// the parity-split spectrum of the split-length column pass (after spec_q is built)
+Status build_spec_split(rk_setup* s, cudaStream_t st);
 // the embedding's plans from its ps1 / ps2 (same rules)
 Status embedding_plans(rk_setup* s);
 

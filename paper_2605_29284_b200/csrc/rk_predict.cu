@@ -22,7 +22,11 @@
 #include <memory>
 #include <mutex>
 
+#include <cooperative_groups.h>
+
 #include "rk_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rk {
 // Per-CTA phase timestamps (%globaltimer, ns) for the three predict kernels, compiled in with
@@ -339,6 +343,11 @@ struct ColArgs {
   double scale;
   int tw_off;                // smem offset (double2 units) of the staged twiddle table
   SplitTw sw;                // split-length kernel: w_P^n tables
+  const double* spec_s;      // split-length kernel: parity-split spectrum (ncols, 2, ldh)
+  int ldh;
+  int upair;                 // split-length kernel: write U pair-blocked (see UPair)
+  int64_t ldp;
+  int hh;
 };
 
 template <int MODE, bool TWS, int FM>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
@@ -435,6 +444,9 @@ struct RowInvArgs {
   int ep_smem;               // 1: epilogue operands prefetched to smem, 0: read from global
   int xg_bulk;               // X_g is 16-byte aligned: one TMA bulk copy per CTA
   SplitTw sw;                // split-length kernel: w_P^n tables
+  int upair;                 // split-length kernel: U is pair-blocked (see UPair)
+  int64_t ldp;
+  int hh;
 };
 
 template <bool TWS, int FM>
@@ -561,20 +573,27 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
 // w_P^n factors come from two staged tables, w_P^n = hi[n / 128] lo[n % 128] (one complex
 // product), built on the host in long double.
 
-// pass 1, sparse gather: row pair -> even / odd half lines -> T rows kx (kx parity = half)
-__global__ void __launch_bounds__(kFftWideThreads, 1) row_fwd_split_kernel(const RowFwdArgs a) {
+// One CTA per half line (two CTAs per SM: ~86-111 KB of shared memory each, so one CTA's
+// global phases overlap the other's transform).  Pass 1 needs no exchange (each half yields the
+// outputs kx of its parity); passes 2 and 3 pair the two halves of a line in a 2-CTA cluster and
+// combine them through distributed shared memory.
+constexpr int kSplitThreads = 512;   // the WIDE plan's threads per half line (n <= 4608)
+
+// pass 1, sparse gather: row pair -> this CTA's half line -> T rows kx with kx % 2 == half.
+// The pair's two CTAs (a 2-CTA cluster) split the gather by nodes: each forms the sums of half
+// the pair's active nodes and writes them into both half lines (its own and, over DSMEM, its
+// partner's); the odd half then twists its copy by w_P^x.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) row_fwd_split_kernel(const RowFwdArgs a) {
   extern __shared__ __align__(16) double2 smem[];
-  const int H = a.pl.n, P = 2 * H;
+  cg::cluster_group cl = cg::this_cluster();
+  const int half = (int)cl.block_rank();
+  const int H = a.pl.n;
   const int nthr = a.pl.nthr;
-  const int line = threadIdx.x / nthr;
-  const int tl = threadIdx.x - line * nthr;
-  const int pl_ = line >> 1, half = line & 1;
-  const int t2 = tl + half * nthr, n2 = 2 * nthr;   // the pair's threads
+  const int tl = threadIdx.x;
+  const int pidx = blockIdx.x >> 1;
   const int b = blockIdx.y;
-  double2* be = smem + (size_t)(2 * pl_) * H;
-  double2* bo = be + H;
-  double2* buf = half ? bo : be;
-  const int pidx = blockIdx.x * a.lpc + pl_;
+  double2* buf = smem;
+  double* bo_remote = (double*)cl.map_shared_rank(buf, half ^ 1);
   const int ya = 2 * pidx;
   const bool va = ya < a.nrows;
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
@@ -582,7 +601,7 @@ __global__ void __launch_bounds__(kFftWideThreads, 1) row_fwd_split_kernel(const
   pdl_wait();
   const SparseSrc& g = a.sp;
   const double* __restrict__ cb = g.c + (int64_t)b * g.c_stride;
-  double* __restrict__ prod = (double*)(smem + a.prod_off) + (size_t)pl_ * 2 * a.prod_cap;
+  double* __restrict__ prod = (double*)(smem + a.prod_off);
   int2* __restrict__ nrec = (int2*)(prod + a.prod_cap);
   for (int x = tl; x < H; x += nthr) buf[x] = make_double2(0.0, 0.0);
   int4 P0 = make_int4(0, 0, 0, 0), P1 = P0;
@@ -592,206 +611,232 @@ __global__ void __launch_bounds__(kFftWideThreads, 1) row_fwd_split_kernel(const
   }
   const int n0 = P0.x, n1 = P0.y, e0 = P0.z;
   const int nn = P1.x - n0;
-  const int cnt = P1.z - e0;
+  // this CTA's nodes [kA, kB) and their contributions [eA, eB) (relative to e0)
+  const int kA = half ? (nn + 1) / 2 : 0, kB = half ? nn : (nn + 1) / 2;
+  const int eA = kA < nn ? (kA ? __ldg(&g.node_off[n0 + kA]) - e0 : 0) : (P1.z - e0);
+  const int eB = kB ? __ldg(&g.node_off[n0 + kB]) - e0 : 0;
+  const int cnt = max(eB - eA, 0), nk = kB - kA;
   const int rowq = ya * g.M1;
   constexpr int U = 4;
-  const int m = max(cnt, nn);
-  for (int i0 = t2; i0 < m; i0 += U * n2) {
+  const int m = max(cnt, nk);
+  for (int i0 = tl; i0 < m; i0 += U * nthr) {
     double w[U];
     int ci[U], nq[U], ne[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int i = i0 + u * n2;
-      w[u] = i < cnt ? __ldg(&g.ent_wv[e0 + i]) : 0.0;
-      ci[u] = i < cnt ? __ldg(&g.ent_c[e0 + i]) : 0;
-      nq[u] = i < nn ? __ldg(&g.node_q[n0 + i]) : 0;
-      ne[u] = i < nn ? __ldg(&g.node_off[n0 + i + 1]) : 0;
+      const int i = i0 + u * nthr;
+      w[u] = i < cnt ? __ldg(&g.ent_wv[e0 + eA + i]) : 0.0;
+      ci[u] = i < cnt ? __ldg(&g.ent_c[e0 + eA + i]) : 0;
+      nq[u] = i < nk ? __ldg(&g.node_q[n0 + kA + i]) : 0;
+      ne[u] = i < nk ? __ldg(&g.node_off[n0 + kA + i + 1]) : 0;
     }
     double cv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) cv[u] = i0 + u * n2 < cnt ? __ldg(&cb[ci[u]]) : 0.0;
+    for (int u = 0; u < U; ++u) cv[u] = i0 + u * nthr < cnt ? __ldg(&cb[ci[u]]) : 0.0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int i = i0 + u * n2;
+      const int i = i0 + u * nthr;
       if (i < cnt) prod[i] = __dmul_rn(w[u], cv[u]);
-      if (i < nn) {
-        const int odd = n0 + i >= n1;
-        nrec[i] = make_int2(ne[u] - e0, 2 * (nq[u] - rowq - odd * g.M1) + odd);
+      if (i < nk) {
+        const int odd = n0 + kA + i >= n1;
+        nrec[i] = make_int2(ne[u] - e0 - eA, 2 * (nq[u] - rowq - odd * g.M1) + odd);
       }
     }
   }
-  __syncthreads();
-  double* bd = (double*)be;
-  for (int k = t2; k < nn; k += n2) {
+  cl.sync();   // products staged here; both half lines zeroed (remote writes may follow)
+  double* bd = (double*)buf;
+  for (int k = tl; k < nk; k += nthr) {
     const int s0 = k ? nrec[k - 1].x : 0;
     const int2 r = nrec[k];
     double acc = 0.0;
     for (int i = s0; i < r.x; ++i) acc = __dadd_rn(acc, prod[i]);   // (w * c) then add, as np.add.at
     bd[r.y] = acc;
+    bo_remote[r.y] = acc;
   }
-  __syncthreads();
-  if (half)
-    for (int x = tl; x < a.ncols; x += nthr) bo[x] = cmul(be[x], split_w(wt, x));
-  __syncthreads();
-  fft_line<false, true, 1>(buf, pls, tl, 1 + (threadIdx.x / nthr));
-  __syncthreads();   // both halves
+  cl.sync();   // both CTAs' sums are in both lines
+  if (half) {
+    for (int x = tl; x < a.ncols; x += nthr) buf[x] = cmul(buf[x], split_w(wt, x));
+    __syncthreads();
+  }
+  fft_line<false, true, 1>(buf, pls, tl);
   pdl_trigger();
-  // Z[k] of the full transform: k even -> be[k / 2], k odd -> bo[(k - 1) / 2]; U / V split as
-  // in row_fwd_kernel with conj Z[P - k] from the same half
-  const int nr = 2 * a.lpc;
+  // Z[kx], kx = 2 mm + half, is buf[mm]; conj Z[P - kx] comes from the same half
   const int Hf = H + 1;
+  const int nkx = (Hf - half + 1) / 2;   // this half's kx count
   double2* T = a.T + (int64_t)b * a.T_bstride;
-  for (int idx = threadIdx.x; idx < Hf * nr; idx += blockDim.x) {
-    const int r = idx % nr, kx = idx / nr;
-    const int l = r >> 1;
-    const int row = 2 * (blockIdx.x * a.lpc + l) + (r & 1);
+  for (int idx = tl; idx < 2 * nkx; idx += nthr) {
+    const int r = idx & 1, mm = idx >> 1;
+    const int kx = 2 * mm + half;
+    const int row = ya + r;
     if (row >= a.nrows) continue;
-    const double2* le = smem + (size_t)(2 * l) * H;
-    double2 z, zc;
-    if ((kx & 1) == 0) {
-      const int mm = kx >> 1;
-      z = le[mm];
-      zc = le[mm ? H - mm : 0];
-    } else {
-      const int mm = (kx - 1) >> 1;
-      z = le[H + mm];
-      zc = le[H + (H - 1 - mm)];
-    }
+    const double2 z = buf[mm];
+    const double2 zc = buf[half ? H - 1 - mm : (mm ? H - mm : 0)];
     double2 o;
-    if ((r & 1) == 0) o = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+    if (r == 0) o = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
     else o = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
     T[(int64_t)kx * a.ldT + row] = o;
   }
-  (void)P;
 }
 
-// pass 2: column kx -> even / odd halves -> x real-even spectrum -> inverse halves -> combine
-// the kept rows -> TMA bulk store
-__global__ void __launch_bounds__(kFftWideThreads, 1) col_split_kernel(const ColArgs a) {
+// U layouts between the column and inverse-row passes: standard U[kx][y] (column pass output
+// contiguous), or pair-blocked when both passes are split-length: element (U row y, column kx) at
+// U[(y / 2) ldp + (kx % 2) 2 hh + 2 (kx / 2) + y % 2], hh = ceil(H1 / 2), ldp = 4 hh -- the
+// inverse-row pass then reads each row pair's parity half as one contiguous run.
+
+// pass 2: column kx, this CTA's half (cluster rank) -> x real-even spectrum -> inverse half;
+// the cluster's two halves are combined over DSMEM, each CTA finishing half the kept rows
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) col_split_kernel(const ColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
-  const int H = a.pl.n, P = 2 * H;
+  cg::cluster_group cl = cg::this_cluster();
+  const int half = (int)cl.block_rank();
+  const int H = a.pl.n;
   const int nthr = a.pl.nthr;
-  const int half = threadIdx.x / nthr;
-  const int tl = threadIdx.x - half * nthr;
+  const int tl = threadIdx.x;
   const int b = blockIdx.y;
-  const int kx = blockIdx.x;
-  double2* be = smem;
-  double2* bo = smem + H;
-  double2* buf = half ? bo : be;
-  double* specs = (double*)(smem + 2 * (size_t)H);
-  uint64_t* bar = (uint64_t*)(specs + a.ldq);
+  const int kx = blockIdx.x >> 1;
+  double2* buf = smem;
+  double* S = (double*)(smem + H);                 // this half's spectrum (ldh)
+  uint64_t* bar = (uint64_t*)(S + a.ldh);
   const double2* Tb = a.T + (int64_t)b * a.T_bstride;
-  if (threadIdx.x == 0) mbar_init(bar, 1);
+  if (tl == 0) mbar_init(bar, 1);
   __syncthreads();
-  const uint32_t colb = (uint32_t)a.nin * 16u, specb = (uint32_t)a.ldq * 8u;
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(bar, colb + specb);
-    bulk_g2s(specs, a.spec_q + (int64_t)kx * a.ldq, specb, bar);
+  const uint32_t colb = (uint32_t)a.nin * 16u, sb = (uint32_t)a.ldh * 8u;
+  if (tl == 0) {
+    mbar_expect_tx(bar, colb + sb);
+    bulk_g2s(S, a.spec_s + ((int64_t)kx * 2 + half) * a.ldh, sb, bar);
   }
   pdl_wait();
-  if (threadIdx.x == 0) bulk_g2s(be, Tb + (int64_t)kx * a.ldT, colb, bar);
+  if (tl == 0) bulk_g2s(buf, Tb + (int64_t)kx * a.ldT, colb, bar);
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
   for (int y = a.nin + tl; y < H; y += nthr) buf[y] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
-  __syncthreads();   // staged twiddle tables visible
-  if (half)
-    for (int y = tl; y < a.nin; y += nthr) bo[y] = cmul(be[y], split_w(wt, y));
   __syncthreads();
-  fft_line<false, true, 1>(buf, pls, tl, 1 + (threadIdx.x / nthr));
-  // spectrum: S[k] = specs[min(k, P - k)], k = 2m + half
-  for (int mm = tl; mm < H; mm += nthr) {
-    const int k = 2 * mm + half;
-    buf[mm] = cscale(buf[mm], specs[min(k, P - k)]);
+  if (half) {
+    for (int y = tl; y < a.nin; y += nthr) buf[y] = cmul(buf[y], split_w(wt, y));
+    __syncthreads();
   }
-  group_sync(1 + half, nthr);
-  fft_line<true, true, 1>(buf, pls, tl, 1 + (threadIdx.x / nthr));
-  __syncthreads();   // both halves
+  fft_line<false, true, 1>(buf, pls, tl);
+  // S[k] for k = 2 mm + half: S_half[min(mm, H - half - mm)]
+  for (int mm = tl; mm < H; mm += nthr) buf[mm] = cscale(buf[mm], S[min(mm, H - half - mm)]);
+  __syncthreads();
+  fft_line<true, true, 1>(buf, pls, tl);
   pdl_trigger();
-  for (int y = a.row0 + threadIdx.x; y < a.row0 + a.nout; y += blockDim.x) {
-    const double2 w = split_w(wt, y);
-    be[y] = cadd(be[y], cmulc(bo[y], w));   // + w^-y (inverse half)
+  cl.sync();   // both halves transformed
+  const double2* other = cl.map_shared_rank(buf, half ^ 1);
+  if (a.upair) {   // pair-blocked U: each thread finishes one U row pair (32 contiguous bytes)
+    const int nq = (a.nout + 1) >> 1, qm = (nq + 1) >> 1;
+    const int q0 = half ? qm : 0, q1 = half ? nq : qm;
+    double2* Ub = a.U + (int64_t)b * a.U_bstride + (int64_t)(kx & 1) * 2 * a.hh + 2 * (kx >> 1);
+    for (int q = q0 + tl; q < q1; q += nthr) {
+      double2 v[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int yo = 2 * q + r;
+        v[r] = make_double2(0.0, 0.0);
+        if (yo < a.nout) {
+          const int y = a.row0 + yo;
+          const double2 e = half ? other[y] : buf[y];
+          const double2 o = half ? buf[y] : other[y];
+          v[r] = cadd(e, cmulc(o, split_w(wt, y)));   // + w^-y (inverse half)
+        }
+      }
+      double2* dst = Ub + (int64_t)q * a.ldp;
+      dst[0] = v[0];
+      dst[1] = v[1];
+    }
+    cl.sync();   // the partner's remote reads of this CTA's rows are done
+    return;
+  }
+  const int mid = a.row0 + ((a.nout + 1) >> 1);
+  const int y0 = half ? mid : a.row0, y1 = half ? a.row0 + a.nout : mid;
+  for (int y = y0 + tl; y < y1; y += nthr) {
+    const double2 e = half ? other[y] : buf[y];
+    const double2 o = half ? buf[y] : other[y];
+    buf[y] = cadd(e, cmulc(o, split_w(wt, y)));   // + w^-y (inverse half)
   }
   fence_async_smem();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    bulk_s2g(a.U + (int64_t)b * a.U_bstride + (int64_t)kx * a.ldU, be + a.row0, (uint32_t)a.nout * 16u);
+  cl.sync();   // the partner's remote reads of this CTA's rows are done
+  if (tl == 0 && y1 > y0) {
+    bulk_s2g(a.U + (int64_t)b * a.U_bstride + (int64_t)kx * a.ldU + (y0 - a.row0), buf + y0,
+             (uint32_t)(y1 - y0) * 16u);
     bulk_commit();
     bulk_wait_read0();
   }
   __syncthreads();
 }
 
-// pass 3: Hermitian pair of interior rows -> even / odd half spectra -> inverse halves ->
-// combine the kept columns -> fixed-part / draw epilogue
-__global__ void __launch_bounds__(kFftWideThreads, 1) row_inv_split_kernel(const RowInvArgs a) {
+// pass 3: Hermitian pair of interior rows -> this CTA's half spectrum (Z[k], k % 2 == half) ->
+// inverse half; the cluster combines the halves over DSMEM, each CTA finishing half the
+// kept columns (fixed-part / draw epilogue)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) row_inv_split_kernel(const RowInvArgs a) {
   extern __shared__ __align__(16) double2 smem[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int half = (int)cl.block_rank();
   const int H = a.pl.n;
   const int nthr = a.pl.nthr;
-  const int line = threadIdx.x / nthr;
-  const int tl = threadIdx.x - line * nthr;
-  const int pl_ = line >> 1, half = line & 1;
-  const int t2 = tl + half * nthr, n2 = 2 * nthr;
+  const int tl = threadIdx.x;
   const int b = blockIdx.y;
   const int Hf = H + 1;
+  const int ya = 2 * (blockIdx.x >> 1);
   const double2* U = a.U + (int64_t)b * a.U_bstride;
+  double2* buf = smem;
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
   pdl_wait();
-  // gather: Z[k] = A[k] + i B[k] (k < Hf) and its Hermitian mirror Z[P - k]; even k -> be, odd -> bo
-  const int tot = a.lpc * Hf;
+  // gather: k = 2 mm + half < Hf -> Z[k] at buf[mm]; its mirror Z[P - k] (1 <= k <= H - 1) at
+  // buf[H - mm] (even) / buf[H - 1 - mm] (odd)
+  const int nk = (Hf - half + 1) / 2;
+  const bool vA = ya < a.nrows, vB = ya + 1 < a.nrows;
   constexpr int D = 8;
-  for (int base = threadIdx.x; base < tot; base += D * blockDim.x) {
+  for (int base = tl; base < nk; base += D * nthr) {
     double2 A[D], B[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const int idx = base + d * blockDim.x;
+      const int mm = base + d * nthr;
       A[d] = B[d] = make_double2(0.0, 0.0);
-      if (idx < tot) {
-        const int l = idx % a.lpc, k = idx / a.lpc;
-        const int ya = 2 * (blockIdx.x * a.lpc + l);
-        const double2* u = U + (int64_t)k * a.ldU + ya;
-        if (ya < a.nrows) A[d] = u[0];
-        if (ya + 1 < a.nrows) B[d] = u[1];
+      if (mm < nk) {
+        if (a.upair) {   // the pair's parity run: contiguous 32-byte records
+          const double2* u = U + (int64_t)(ya >> 1) * a.ldp + (int64_t)half * 2 * a.hh + 2 * mm;
+          A[d] = u[0];
+          B[d] = u[1];
+        } else {
+          const double2* u = U + (int64_t)(2 * mm + half) * a.ldU + ya;
+          if (vA) A[d] = u[0];
+          if (vB) B[d] = u[1];
+        }
       }
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const int idx = base + d * blockDim.x;
-      if (idx < tot) {
-        const int l = idx % a.lpc, k = idx / a.lpc;
-        double2* le = smem + (size_t)(2 * l) * H;
-        const double2 z = make_double2(A[d].x - B[d].y, A[d].y + B[d].x);
-        const double2 zc = make_double2(A[d].x + B[d].y, B[d].x - A[d].y);
-        if ((k & 1) == 0) {
-          le[k >> 1] = z;
-          if (k >= 2 && k <= H - 1) le[H - (k >> 1)] = zc;
-        } else {
-          const int mm = (k - 1) >> 1;
-          le[H + mm] = z;
-          if (k <= H - 1) le[H + (H - 1 - mm)] = zc;
-        }
+      const int mm = base + d * nthr;
+      if (mm < nk) {
+        const int k = 2 * mm + half;
+        buf[mm] = make_double2(A[d].x - B[d].y, A[d].y + B[d].x);
+        if (k >= 1 && k <= H - 1) buf[half ? H - 1 - mm : H - mm] = make_double2(A[d].x + B[d].y, B[d].x - A[d].y);
       }
     }
   }
   __syncthreads();
-  double2* buf = smem + (size_t)line * H;
-  fft_line<true, true, 1>(buf, pls, tl, 1 + (threadIdx.x / nthr));
-  __syncthreads();   // both halves
-  const double2* be = smem + (size_t)(2 * pl_) * H;
-  const double2* bo = be + H;
-  const int ya = 2 * (blockIdx.x * a.lpc + pl_);
+  fft_line<true, true, 1>(buf, pls, tl);
+  cl.sync();   // both halves transformed
+  const double2* other = cl.map_shared_rank(buf, half ^ 1);
   const double* beta = a.beta ? a.beta + (int64_t)b * a.p : nullptr;
   const double* gb = a.g ? a.g + (int64_t)b * a.g_bstride : nullptr;
   const int pc = a.epi == EPI_COV ? a.p : 0;
   double* out = a.out + (int64_t)b * a.out_bstride;
-  for (int e = t2; e < 2 * a.ncols; e += n2) {
-    const int which = e >= a.ncols;
-    const int x = e - which * a.ncols;
+  const int xm = (a.ncols + 1) >> 1;
+  const int x0 = half ? xm : 0, x1 = half ? a.ncols : xm;
+  const int w = x1 - x0;
+  for (int e = tl; e < 2 * w; e += nthr) {
+    const int which = e >= w;
+    const int x = x0 + e - which * w;
     const int y = ya + which;
     if (y >= a.nrows) continue;
     const int nn = a.col0 + x;
-    const double2 z = cadd(be[nn], cmulc(bo[nn], split_w(wt, nn)));
+    const double2 ev = half ? other[nn] : buf[nn];
+    const double2 ov = half ? buf[nn] : other[nn];
+    const double2 z = cadd(ev, cmulc(ov, split_w(wt, nn)));
     double v = which ? z.y : z.x;
     if (a.epi == EPI_SCALAR) {
       v = v + beta[0];
@@ -804,6 +849,7 @@ __global__ void __launch_bounds__(kFftWideThreads, 1) row_inv_split_kernel(const
     if (gb) v = gb[(int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + x] - v;
     out[(int64_t)y * a.ldo + x] = v;
   }
+  cl.sync();   // the partner's remote reads are done before this CTA's shared memory goes away
 }
 
 // ----------------------------------------------------------------- launches
@@ -914,7 +960,7 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
   return Status::ok();
 }
 
-// split-length launches (see row_fwd_split_kernel); false when the layout does not fit
+// split-length launches (see row_fwd_split_kernel); *done = false when the layout does not fit
 static inline size_t split_tail(size_t bytes, const FftPlan& pl, SplitTw* sw, int* tw_off) {
   *tw_off = tw_slot(bytes);
   bytes = (size_t)*tw_off * 16 + (size_t)pl.ntw * 16;
@@ -926,15 +972,15 @@ static Status launch_row_fwd_split(const RowFwdArgs& a0, int batch, cudaStream_t
   RowFwdArgs a = a0;
   *done = false;
   a.lpc = 1;
-  if (2 * a.pl.nthr > kFftWideThreads) return Status::ok();
-  size_t smem = sizeof(double2) * 2 * (size_t)a.pl.n;
+  if (a.pl.nthr > kSplitThreads) return Status::ok();
+  size_t smem = sizeof(double2) * (size_t)a.pl.n;
   a.prod_off = tw_slot(smem);
   smem = (size_t)a.prod_off * 16 + sizeof(double) * 2 * (size_t)a.prod_cap;
   smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
   if (smem > kSmemMax) return Status::ok();
   RK_TRY(set_smem_attr((const void*)row_fwd_split_kernel, smem));
-  const dim3 grid((unsigned)((a.nrows + 1) / 2), (unsigned)batch);
-  RK_CUDA_TRY(launch_pdl(row_fwd_split_kernel, grid, dim3(2 * a.pl.nthr), smem, st, a));
+  const dim3 grid((unsigned)(2 * ((a.nrows + 1) / 2)), (unsigned)batch);
+  row_fwd_split_kernel<<<grid, a.pl.nthr, smem, st>>>(a);
   count_launch();
   RK_LAUNCH_CHECK();
   *done = true;
@@ -945,13 +991,14 @@ static Status launch_col_split(const ColArgs& a0, int batch, cudaStream_t st, bo
   ColArgs a = a0;
   *done = false;
   a.lpc = 1;
-  if (2 * a.pl.nthr > kFftWideThreads) return Status::ok();
-  size_t smem = sizeof(double2) * 2 * (size_t)a.pl.n + sizeof(double) * (size_t)a.ldq + 16;
+  if (a.pl.nthr > kSplitThreads) return Status::ok();
+  if (!a.spec_s) return Status::ok();
+  size_t smem = sizeof(double2) * (size_t)a.pl.n + sizeof(double) * (size_t)a.ldh + 16;
   smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
   if (smem > kSmemMax) return Status::ok();
   RK_TRY(set_smem_attr((const void*)col_split_kernel, smem));
-  const dim3 grid((unsigned)a.ncols, (unsigned)batch);
-  RK_CUDA_TRY(launch_pdl(col_split_kernel, grid, dim3(2 * a.pl.nthr), smem, st, a));
+  const dim3 grid((unsigned)(2 * a.ncols), (unsigned)batch);
+  col_split_kernel<<<grid, a.pl.nthr, smem, st>>>(a);
   count_launch();
   RK_LAUNCH_CHECK();
   *done = true;
@@ -962,13 +1009,13 @@ static Status launch_row_inv_split(const RowInvArgs& a0, int batch, cudaStream_t
   RowInvArgs a = a0;
   *done = false;
   a.lpc = 1;
-  if (2 * a.pl.nthr > kFftWideThreads) return Status::ok();
-  size_t smem = sizeof(double2) * 2 * (size_t)a.pl.n;
+  if (a.pl.nthr > kSplitThreads) return Status::ok();
+  size_t smem = sizeof(double2) * (size_t)a.pl.n;
   smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
   if (smem > kSmemMax) return Status::ok();
   RK_TRY(set_smem_attr((const void*)row_inv_split_kernel, smem));
-  const dim3 grid((unsigned)((a.nrows + 1) / 2), (unsigned)batch);
-  RK_CUDA_TRY(launch_pdl(row_inv_split_kernel, grid, dim3(2 * a.pl.nthr), smem, st, a));
+  const dim3 grid((unsigned)(2 * ((a.nrows + 1) / 2)), (unsigned)batch);
+  row_inv_split_kernel<<<grid, a.pl.nthr, smem, st>>>(a);
   count_launch();
   RK_LAUNCH_CHECK();
   *done = true;
@@ -1101,11 +1148,20 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
                             const HostIo* hio = nullptr, const SparseSrc* sp = nullptr) {
   const int64_t ldT = round_even(s->M2);
   const int64_t ldU = round_even(nout);
+  // pair-blocked U when both the column and the inverse-row passes are split-length
+  const bool split2 = s->h2v.v[2].n && s->spec_s && row0 + nout <= s->p2 / 2;
+  const bool split3 = s->h1v.v[2].n && col0 + ncols <= s->p1 / 2;
+  // measured on cfg5 (B200): pair-blocked U takes pass 3 from 0.336 to 0.291 ms but pass 2's
+  // scattered 32-byte stores cost more (0.697 -> 0.813 ms); off unless RK_UPAIR=1
+  static const bool upair_env = getenv("RK_UPAIR") && atoi(getenv("RK_UPAIR")) == 1;
+  const bool upair = upair_env && split2 && split3;
+  const int hh = (s->H1 + 1) / 2;
+  const int64_t U_bstride = (int64_t)(s->H1 + 1) * ldU;   // holds either layout
   double2 *T = nullptr, *U = nullptr;
   const bool own = !(ws && batch == 1);
   if (own) {
     RK_TRY(scratch_alloc((void**)&T, sizeof(double2) * (size_t)s->H1 * ldT * batch, st));
-    RK_TRY(scratch_alloc((void**)&U, sizeof(double2) * (size_t)s->H1 * ldU * batch, st));
+    RK_TRY(scratch_alloc((void**)&U, sizeof(double2) * (size_t)U_bstride * batch, st));
   } else {
     T = ws->T;
     U = ws->U;
@@ -1146,6 +1202,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     RowFwdArgs rs = ra;
     rs.pl = s->h1v.v[2];
     rs.sw = s->sw1;
+    rs.prod_cap = (int)((s->max_half_ent + 1) & ~int64_t(1));   // each CTA stages half the nodes
     RK_TRY(launch_row_fwd_split(rs, batch, st, &done));
   }
   if (!done) RK_TRY(launch_row_fwd(sp ? SRC_SPARSE : SRC_ROWS, ra, batch, st));
@@ -1164,12 +1221,17 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   ca.nout = nout;
   ca.U = U;
   ca.ldU = ldU;
-  ca.U_bstride = (int64_t)s->H1 * ldU;
+  ca.U_bstride = U_bstride;
   done = false;
-  if (s->h2v.v[2].n && row0 + nout <= s->p2 / 2) {   // split-length column pass
+  if (split2) {   // split-length column pass
     ColArgs cs = ca;
     cs.pl = s->h2v.v[2];
     cs.sw = s->sw2;
+    cs.spec_s = s->spec_s;
+    cs.ldh = s->ldh;
+    cs.upair = upair;
+    cs.hh = hh;
+    cs.ldp = 4LL * hh;
     RK_TRY(launch_col_split(cs, batch, st, &done));
   }
   if (!done) RK_TRY(launch_col(0, ca, batch, st));
@@ -1183,13 +1245,15 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   ia.U_bstride = ca.U_bstride;
   ia.col0 = col0;
   ia.ncols = ncols;
-  const bool split3 = s->h1v.v[2].n && col0 + ncols <= s->p1 / 2;
   if (!hio) {
     done = false;
     if (split3) {   // split-length inverse row pass
       RowInvArgs is = ia;
       is.pl = s->h1v.v[2];
       is.sw = s->sw1;
+      is.upair = upair;
+      is.hh = hh;
+      is.ldp = 4LL * hh;
       RK_TRY(launch_row_inv_split(is, batch, st, &done));
     }
     if (!done) RK_TRY(launch_row_inv(ia, batch, st));
@@ -1199,7 +1263,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
       const int r1 = std::min(nout, r0 + per);
       RowInvArgs ck = ia;
       ck.nrows = r1 - r0;
-      ck.U = U + r0;
+      ck.U = upair && split3 ? U + (int64_t)(r0 / 2) * 4LL * hh : U + r0;   // r0 is even
       ck.out = ia.out + (int64_t)r0 * ia.ldo;
       if (ck.xg) ck.xg = ia.xg + (int64_t)r0 * ncols * ia.p;
       ck.g_row0 = ia.g_row0 + r0;
@@ -1210,6 +1274,9 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
         RowInvArgs is = ck;
         is.pl = s->h1v.v[2];
         is.sw = s->sw1;
+        is.upair = upair;
+        is.hh = hh;
+        is.ldp = 4LL * hh;
         RK_TRY(launch_row_inv_split(is, 1, st, &done));
       }
       if (!done) RK_TRY(launch_row_inv(ck, 1, st));
@@ -1307,7 +1374,7 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
   w->serial = ++serial;
   const int64_t ldT = round_even(s->M2), ldU = round_even(s->m2);
   RK_CUDA_TRY(cudaMalloc(&w->T, sizeof(double2) * (size_t)s->H1 * ldT));
-  RK_CUDA_TRY(cudaMalloc(&w->U, sizeof(double2) * (size_t)s->H1 * ldU));
+  RK_CUDA_TRY(cudaMalloc(&w->U, sizeof(double2) * (size_t)(s->H1 + 1) * ldU));   // either U layout
   // c and beta staged back to back (one upload per host-path call): beta at an even offset
   const int64_t boff = (std::max<int64_t>(s->n, 2) + 1) & ~int64_t(1);
   RK_CUDA_TRY(cudaMalloc(&w->c_in, sizeof(double) * (boff + 16)));

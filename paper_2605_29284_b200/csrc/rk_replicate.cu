@@ -28,14 +28,14 @@ struct SetupHdr {
   uint64_t magic;
   rk_model model;
   rk_grid grid;
-  int32_t L, bs, M, M1, M2, m1, m2, p1, p2, H1, Q2, pblk_cap;
-  int64_t n, nnodes, max_pair_ent, pblk_stride;
+  int32_t L, bs, M, M1, M2, m1, m2, p1, p2, H1, Q2, pblk_cap, ldh;
+  int64_t n, nnodes, max_pair_ent, max_half_ent, pblk_stride;
   double px0, py0, cond_var_min;
   int32_t emb_ready, ps1, ps2, doubled, hs1, qs2;
   int64_t field_bytes[24];
   int32_t nfields, has_field[24];
 };
-constexpr uint64_t kSetupMagic = 0x52'4B'53'45'54'55'50'31ULL;   // "RKSETUP1"
+constexpr uint64_t kSetupMagic = 0x52'4B'53'45'54'55'50'32ULL;   // "RKSETUP2"
 
 struct Field {
   void** slot;
@@ -64,6 +64,7 @@ std::vector<Field> setup_fields(rk_setup* s) {
       {(void**)&s->pair_info, sizeof(int4) * (npairs + 1)},
       {(void**)&s->pblk, (size_t)(s->pblk_stride * npairs)},
       {(void**)&s->spec_q, sizeof(double) * (size_t)s->H1 * s->Q2},
+      {(void**)&s->spec_s, sizeof(double) * (size_t)s->H1 * 2 * s->ldh},
       {(void**)&s->kn_chol_dev, sizeof(double) * M * M},
       {(void**)&s->emb.root_q, sizeof(double) * (size_t)s->emb.hs1 * s->emb.qs2},
   };
@@ -79,8 +80,9 @@ SetupHdr header_of(rk_setup* s) {
   h.model = s->model;
   h.grid = s->grid;
   h.L = s->L; h.bs = s->bs; h.M = s->M; h.M1 = s->M1; h.M2 = s->M2; h.m1 = s->m1; h.m2 = s->m2;
-  h.p1 = s->p1; h.p2 = s->p2; h.H1 = s->H1; h.Q2 = s->Q2; h.pblk_cap = s->pblk_cap;
-  h.n = s->n; h.nnodes = s->nnodes; h.max_pair_ent = s->max_pair_ent; h.pblk_stride = s->pblk_stride;
+  h.p1 = s->p1; h.p2 = s->p2; h.H1 = s->H1; h.Q2 = s->Q2; h.pblk_cap = s->pblk_cap; h.ldh = s->ldh;
+  h.n = s->n; h.nnodes = s->nnodes; h.max_pair_ent = s->max_pair_ent; h.max_half_ent = s->max_half_ent;
+  h.pblk_stride = s->pblk_stride;
   h.px0 = s->px0; h.py0 = s->py0; h.cond_var_min = s->cond_var_min;
   h.emb_ready = s->emb.ready; h.ps1 = s->emb.ps1; h.ps2 = s->emb.ps2; h.doubled = s->emb.doubled;
   h.hs1 = s->emb.hs1; h.qs2 = s->emb.qs2;
@@ -107,8 +109,9 @@ Status setup_from_header(const SetupHdr& h, rk_setup* s) {
   s->mat = make_matern_dev(h.model);
   s->grid = h.grid;
   s->L = h.L; s->bs = h.bs; s->M = h.M; s->M1 = h.M1; s->M2 = h.M2; s->m1 = h.m1; s->m2 = h.m2;
-  s->p1 = h.p1; s->p2 = h.p2; s->H1 = h.H1; s->Q2 = h.Q2; s->pblk_cap = h.pblk_cap;
-  s->n = h.n; s->nnodes = h.nnodes; s->max_pair_ent = h.max_pair_ent; s->pblk_stride = h.pblk_stride;
+  s->p1 = h.p1; s->p2 = h.p2; s->H1 = h.H1; s->Q2 = h.Q2; s->pblk_cap = h.pblk_cap; s->ldh = h.ldh;
+  s->n = h.n; s->nnodes = h.nnodes; s->max_pair_ent = h.max_pair_ent; s->max_half_ent = h.max_half_ent;
+  s->pblk_stride = h.pblk_stride;
   s->px0 = h.px0; s->py0 = h.py0; s->cond_var_min = h.cond_var_min;
   RK_TRY(setup_plans(s));
   Embedding& e = s->emb;
