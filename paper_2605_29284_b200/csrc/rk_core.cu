@@ -852,6 +852,227 @@ __global__ void __launch_bounds__(256, 2) weights_kernel_ob(WArgs a) {
   }
 }
 
+// ----------------------------------------------------------------- K1 on FP64 tensor cores
+// weights_kernel_mma<L>: a warp solves 8 observations at once as an (MP x 8) right-hand-side
+// block Y (MP = M rounded up to a multiple of 8; padded rows have k = 0 and a unit diagonal, so
+// they stay exactly 0), blocked by 8-row tiles:
+//   forward  L y = k : for tile t: substitution inside the 8 x 8 diagonal block (column
+//                      oriented, reciprocal diagonal), then Y_u -= L_ut Y_t for every u > t as
+//                      two mma.m8n8k4 f64 (DMMA) per tile pair;
+//   backward L'w = y : the same from the last tile up with L' (its blocks staged transposed).
+// Y lives in the DMMA accumulator layout (lane = 4 g + q holds rows g, observations 2q, 2q+1 of
+// every tile); a solved tile becomes the B operand of the updates by one shuffle per register.
+// This is a blocked (backward-stable) TRSM, not the explicit inverse (hard part 1);
+// each observation's solve depends only on its own column (DMMA columns are independent), so a
+// weight row does not depend on which observations share the warp.  n (2 M^2) flops go from
+// ~2440 issued instructions per observation (shuffle -> multiply -> FMA chains, weights_kernel_ob)
+// to ~300, the off-diagonal work on the tensor pipe.
+__device__ __forceinline__ void dmma884_w(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int L>
+struct WMma {
+  static constexpr int BS = 2 * L, M = BS * BS, T = (M + 7) / 8, MP = 8 * T;
+  static constexpr int FRAG = T * T * 2 * 32;   // doubles per A-fragment table
+  static constexpr int DLD = 72;                // padded 8 x 8 diagonal block: [g * 9 + r]
+  static constexpr size_t smem_bytes() { return sizeof(double) * (2 * FRAG + 2 * T * DLD + MP + 8 * MP * 8); }
+};
+
+template <int L>
+__global__ void __launch_bounds__(256, 2) weights_kernel_mma(WArgs a) {
+  using W = WMma<L>;
+  constexpr int BS = W::BS, M = W::M, T = W::T, MP = W::MP;
+  extern __shared__ double wsm[];
+  double* AF = wsm;                    // forward A fragments: -L[8u + g][8t + 4kb + q]
+  double* AB = AF + W::FRAG;           // backward A fragments: -L[8t + 4kb + q][8u + g]
+  double* DF = AB + W::FRAG;           // diagonal blocks: DF[t][g * 9 + r] = L[8t + g][8t + r]
+  double* DB = DF + T * W::DLD;        // transposed:      DB[t][g * 9 + r] = L[8t + r][8t + g]
+  double* rd = DB + T * W::DLD;        // 1 / L[m][m] (1 on padded rows)
+  double* kw = rd + MP + (threadIdx.x >> 5) * MP * 8;   // this warp's cross covariances [m][obs]
+  auto Lat = [&](int r, int c) -> double {
+    if (r < M && c < M) return a.chol[r * M + c];
+    return r == c ? 1.0 : 0.0;
+  };
+  for (int e = threadIdx.x; e < T * T * 2 * 32; e += blockDim.x) {
+    const int ln = e & 31, kb = (e >> 5) & 1, tu = e >> 6, t = tu % T, u = tu / T;
+    const int g = ln >> 2, q = ln & 3;
+    AF[e] = -Lat(8 * u + g, 8 * t + 4 * kb + q);
+    AB[e] = -Lat(8 * t + 4 * kb + q, 8 * u + g);
+  }
+  for (int e = threadIdx.x; e < T * 64; e += blockDim.x) {
+    const int t = e >> 6, g = (e >> 3) & 7, r = e & 7;
+    DF[t * W::DLD + g * 9 + r] = Lat(8 * t + g, 8 * t + r);
+    DB[t * W::DLD + g * 9 + r] = Lat(8 * t + r, 8 * t + g);
+  }
+  for (int m = threadIdx.x; m < MP; m += blockDim.x) rd[m] = 1.0 / Lat(m, m);
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int64_t ntask = (a.n + 7) / 8;
+  const int64_t stride = (int64_t)gridDim.x * wpb;
+  const int64_t trips = (ntask + stride - 1) / stride;
+  for (int64_t it = 0; it < trips; ++it) {
+    const int64_t i0 = ((int64_t)blockIdx.x * wpb + warp + it * stride) * 8;
+    __syncwarp();   // the previous trip's reads of kw are done
+    // this lane's two observations 2q, 2q + 1 of the task (accumulator columns) and, for the
+    // cross covariances, observation lane & 7
+    bool live[2], on_node[2];
+    int xlo[2], ylo[2];
+    double xs[2], ys[2];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int o = j < 2 ? 2 * q + j : (lane & 7);
+      const int64_t i = i0 + o;
+      bool lv = i < a.n;
+      const double x = lv ? a.obs[2 * i] : a.px0, y = lv ? a.obs[2 * i + 1] : a.py0;
+      const double tx = __ddiv_rn(__dsub_rn(x, a.px0), a.hx);
+      const double ty = __ddiv_rn(__dsub_rn(y, a.py0), a.hy);
+      int cx = 0, cy = 0;
+      if (lv && !(tx >= -1.0e-9 && tx <= a.hix && ty >= -1.0e-9 && ty <= a.hiy)) {
+        if (j == 2 && lane < 8) atomicMin(&a.err[0], (int)i);
+        lv = false;
+      }
+      if (lv) {
+        cx = snap_cell(tx);
+        cy = snap_cell(ty);
+        if (cx - (L - 1) < 0 || cy - (L - 1) < 0 || cx + L > a.M1 - 1 || cy + L > a.M2 - 1) {
+          if (j == 2 && lane < 8) atomicMin(&a.err[1], (int)i);
+          lv = false;
+        }
+      }
+      if (j < 2) {
+        live[j] = lv;
+        xlo[j] = cx - (L - 1);
+        ylo[j] = cy - (L - 1);
+        const double ox = __dsub_rn(tx, (double)cx), oy = __dsub_rn(ty, (double)cy);
+        on_node[j] = fabs(ox) <= 1.0e-9 && fabs(oy) <= 1.0e-9;
+      } else {
+        // cross covariances of observation lane & 7 to block rows m = lane / 8 + 4 k, staged in
+        // the warp's (MP x 8) smem block (four independent evaluations per iteration; the Matern
+        // code stays out of the register-resident solve)
+        int bad = 0;
+#pragma unroll 4
+        for (int m = lane >> 3; m < MP; m += 4) {
+          double kv = 0.0;
+          if (lv && m < M) {
+            const int r = m / BS, c = m % BS;
+            const double nx = __dadd_rn(a.px0, __dmul_rn((double)(cx - (L - 1) + c), a.hx));
+            const double ny = __dadd_rn(a.py0, __dmul_rn((double)(cy - (L - 1) + r), a.hy));
+            kv = matern_cov(a.P, hypot(__dsub_rn(nx, x), __dsub_rn(ny, y)), &bad);
+          }
+          kw[m * 8 + (lane & 7)] = kv;
+        }
+        if (bad) atomicOr(&a.err[2], 1);
+      }
+    }
+    __syncwarp();
+    double Y[T][2];
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) Y[t][j] = kw[(8 * t + g) * 8 + 2 * q + j];
+    if (it == 0) __syncthreads();   // factor tables staged (their loads overlap the first k)
+    // forward substitution L y = k
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const double* D = DF + t * W::DLD + g * 9;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const double s = rd[8 * t + r];
+        const double y0 = __shfl_sync(0xffffffffu, Y[t][0] * s, 4 * r + q);
+        const double y1 = __shfl_sync(0xffffffffu, Y[t][1] * s, 4 * r + q);
+        if (g == r) {
+          Y[t][0] = y0;
+          Y[t][1] = y1;
+        } else if (g > r) {
+          const double l = D[r];
+          Y[t][0] = fma(-l, y0, Y[t][0]);
+          Y[t][1] = fma(-l, y1, Y[t][1]);
+        }
+      }
+      if (t + 1 < T) {
+        double bf[2];
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb) {
+          const int src = (4 * kb + q) * 4 + (g >> 1);
+          const double v0 = __shfl_sync(0xffffffffu, Y[t][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, Y[t][1], src);
+          bf[kb] = (g & 1) ? v1 : v0;
+        }
+#pragma unroll
+        for (int u = t + 1; u < T; ++u)
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb)
+            dmma884_w(Y[u][0], Y[u][1], AF[((u * T + t) * 2 + kb) * 32 + lane], bf[kb]);
+      }
+    }
+    // back substitution L' w = y
+#pragma unroll
+    for (int t = T - 1; t >= 0; --t) {
+      const double* D = DB + t * W::DLD + g * 9;
+#pragma unroll
+      for (int r = 7; r >= 0; --r) {
+        const double s = rd[8 * t + r];
+        const double w0 = __shfl_sync(0xffffffffu, Y[t][0] * s, 4 * r + q);
+        const double w1 = __shfl_sync(0xffffffffu, Y[t][1] * s, 4 * r + q);
+        if (g == r) {
+          Y[t][0] = w0;
+          Y[t][1] = w1;
+        } else if (g < r) {
+          const double l = D[r];
+          Y[t][0] = fma(-l, w0, Y[t][0]);
+          Y[t][1] = fma(-l, w1, Y[t][1]);
+        }
+      }
+      if (t > 0) {
+        double bf[2];
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb) {
+          const int src = (4 * kb + q) * 4 + (g >> 1);
+          const double v0 = __shfl_sync(0xffffffffu, Y[t][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, Y[t][1], src);
+          bf[kb] = (g & 1) ? v1 : v0;
+        }
+#pragma unroll
+        for (int u = 0; u < t; ++u)
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb)
+            dmma884_w(Y[u][0], Y[u][1], AB[((u * T + t) * 2 + kb) * 32 + lane], bf[kb]);
+      }
+    }
+    // cond_var = sigma2 - w . k (sum over this lane's rows, then over the 8 row groups)
+    double part[2] = {0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) part[j] = fma(Y[t][j], kw[(8 * t + g) * 8 + 2 * q + j], part[j]);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) part[j] += __shfl_xor_sync(0xffffffffu, part[j], o);
+    constexpr int corner = (L - 1) * BS + (L - 1);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (!live[j]) continue;
+      const int64_t i = i0 + 2 * q + j;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int m = 8 * t + g;
+        if (m < M) a.weights[i * M + m] = on_node[j] ? (m == corner ? 1.0 : 0.0) : Y[t][j];
+      }
+      if (g == 0) {
+        double cv = a.P.sigma2 - part[j];
+        if (on_node[j]) cv = 0.0;
+        if (cv < 0.0 && cv > -1.0e-10 * a.P.sigma2) cv = 0.0;
+        a.cond_var[i] = cv;
+        a.base[i] = ylo[j] * a.M1 + xlo[j];
+      }
+    }
+  }
+}
+
 // cell_start[b] = lower_bound(sorted keys, b) for b in [0, nb]
 __global__ void cell_start_kernel(const int32_t* __restrict__ keys, int64_t n, int32_t* cs,
                                   int64_t nb) {
@@ -1251,7 +1472,28 @@ static Status launch_weights(const rk_setup* s, int32_t* base, double* weights, 
       kern<<<nb, 256, wsl, st>>>(wa);
       return Status::ok();
     };
-    if (L == 1) RK_TRY(launch_l(weights_kernel_l<1>));
+    // RK_WEIGHTS_MMA: the FP64 tensor-core blocked solve (weights_kernel_mma) for L >= 2
+    static const int mma_env = getenv("RK_WEIGHTS_MMA") ? atoi(getenv("RK_WEIGHTS_MMA")) : -1;
+    // default: L >= 3 with enough observations to fill the GPU with 8-observation tasks (measured:
+    // cfg5 L = 4 0.204 -> 0.077 ms, cfg3 0.096 -> 0.050, cfg4 0.023 -> 0.014; cfg2's 1368
+    // observations are 171 tasks, latency-bound: 0.016 ms one observation per warp vs 0.037)
+    const bool use_mma = mma_env >= 0 ? (mma_env != 0 && L >= 2) : (L >= 3 && n >= 2048);
+    auto launch_mma = [&](auto kern, size_t smem) -> Status {
+      RK_TRY(set_smem_attr((const void*)kern, smem));
+      int per_sm = 0;
+      RK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+      const int nb = (int)std::min<int64_t>(ceil_div(ceil_div(n, 8), 8), (int64_t)sms * std::max(per_sm, 1));
+      kern<<<nb, 256, smem, st>>>(wa);
+      return Status::ok();
+    };
+    if (use_mma) {
+      if (L == 2) RK_TRY(launch_mma(weights_kernel_mma<2>, WMma<2>::smem_bytes()));
+      else if (L == 3) RK_TRY(launch_mma(weights_kernel_mma<3>, WMma<3>::smem_bytes()));
+      else RK_TRY(launch_mma(weights_kernel_mma<4>, WMma<4>::smem_bytes()));
+    }
+    else if (L == 1) RK_TRY(launch_l(weights_kernel_l<1>));
     else if (L == 2) RK_TRY(launch_l(weights_kernel_l<2>));
     else if (L >= 3 && ob >= 2) {
       if (L == 3) RK_TRY(ob >= 4 ? launch_ob(weights_kernel_ob<3, 4>, 4) : launch_ob(weights_kernel_ob<3, 2>, 2));

@@ -499,9 +499,10 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
   }
   pdl_wait();   // U is the predecessor's output
   // strided gather of both rows of every line (Z[k] = A[k] + i B[k], Hermitian upper half),
-  // batched 8 deep per thread for memory-level parallelism
+  // batched 5 deep per thread for memory-level parallelism (5 x 512 threads cover a 4374-point
+  // line's 2188 entries in one round trip; 8 deep spilled the 64-register kernels)
   const int tot = a.lpc * H;
-  constexpr int D = 8;
+  constexpr int D = 5;
   for (int base = threadIdx.x; base < tot; base += D * blockDim.x) {
     double2 A[D], B[D];
 #pragma unroll
@@ -788,7 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
   // buf[H - mm] (even) / buf[H - 1 - mm] (odd)
   const int nk = (Hf - half + 1) / 2;
   const bool vA = ya < a.nrows, vB = ya + 1 < a.nrows;
-  constexpr int D = 8;
+  constexpr int D = 5;   // 5 x 512 threads cover a half line's <= 2305 entries in one round trip
   for (int base = tl; base < nk; base += D * nthr) {
     double2 A[D], B[D];
 #pragma unroll

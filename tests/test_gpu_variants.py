@@ -3,8 +3,12 @@ inputs, compared with the default path.
 
 * RK_SPLIT=0: the full-length FFT passes instead of the split-length ones (for tori above the
   WIDE-plan lengths, P = 2 H with the nonzero rows / kept outputs below H): equal to 1e-13;
-* RK_WEIGHTS_OB=0 / 2: the one-observation-per-warp weights kernels instead of the 4-per-warp
-  interleaved one: bitwise identical weights and fields (same operations, same order).
+* RK_WEIGHTS_OB=0 / 2 (with RK_WEIGHTS_MMA=0): the one-observation-per-warp substitution
+  kernels instead of the interleaved one: bitwise identical weights and fields (same
+  operations, same order);
+* RK_WEIGHTS_MMA=1 / 0: the FP64 tensor-core blocked solve against the substitution kernels:
+  a different (backward-stable) operation order, so the weights agree to the conditioning of
+  K_N and the fields to 1e-10, and the interpolation residual stays < 1e-8.
 """
 import os
 import subprocess
@@ -31,7 +35,8 @@ c = rng.normal(size=n)
 field = pk.predict_rapid(st, c, np.array([0.25]))
 cstar = st.coefficients_to_grid(c)
 conv = pk.convolve_filter(st.filter_spectrum, st.embed_dims, cstar)
-np.savez({out!r}, field=field, w=st.weights, conv=conv, embed=np.array(st.embed_dims))
+np.savez({out!r}, field=field, w=st.weights, cv=st.cond_var, idx=st.neighbor_indices, conv=conv,
+         embed=np.array(st.embed_dims), obs=obs, h=np.array(grid.spacing))
 """
 
 
@@ -57,11 +62,34 @@ def test_split_length_passes_match_full_length(tmp_path, dims):
 @pytest.mark.parametrize("L,nu", [(3, 1.5), (4, 2.5), (3, 1.0)])
 def test_weights_kernel_variants_bitwise(tmp_path, L, nu):
     kw = dict(n=5000, L=L, dims=(300, 280), nu=nu)
-    a = _run(tmp_path, "ob4", {}, **kw)
+    a = _run(tmp_path, "ob4", {"RK_WEIGHTS_MMA": "0", "RK_WEIGHTS_OB": "4"}, **kw)
     for v in ("0", "2"):
-        b = _run(tmp_path, "ob" + v, {"RK_WEIGHTS_OB": v}, **kw)
+        b = _run(tmp_path, "ob" + v, {"RK_WEIGHTS_MMA": "0", "RK_WEIGHTS_OB": v}, **kw)
         assert np.array_equal(a["w"], b["w"]), v
         assert np.array_equal(a["field"], b["field"]), v
+
+
+@pytest.mark.parametrize("L,nu", [(2, 1.5), (3, 1.5), (3, 1.0), (4, 2.5), (4, 0.5)])
+def test_weights_mma_matches_substitution(tmp_path, L, nu):
+    from oracle import rk_oracle as ro
+    kw = dict(n=5000, L=L, dims=(300, 280), nu=nu)
+    a = _run(tmp_path, "mma", {"RK_WEIGHTS_MMA": "1"}, **kw)
+    b = _run(tmp_path, "sub", {"RK_WEIGHTS_MMA": "0"}, **kw)
+    assert np.array_equal(a["idx"], b["idx"])
+    assert rel_err(a["field"], b["field"]) < 1e-10
+    assert np.abs(a["cv"] - b["cv"]).max() < 1e-10
+    # both weight sets satisfy the interpolation condition K_N w_i = k_i to the same k_i
+    # (reference test_acceptance.py:98-116; the substitution kernels' residual is pinned against
+    # the reference goldens in test_gpu_parity): |K_N (w_mma - w_sub)| < 1e-8
+    model = ro.Model(1.0, 12.0, nu)
+    hx, hy = a["h"]
+    bs = 2 * L
+    off = np.stack(np.meshgrid(np.arange(bs) * hx, np.arange(bs) * hy), -1).reshape(-1, 2)
+    d = off[:, None, :] - off[None, :, :]
+    kn = model.cov(np.hypot(d[..., 0], d[..., 1]))
+    kn = 0.5 * (kn + kn.T)
+    res = np.abs(kn @ (a["w"] - b["w"]).T).max()
+    assert res < 1e-8, res
 
 
 CFG2 = """

@@ -1,5 +1,5 @@
-"""K1 (weights kernel) time per configuration and kernel variant (RK_WEIGHTS_OB), each variant in
-its own process (the switch is read once).  Prints one JSON line per (config, variant)."""
+"""K1 (weights kernel) time per configuration and kernel variant (RK_WEIGHTS_MMA / RK_WEIGHTS_OB),
+each variant in its own process (the switches are read once).  Prints one JSON line per variant."""
 import json
 import os
 import subprocess
@@ -22,8 +22,10 @@ for name, wl in (("cfg2", workloads.cfg2()), ("cfg3", workloads.cfg3()), ("cfg4"
 print(json.dumps(out))
 '''
 res = {}
-for ob in ("0", "2", "4"):
-    r = subprocess.run([sys.executable, "-c", CODE], env=dict(os.environ, RK_WEIGHTS_OB=ob), capture_output=True, text=True)
-    res["OB" + ob] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-500:]
-    print(ob, res["OB" + ob], flush=True)
+VARIANTS = {"MMA": {"RK_WEIGHTS_MMA": "1"}, "OB0": {"RK_WEIGHTS_MMA": "0", "RK_WEIGHTS_OB": "0"},
+            "OB2": {"RK_WEIGHTS_MMA": "0", "RK_WEIGHTS_OB": "2"}}
+for tag, env in VARIANTS.items():
+    r = subprocess.run([sys.executable, "-c", CODE], env=dict(os.environ, **env), capture_output=True, text=True)
+    res[tag] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-500:]
+    print(tag, res[tag], flush=True)
 json.dump(res, open("gpurun_out/weights_sweep.json", "w"), indent=1)
