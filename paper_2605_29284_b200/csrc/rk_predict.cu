@@ -348,6 +348,8 @@ struct ColArgs {
   int upair;                 // split-length kernel: write U pair-blocked (see UPair)
   int64_t ldp;
   int hh;
+  int x_off;                 // col_pair_kernel: smem offset (double2 units) of its 2 mbarriers
+  int batch;                 // col_pair_kernel: fields per launch (persistent over columns x batch)
 };
 
 template <int MODE, bool TWS, int FM>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
@@ -767,6 +769,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
   __syncthreads();
 }
 
+// pass 2, one CTA per SM holding a whole column: two 512-thread groups, group 0 the odd half
+// (buffer A, input twisted by w_P^y), group 1 the even half (buffer B), each transforming with its
+// own named barrier, so the halves are combined from the same shared memory (no cluster barrier,
+// no DSMEM, no partner skew as in col_split_kernel).  The staging buffer X is time-shared by TMA:
+// the column's input, then its spectrum, which lands during the forward transforms.
+//   A, B: H double2 each; X: max(nin double2, 2 ldh doubles); twiddle tables; 2 mbarriers.
+// (One column per CTA: a persistent loop over columns, which would let the next column's input
+// land during the inverse transforms, makes ptxas spill the butterflies at the 64-register bound.)
+__global__ void __launch_bounds__(2 * kSplitThreads, 1) col_pair_kernel(const ColArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int H = a.pl.n, G = a.pl.nthr;
+  const int grp = (int)threadIdx.x >= G;   // 0: odd half (A), 1: even half (B)
+  const int tl = threadIdx.x - grp * G;
+  double2* A = smem;
+  double2* B = smem + H;
+  const double2* X = smem + 2 * H;
+  double2* mine = smem + grp * H;
+  uint64_t* bar = (uint64_t*)(smem + a.x_off);   // [0] input, [1] spectrum
+  const int kx = blockIdx.x;
+  const int64_t b = blockIdx.y;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    mbar_expect_tx(bar, (uint32_t)a.nin * 16u);
+    bulk_g2s(smem + 2 * H, a.T + b * a.T_bstride + (int64_t)kx * a.ldT, (uint32_t)a.nin * 16u, bar);
+  }
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
+  for (int y = a.nin + tl; y < H; y += G) mine[y] = make_double2(0.0, 0.0);
+  __syncthreads();
+  mbar_wait(bar, 0);
+  if (grp == 0) {
+    for (int y = tl; y < a.nin; y += G) A[y] = cmul(X[y], split_w(wt, y));
+  } else {
+    for (int y = tl; y < a.nin; y += G) B[y] = X[y];
+  }
+  fence_async_smem();
+  __syncthreads();   // X consumed
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(bar + 1, (uint32_t)a.ldh * 16u);
+    bulk_g2s(smem + 2 * H, a.spec_s + (int64_t)kx * 2 * a.ldh, (uint32_t)a.ldh * 16u, bar + 1);
+  }
+  fft_line<false, true, 1>(mine, pls, tl, 1 + grp);
+  mbar_wait(bar + 1, 0);
+  {
+    const int half = grp ^ 1;
+    const double* S = (const double*)X + half * a.ldh;
+    for (int mm = tl; mm < H; mm += G) mine[mm] = cscale(mine[mm], S[min(mm, H - half - mm)]);
+  }
+  group_sync(1 + grp, G);
+  fft_line<true, true, 1>(mine, pls, tl, 1 + grp);
+  __syncthreads();   // both halves transformed
+  for (int y = a.row0 + (int)threadIdx.x; y < a.row0 + a.nout; y += 2 * G)
+    B[y] = cadd(B[y], cmulc(A[y], split_w(wt, y)));   // even + w^-y odd
+  fence_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bulk_s2g(a.U + b * a.U_bstride + (int64_t)kx * a.ldU, B + a.row0, (uint32_t)a.nout * 16u);
+    bulk_commit();
+    bulk_wait_read0();
+  }
+}
+
 // pass 3: Hermitian pair of interior rows -> this CTA's half spectrum (Z[k], k % 2 == half) ->
 // inverse half; the cluster combines the halves over DSMEM, each CTA finishing half the
 // kept columns (fixed-part / draw epilogue)
@@ -1006,6 +1071,31 @@ static Status launch_col_split(const ColArgs& a0, int batch, cudaStream_t st, bo
   return Status::ok();
 }
 
+// one CTA per SM, both halves of a column per CTA (col_pair_kernel); *done = false when it does not
+// apply (pair-blocked U, plan wider than a group, shared memory)
+static Status launch_col_pair(const ColArgs& a0, int batch, cudaStream_t st, bool* done) {
+  ColArgs a = a0;
+  *done = false;
+  // measured on cfg5 (B200): 0.765 ms vs the cluster kernel's 0.698 -- one CTA per SM exposes
+  // each column's input load, which two co-resident cluster CTAs hide; off unless RK_COL_PAIR=1
+  static const bool on = getenv("RK_COL_PAIR") && atoi(getenv("RK_COL_PAIR")) == 1;
+  if (!on || a.upair || !a.spec_s || a.pl.nthr > kSplitThreads) return Status::ok();
+  a.lpc = 1;
+  a.batch = batch;
+  const size_t xb = std::max((size_t)a.nin * 16, (size_t)a.ldh * 16);
+  size_t smem = sizeof(double2) * 2 * (size_t)a.pl.n + xb;
+  smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
+  a.x_off = tw_slot(smem);
+  smem = (size_t)a.x_off * 16 + 16;
+  if (smem > kSmemMax) return Status::ok();
+  RK_TRY(set_smem_attr((const void*)col_pair_kernel, smem));
+  col_pair_kernel<<<dim3((unsigned)a.ncols, (unsigned)batch), 2 * a.pl.nthr, smem, st>>>(a);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  *done = true;
+  return Status::ok();
+}
+
 static Status launch_row_inv_split(const RowInvArgs& a0, int batch, cudaStream_t st, bool* done) {
   RowInvArgs a = a0;
   *done = false;
@@ -1233,7 +1323,8 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     cs.upair = upair;
     cs.hh = hh;
     cs.ldp = 4LL * hh;
-    RK_TRY(launch_col_split(cs, batch, st, &done));
+    RK_TRY(launch_col_pair(cs, batch, st, &done));
+    if (!done) RK_TRY(launch_col_split(cs, batch, st, &done));
   }
   if (!done) RK_TRY(launch_col(0, ca, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));

@@ -6,6 +6,8 @@ inputs, compared with the default path.
 * RK_WEIGHTS_OB=0 / 2 (with RK_WEIGHTS_MMA=0): the one-observation-per-warp substitution
   kernels instead of the interleaved one: bitwise identical weights and fields (same
   operations, same order);
+* RK_COL_PAIR=1 / 0: the split-length column pass with both halves in one CTA against the
+  2-CTA cluster version: bitwise identical;
 * RK_WEIGHTS_MMA=1 / 0: the FP64 tensor-core blocked solve against the substitution kernels:
   a different (backward-stable) operation order, so the weights agree to the conditioning of
   K_N and the fields to 1e-10, and the interpolation residual stays < 1e-8.
@@ -57,6 +59,18 @@ def test_split_length_passes_match_full_length(tmp_path, dims):
     assert max(a["embed"]) > 4608   # a split-length torus
     assert rel_err(a["field"], b["field"]) < 1e-13
     assert rel_err(a["conv"], b["conv"]) < 1e-13
+
+
+@pytest.mark.parametrize("dims", [(2600, 2500), (4096, 4096)])
+def test_column_pass_one_cta_vs_cluster_bitwise(tmp_path, dims):
+    """Split-length column pass: both halves in one CTA (col_pair_kernel, RK_COL_PAIR=1) vs the
+    2-CTA cluster exchanging over DSMEM (col_split_kernel): same operations, bitwise equal."""
+    kw = dict(n=6000, L=2, dims=dims, nu=1.5)
+    a = _run(tmp_path, "pair", {"RK_COL_PAIR": "1"}, **kw)
+    b = _run(tmp_path, "cluster", {"RK_COL_PAIR": "0"}, **kw)
+    assert max(a["embed"]) > 4608
+    assert np.array_equal(a["field"], b["field"])
+    assert np.array_equal(a["conv"], b["conv"])
 
 
 @pytest.mark.parametrize("L,nu", [(3, 1.5), (4, 2.5), (3, 1.0)])
