@@ -8,6 +8,7 @@
 //   build_setup         rapid.py:177-230      -> rk_build_setup (weights_kernel + sort +
 //                                                spectrum_quarter)
 #include <algorithm>
+#include <tuple>
 #include <atomic>
 #include <climits>
 #include <set>
@@ -115,6 +116,34 @@ Status split_table(int P, SplitTw* out) {
   w.nhi = nhi;
   cache[{dev, P}] = w;
   *out = w;
+  return Status::ok();
+}
+
+// in-place Cooley-Tukey plan (rk_fft_ct.cuh) with its twiddle table on the device, cached per
+// (device, n, group threads); G = 0 picks the plan's default group size
+Status ct_plan_for(int n, int G, CtPlan* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, CtPlan> cache;
+  int dev = 0;
+  RK_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, n, G});
+  if (it != cache.end()) {
+    *out = it->second;
+    return Status::ok();
+  }
+  CtPlan p{};
+  if (!ct_plan_make(n, &p, 1024, G)) return Status::err(RK_INTERNAL, "no Cooley-Tukey plan for this length");
+  std::vector<double2> t;
+  ct_twiddles(p, t, [](double x, double y) { return make_double2(x, y); });
+  double2* d = nullptr;
+  if (!t.empty()) {
+    RK_CUDA_TRY(cudaMalloc(&d, sizeof(double2) * t.size()));
+    RK_CUDA_TRY(cudaMemcpy(d, t.data(), sizeof(double2) * t.size(), cudaMemcpyHostToDevice));
+  }
+  p.tw = d;
+  cache[{dev, n, G}] = p;
+  *out = p;
   return Status::ok();
 }
 

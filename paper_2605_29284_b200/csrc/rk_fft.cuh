@@ -383,23 +383,23 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
   const double2* tw = pl.tw;   // stage 1 (Ns = 1) needs no twiddles and has no block
   const uint32_t* mg = reinterpret_cast<const uint32_t*>(pl.tw + pl.ntw - kFftMagicSlots);
   int Ns = 1, si = 0;   // si: stage index (magic divisors)
+  // the radix-6 / 3 stage first: as the Ns = 1 stage it needs no twiddles, which keeps the WIDE
+  // kernels' two-butterfly radix-6 stage inside 64 registers
+  if (pl.r3 == 6) {
+    fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
+    Ns *= 6;
+    ++si;
+  } else if (pl.r3 == 3) {
+    fft_stage<3, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
+    Ns *= 3;
+    ++si;
+  }
 #pragma unroll 1
   for (int s = 0; s < pl.n9; ++s) {
     if (FM == 2) fft_stage9_split<INV, TWS>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     else fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     if (Ns > 1) tw += Ns;
     Ns *= 9;
-    ++si;
-  }
-  if (pl.r3 == 6) {
-    fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
-    if (Ns > 1) tw += Ns;
-    Ns *= 6;
-    ++si;
-  } else if (pl.r3 == 3) {
-    fft_stage<3, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
-    if (Ns > 1) tw += Ns;
-    Ns *= 3;
     ++si;
   }
 #pragma unroll 1
@@ -425,8 +425,8 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
 // ----------------------------------------------------------------- host planning
 inline int fft_stage_list(const FftPlan& pl, int* rad) {
   int ns = 0;
-  for (int i = 0; i < pl.n9; ++i) rad[ns++] = 9;
   if (pl.r3 > 1) rad[ns++] = pl.r3;
+  for (int i = 0; i < pl.n9; ++i) rad[ns++] = 9;
   for (int i = 0; i < pl.n8; ++i) rad[ns++] = 8;
   if (pl.r2 == 16) {
     rad[ns++] = 4;

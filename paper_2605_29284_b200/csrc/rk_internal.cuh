@@ -7,6 +7,7 @@
 
 #include "rk_common.cuh"
 #include "rk_fft.cuh"
+#include "rk_fft_ct.cuh"
 #include "rk_matern.cuh"
 
 namespace rk {
@@ -27,6 +28,7 @@ struct SplitTw {
   int off = 0;                   // smem offset (double2 units) where a kernel stages them
 };
 Status split_table(int P, SplitTw* out);   // cached per (device, P)
+Status ct_plan_for(int n, int G, CtPlan* out);   // cached per (device, n, G); rk_fft_ct.cuh
 __device__ __forceinline__ const double2* stage_split_tw(const SplitTw& t, double2* dst) {
   for (int i = threadIdx.x; i < 128 + t.nhi; i += blockDim.x) dst[i] = i < 128 ? __ldg(&t.lo[i]) : __ldg(&t.hi[i - 128]);
   return dst;

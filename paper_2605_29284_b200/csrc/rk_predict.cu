@@ -350,6 +350,8 @@ struct ColArgs {
   int hh;
   int x_off;                 // col_pair_kernel: smem offset (double2 units) of its 2 mbarriers
   int batch;                 // col_pair_kernel: fields per launch (persistent over columns x batch)
+  CtPlan ct;                 // col_split_ct_kernel: in-place Cooley-Tukey plan of the half length
+  int ct_off;                // smem offset (double2 units) where its twiddles are staged
 };
 
 template <int MODE, bool TWS, int FM>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
@@ -832,6 +834,68 @@ __global__ void __launch_bounds__(2 * kSplitThreads, 1) col_pair_kernel(const Co
   }
 }
 
+// pass 2 as col_split_kernel, with the in-place Cooley-Tukey engine (rk_fft_ct.cuh): forward DIF,
+// the spectrum product fused into the last forward / first inverse stage (frequency of each
+// digit-reversed position computed on the fly), inverse DIT; one barrier per stage, group-local
+// barriers after the first stage.  kCtThreads bounds the threads per half line (9 groups of 64
+// for the 4374-point halves of cfg5's 8748 torus).
+// MAXT: 576 (9 groups of 64, 56 registers) or 288 (9 single-warp groups, barriers after the
+// first stage are __syncwarp, up to 113 registers).
+constexpr int kCtThreads = 576;
+template <int MAXT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MAXT, 2) col_split_ct_kernel(const __grid_constant__ ColArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int half = (int)cl.block_rank();
+  const int H = a.ct.n;
+  const int nthr = a.ct.nthr;
+  const int tl = threadIdx.x;
+  const int b = blockIdx.y;
+  const int kx = blockIdx.x >> 1;
+  double2* buf = smem;
+  double* S = (double*)(smem + H);                 // this half's spectrum (ldh)
+  uint64_t* bar = (uint64_t*)(S + a.ldh);
+  const double2* Tb = a.T + (int64_t)b * a.T_bstride;
+  if (tl == 0) {
+    mbar_init(bar, 1);
+    const uint32_t colb = (uint32_t)a.nin * 16u, sb = (uint32_t)a.ldh * 8u;
+    mbar_expect_tx(bar, colb + sb);
+    bulk_g2s(S, a.spec_s + ((int64_t)kx * 2 + half) * a.ldh, sb, bar);
+    bulk_g2s(buf, Tb + (int64_t)kx * a.ldT, colb, bar);
+  }
+  const CtPlan& cp = a.ct;   // parameter space (grid constant): indexed per stage without a local copy
+  double2* tws = smem + a.ct_off;
+  for (int i = tl; i < cp.ntw; i += nthr) tws[i] = __ldg(&cp.tw[i]);
+  const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
+  for (int y = a.nin + tl; y < H; y += nthr) buf[y] = make_double2(0.0, 0.0);
+  __syncthreads();   // barrier initialised, tables staged
+  mbar_wait(bar, 0);
+  if (half) {
+    for (int y = tl; y < a.nin; y += nthr) buf[y] = cmul(buf[y], split_w(wt, y));
+    __syncthreads();
+  }
+  // S[k] for k = 2 f + half: S_half[min(f, H - half - f)]
+  ct_filter_line(buf, cp, tws, tl, 0, [&](int f) { return S[min(f, H - half - f)]; });
+  cl.sync();   // both halves transformed
+  const double2* other = cl.map_shared_rank(buf, half ^ 1);
+  const int mid = a.row0 + ((a.nout + 1) >> 1);
+  const int y0 = half ? mid : a.row0, y1 = half ? a.row0 + a.nout : mid;
+  for (int y = y0 + tl; y < y1; y += nthr) {
+    const double2 e = half ? other[y] : buf[y];
+    const double2 o = half ? buf[y] : other[y];
+    buf[y] = cadd(e, cmulc(o, split_w(wt, y)));   // + w^-y (inverse half)
+  }
+  fence_async_smem();
+  cl.sync();   // the partner's remote reads of this CTA's rows are done
+  if (tl == 0 && y1 > y0) {
+    bulk_s2g(a.U + (int64_t)b * a.U_bstride + (int64_t)kx * a.ldU + (y0 - a.row0), buf + y0,
+             (uint32_t)(y1 - y0) * 16u);
+    bulk_commit();
+    bulk_wait_read0();
+  }
+  __syncthreads();
+}
+
 // pass 3: Hermitian pair of interior rows -> this CTA's half spectrum (Z[k], k % 2 == half) ->
 // inverse half; the cluster combines the halves over DSMEM, each CTA finishing half the
 // kept columns (fixed-part / draw epilogue)
@@ -1096,6 +1160,38 @@ static Status launch_col_pair(const ColArgs& a0, int batch, cudaStream_t st, boo
   return Status::ok();
 }
 
+// split-length column pass on the Cooley-Tukey engine (col_split_ct_kernel); *done = false when it
+// does not apply (RK_COL_CT=0, pair-blocked U, no plan within kCtThreads, shared memory)
+static Status launch_col_split_ct(const ColArgs& a0, int batch, cudaStream_t st, bool* done) {
+  ColArgs a = a0;
+  *done = false;
+  // measured on cfg5 (B200): G = 64 0.804 ms, G = 32 0.701 ms vs the Stockham cluster kernel's
+  // 0.696 (ncu: 40 % more instructions -- per-butterfly index arithmetic, the radix dispatch,
+  // digit reversal -- and 3x the bank conflicts of the strided in-place stages eat the saved
+  // barriers); off unless RK_COL_CT=1
+  static const bool on = getenv("RK_COL_CT") && atoi(getenv("RK_COL_CT")) == 1;
+  static const int g_env = getenv("RK_CT_G") ? atoi(getenv("RK_CT_G")) : 0;
+  if (!on || a.upair || !a.spec_s) return Status::ok();
+  CtPlan cp{};
+  if (!ct_plan_for(a.pl.n, g_env, &cp).good() || cp.nthr > kCtThreads) return Status::ok();
+  a.ct = cp;
+  a.lpc = 1;
+  size_t smem = sizeof(double2) * (size_t)cp.n + sizeof(double) * (size_t)a.ldh + 16;
+  a.ct_off = tw_slot(smem);
+  smem = (size_t)a.ct_off * 16 + (size_t)cp.ntw * 16;
+  a.sw.off = tw_slot(smem);
+  smem = (size_t)a.sw.off * 16 + (size_t)(128 + a.sw.nhi) * 16;
+  if (smem > kSmemMax) return Status::ok();
+  auto kern = cp.nthr <= 288 ? col_split_ct_kernel<288> : col_split_ct_kernel<kCtThreads>;
+  RK_TRY(set_smem_attr((const void*)kern, smem));
+  const dim3 grid((unsigned)(2 * a.ncols), (unsigned)batch);
+  kern<<<grid, cp.nthr, smem, st>>>(a);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  *done = true;
+  return Status::ok();
+}
+
 static Status launch_row_inv_split(const RowInvArgs& a0, int batch, cudaStream_t st, bool* done) {
   RowInvArgs a = a0;
   *done = false;
@@ -1324,6 +1420,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     cs.hh = hh;
     cs.ldp = 4LL * hh;
     RK_TRY(launch_col_pair(cs, batch, st, &done));
+    if (!done) RK_TRY(launch_col_split_ct(cs, batch, st, &done));
     if (!done) RK_TRY(launch_col_split(cs, batch, st, &done));
   }
   if (!done) RK_TRY(launch_col(0, ca, batch, st));

@@ -67,10 +67,23 @@ def test_column_pass_one_cta_vs_cluster_bitwise(tmp_path, dims):
     2-CTA cluster exchanging over DSMEM (col_split_kernel): same operations, bitwise equal."""
     kw = dict(n=6000, L=2, dims=dims, nu=1.5)
     a = _run(tmp_path, "pair", {"RK_COL_PAIR": "1"}, **kw)
-    b = _run(tmp_path, "cluster", {"RK_COL_PAIR": "0"}, **kw)
+    b = _run(tmp_path, "cluster", {"RK_COL_PAIR": "0", "RK_COL_CT": "0"}, **kw)
     assert max(a["embed"]) > 4608
     assert np.array_equal(a["field"], b["field"])
     assert np.array_equal(a["conv"], b["conv"])
+
+
+@pytest.mark.parametrize("dims,g", [((2600, 2500), "0"), ((4096, 4096), "0"), ((4096, 4096), "32")])
+def test_column_pass_cooley_tukey_vs_stockham(tmp_path, dims, g):
+    """Split-length column pass on the in-place Cooley-Tukey engine (DIF, spectrum product in
+    digit-reversed order, DIT; RK_COL_CT=1, group size RK_CT_G) vs the Stockham engine: a
+    different operation order, equal to 1e-13."""
+    kw = dict(n=6000, L=2, dims=dims, nu=1.5)
+    a = _run(tmp_path, "ct", {"RK_COL_CT": "1", "RK_CT_G": g}, **kw)
+    b = _run(tmp_path, "stockham", {"RK_COL_CT": "0"}, **kw)
+    assert max(a["embed"]) > 4608
+    assert rel_err(a["field"], b["field"]) < 1e-13
+    assert rel_err(a["conv"], b["conv"]) < 1e-13
 
 
 @pytest.mark.parametrize("L,nu", [(3, 1.5), (4, 2.5), (3, 1.0)])
