@@ -957,27 +957,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
   double* out = a.out + (int64_t)b * a.out_bstride;
   const int xm = (a.ncols + 1) >> 1;
   const int x0 = half ? xm : 0, x1 = half ? a.ncols : xm;
-  const int w = x1 - x0;
-  for (int e = tl; e < 2 * w; e += nthr) {
-    const int which = e >= w;
-    const int x = x0 + e - which * w;
-    const int y = ya + which;
-    if (y >= a.nrows) continue;
+  // each combined value z gives both rows (real part: row ya, imaginary part: row ya + 1), so the
+  // partner's value is read over DSMEM once per column
+  for (int x = x0 + tl; x < x1; x += nthr) {
     const int nn = a.col0 + x;
     const double2 ev = half ? other[nn] : buf[nn];
     const double2 ov = half ? buf[nn] : other[nn];
     const double2 z = cadd(ev, cmulc(ov, split_w(wt, nn)));
-    double v = which ? z.y : z.x;
-    if (a.epi == EPI_SCALAR) {
-      v = v + beta[0];
-    } else if (a.epi == EPI_COV) {
-      const double* xr = a.xg + ((int64_t)y * a.ncols + x) * pc;
-      double fx = 0.0;
-      for (int q = 0; q < pc; ++q) fx = fma(xr[q], beta[q], fx);
-      v = v + fx;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const int y = ya + which;
+      if (y >= a.nrows) break;
+      double v = which ? z.y : z.x;
+      if (a.epi == EPI_SCALAR) {
+        v = v + beta[0];
+      } else if (a.epi == EPI_COV) {
+        const double* xr = a.xg + ((int64_t)y * a.ncols + x) * pc;
+        double fx = 0.0;
+        for (int q = 0; q < pc; ++q) fx = fma(xr[q], beta[q], fx);
+        v = v + fx;
+      }
+      if (gb) v = gb[(int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + x] - v;
+      out[(int64_t)y * a.ldo + x] = v;
     }
-    if (gb) v = gb[(int64_t)(a.g_row0 + y) * a.g_ld + a.g_col0 + x] - v;
-    out[(int64_t)y * a.ldo + x] = v;
   }
   cl.sync();   // the partner's remote reads are done before this CTA's shared memory goes away
 }

@@ -1,0 +1,114 @@
+"""Turn tools/gpu_evidence.sh's raw output (gpurun_out/) into the committed round-2 evidence:
+profiles/round2_bench_<tag>.json, round2_bench_ref_<tag>.json, round2_launches_<tag>.csv +
+_summary.txt, round2_ncu_full_<tag>_summary.txt and round2_traffic.json (the per-launch DRAM
+bytes and shared-memory busy fraction bench.py reports in roofline.traffic / smem_busy_frac).
+python tools/summarize_round2.py <tag>"""
+import collections
+import csv
+import json
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+RAW = os.path.join(ROOT, "gpurun_out")
+OUT = os.environ.get("RK_EVIDENCE_OUT", os.path.join(ROOT, "profiles"))
+PASS = [("row_fwd", "pass1_gather_rowfft"), ("col_split", "pass2_column_filter"), ("col_kernel", "pass2_column_filter"),
+        ("row_inv", "pass3_rowifft_epilogue"), ("weights_kernel", "weights_k1")]
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__grid_size",
+           "launch__block_size", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
+           "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+           "sm__cycles_elapsed.avg", "smsp__inst_executed.sum",
+           "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+           "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+           "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+           "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+           "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+           "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio"]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def ncu_raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                         capture_output=True, text=True).stdout
+    r = list(csv.reader(txt.splitlines()))
+    return r[0], r[1], [dict(zip(r[0], row)) for row in r[2:]]
+
+
+def main(tag):
+    for src, dst in ((f"bench_{tag}.json", f"round2_bench_{tag}.json"), (f"bench_ref_{tag}.json", f"round2_bench_ref_{tag}.json"),
+                     (f"launches_{tag}.csv", f"round2_launches_{tag}.csv")):
+        if os.path.exists(os.path.join(RAW, src)):
+            shutil.copy(os.path.join(RAW, src), os.path.join(OUT, dst))
+    rows = list(csv.reader(open(os.path.join(RAW, f"launches_{tag}.csv"))))
+    h, agg, per = None, collections.defaultdict(lambda: [0, 0.0]), collections.defaultdict(list)
+    for r in rows:
+        if r and r[0] == "ID":
+            h = r
+            continue
+        if h and len(r) == len(h):
+            d = dict(zip(h, r))
+            if d["Metric Name"] != "gpu__time_duration.sum":
+                continue
+            v = float(d["Metric Value"].replace(",", ""))
+            u = d["Metric Unit"]
+            v = v / 1000 if u in ("ns", "nsecond") else (v * 1000 if u in ("ms", "msecond") else v)
+            k = re.sub(r"\(.*", "", d["Kernel Name"])[:64]
+            agg[k][0] += 1
+            agg[k][1] += v
+            per[k].append(v)
+    tot = sum(v for _, v in agg.values())
+    lines = ["ncu --metrics gpu__time_duration.sum --clock-control none -c 600 python bench.py --steps 5 --warmup 3 "
+             "--no-extra --no-cpu: cold-cache, serialized per-launch durations (setup kernels run once)"]
+    for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1])[:28]:
+        lines.append(f"{v:10.1f} us {100 * v / tot:5.1f}% x{n:4d}  avg {v / n:8.2f} us  {k}")
+    # median per launch: the bench's e2e steps run pass 3 into mapped pinned host memory
+    # (zero-copy, PCIe-bound), which inflates that kernel's mean
+    step = {k: sorted(v)[len(v) // 2] for k, v in per.items()
+            if re.search(r"(row_fwd|col|row_inv)_split_kernel|weights_kernel_mma", k)}
+    ps = sum(step.values())
+    lines.append("headline step kernels (median per launch, share of the step; e2e launches of pass 3 write "
+                 "host memory over PCIe and are excluded by the median): " +
+                 ", ".join(f"{k}: {v:.1f} us ({100 * v / ps:.0f}%)" for k, v in step.items()))
+    open(os.path.join(OUT, f"round2_launches_{tag}_summary.txt"), "w").write("\n".join(lines) + "\n")
+    traffic = {"source": f"ncu --set full --clock-control none (tools/gpu_evidence.sh {tag}): "
+                         "dram__bytes_read.sum + dram__bytes_write.sum per launch", "kernels": {}}
+    out = []
+    for cfg, fname in (("cfg5", f"full_cfg5_{tag}"), ("cfg3", f"full_cfg3_{tag}"), ("cfg2", f"full_cfg2_{tag}"),
+                       ("cfg3", f"full_w_cfg3_{tag}"), ("cfg2", f"full_w_cfg2_{tag}"), ("cs_cfg4", f"full_cs_{tag}")):
+        rep = os.path.join(RAW, fname + ".ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        hh, units, recs = ncu_raw(rep)
+        out.append(f"== {cfg} ({fname}.ncu-rep)")
+        for d in recs:
+            kn = d["Kernel Name"]
+            out.append(f"  {kn[:90]}")
+            for k, u in zip(hh, units):
+                if "__" in k:
+                    out.append(f"     {k:90s} {d[k]} {u}")
+            name = next((v for kk, v in PASS if kk in kn), None)
+            if name is None or cfg == "cs_cfg4":
+                continue
+            rd = float(d["dram__bytes_read.sum"]) * SCALE[units[hh.index("dram__bytes_read.sum")]]
+            wr = float(d["dram__bytes_write.sum"]) * SCALE[units[hh.index("dram__bytes_write.sum")]]
+            wf = float(d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"])
+            cyc = float(d["sm__cycles_elapsed.avg"])
+            traffic["kernels"].setdefault(cfg, {})[name] = {
+                "kernel": re.sub(r"\(.*", "", kn), "dram_bytes": rd + wr, "read": rd, "write": wr,
+                "ncu_us": float(d["gpu__time_duration.sum"]) * (1000 if units[hh.index("gpu__time_duration.sum")] == "ms" else 1),
+                "smem_busy_frac": round(wf / (148 * cyc), 4),
+                "fp64_pipe_pct": float(d["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"])}
+    open(os.path.join(OUT, f"round2_ncu_full_{tag}_summary.txt"), "w").write("\n".join(out) + "\n")
+    json.dump(traffic, open(os.path.join(OUT, "round2_traffic.json"), "w"), indent=1)
+    print("\n".join(lines[:14]))
+    print(json.dumps(traffic["kernels"], indent=1)[:1500])
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "b")
