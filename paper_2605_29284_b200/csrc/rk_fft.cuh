@@ -254,9 +254,16 @@ __device__ __forceinline__ void group_sync(int id, int count) {
   else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int R, bool INV, bool TWS = false, bool WIDE = false>
+// Element hooks of the first / last stage (fft_line_pp): Pre(i, v) transforms element i of the
+// stage's input as it is loaded, Post(i, v) element i of its output as it is stored.
+struct FftNoOp {
+  __device__ __forceinline__ double2 operator()(int, double2 v) const { return v; }
+};
+
+template <int R, bool INV, bool TWS = false, bool WIDE = false, class Pre = FftNoOp, class Post = FftNoOp>
 __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
-                                          const double2* __restrict__ tw, uint32_t nsm, int bid = 0) {
+                                          const double2* __restrict__ tw, uint32_t nsm, int bid = 0,
+                                          const Pre& pre = Pre(), const Post& post = Post()) {
   constexpr int K = WIDE ? fft_kmax_wide(R) : fft_kmax(R);
   const int nb = n / R;
   double2 a[K][R];
@@ -274,7 +281,7 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
     }
     if (j < nb) {
 #pragma unroll
-      for (int k = 0; k < R; ++k) a[q][k] = buf[j + k * nb];
+      for (int k = 0; k < R; ++k) a[q][k] = pre(j + k * nb, buf[j + k * nb]);
       if (jm != 0) {
         const double2 w1 = TWS ? tw[jm] : __ldg(&tw[jm]);
         double2 wk = w1;
@@ -293,7 +300,7 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
   for (int q = 0; q < K; ++q) {
     if (outb[q] >= 0) {
 #pragma unroll
-      for (int k = 0; k < R; ++k) buf[outb[q] + k * Ns] = a[q][k];
+      for (int k = 0; k < R; ++k) buf[outb[q] + k * Ns] = post(outb[q] + k * Ns, a[q][k]);
     }
   }
   group_sync(bid, nthr);
@@ -420,6 +427,37 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
       ++si;
     }
   }
+}
+
+// fft_line with hooks: pre on the first stage's loads, post on the last stage's stores (each a
+// pass over the line and a barrier saved, e.g. the split-length twist before a forward transform
+// and the spectrum product after it).  Schedules {3 or 6} 9^n9 only (fft_line_pp_ok); the stage
+// arithmetic is fft_line's, so the transform is bitwise the same as hooks applied in passes.
+inline bool fft_line_pp_ok(const FftPlan& pl) { return pl.r3 > 1 && pl.n9 >= 1 && pl.n8 == 0 && pl.r2 == 1; }
+template <bool INV, bool TWS, int FM, class Pre, class Post>
+__device__ __forceinline__ void fft_line_pp(double2* __restrict__ buf, const FftPlan& pl, int t, int bid,
+                                            const Pre& pre, const Post& post) {
+  constexpr bool WIDE = FM >= 1;
+  const int n = pl.n, nthr = pl.nthr;
+  const double2* tw = pl.tw;
+  const uint32_t* mg = reinterpret_cast<const uint32_t*>(pl.tw + pl.ntw - kFftMagicSlots);
+  int Ns;
+  if (pl.r3 == 6) {
+    fft_stage<6, INV, TWS, WIDE, Pre, FftNoOp>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
+    Ns = 6;
+  } else {
+    fft_stage<3, INV, TWS, WIDE, Pre, FftNoOp>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
+    Ns = 3;
+  }
+  int si = 1;
+#pragma unroll 1
+  for (int s = 0; s < pl.n9 - 1; ++s) {
+    fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, mg[si], bid);
+    tw += Ns;
+    Ns *= 9;
+    ++si;
+  }
+  fft_stage<9, INV, TWS, WIDE, FftNoOp, Post>(buf, n, Ns, t, nthr, tw, mg[si], bid, FftNoOp(), post);
 }
 
 // ----------------------------------------------------------------- host planning

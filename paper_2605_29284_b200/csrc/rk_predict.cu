@@ -350,6 +350,8 @@ struct ColArgs {
   int hh;
   int x_off;                 // col_pair_kernel: smem offset (double2 units) of its 2 mbarriers
   int batch;                 // col_pair_kernel: fields per launch (persistent over columns x batch)
+  int fuse_pp;               // col_split_kernel: twist / spectrum product fused into the first /
+                             // last forward stage (fft_line_pp; RK_FUSE_PP=0 keeps the passes)
   CtPlan ct;                 // col_split_ct_kernel: in-place Cooley-Tukey plan of the half length
   int ct_off;                // smem offset (double2 units) where its twiddles are staged
 };
@@ -717,14 +719,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
   for (int y = a.nin + tl; y < H; y += nthr) buf[y] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
-  if (half) {
-    for (int y = tl; y < a.nin; y += nthr) buf[y] = cmul(buf[y], split_w(wt, y));
+  // S[k] for k = 2 mm + half: S_half[min(mm, H - half - mm)]
+  if (a.fuse_pp) {   // the odd half's twist on the first stage's loads, the product on the last stage's stores
+    fft_line_pp<false, true, 1>(
+        buf, pls, tl, 0,
+        [&](int y, double2 v) { return half ? cmul(v, split_w(wt, y)) : v; },
+        [&](int mm, double2 v) { return cscale(v, S[min(mm, H - half - mm)]); });
+  } else {
+    if (half) {
+      for (int y = tl; y < a.nin; y += nthr) buf[y] = cmul(buf[y], split_w(wt, y));
+      __syncthreads();
+    }
+    fft_line<false, true, 1>(buf, pls, tl);
+    for (int mm = tl; mm < H; mm += nthr) buf[mm] = cscale(buf[mm], S[min(mm, H - half - mm)]);
     __syncthreads();
   }
-  fft_line<false, true, 1>(buf, pls, tl);
-  // S[k] for k = 2 mm + half: S_half[min(mm, H - half - mm)]
-  for (int mm = tl; mm < H; mm += nthr) buf[mm] = cscale(buf[mm], S[min(mm, H - half - mm)]);
-  __syncthreads();
   fft_line<true, true, 1>(buf, pls, tl);
   pdl_trigger();
   cl.sync();   // both halves transformed
@@ -1128,6 +1137,8 @@ static Status launch_col_split(const ColArgs& a0, int batch, cudaStream_t st, bo
   size_t smem = sizeof(double2) * (size_t)a.pl.n + sizeof(double) * (size_t)a.ldh + 16;
   smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
   if (smem > kSmemMax) return Status::ok();
+  static const bool fuse = !(getenv("RK_FUSE_PP") && atoi(getenv("RK_FUSE_PP")) == 0);
+  a.fuse_pp = fuse && fft_line_pp_ok(a.pl);
   RK_TRY(set_smem_attr((const void*)col_split_kernel, smem));
   const dim3 grid((unsigned)(2 * a.ncols), (unsigned)batch);
   col_split_kernel<<<grid, a.pl.nthr, smem, st>>>(a);

@@ -73,6 +73,18 @@ def test_column_pass_one_cta_vs_cluster_bitwise(tmp_path, dims):
     assert np.array_equal(a["conv"], b["conv"])
 
 
+@pytest.mark.parametrize("dims", [(2600, 2500), (4096, 4096)])
+def test_column_pass_fused_hooks_bitwise(tmp_path, dims):
+    """Split-length column pass with the odd half's twist fused into the first stage's loads and
+    the spectrum product into the last forward stage's stores (RK_FUSE_PP=1) vs separate passes:
+    the same arithmetic, bitwise equal."""
+    kw = dict(n=6000, L=2, dims=dims, nu=1.5)
+    a = _run(tmp_path, "fused", {"RK_FUSE_PP": "1"}, **kw)
+    b = _run(tmp_path, "passes", {"RK_FUSE_PP": "0"}, **kw)
+    assert np.array_equal(a["field"], b["field"])
+    assert np.array_equal(a["conv"], b["conv"])
+
+
 @pytest.mark.parametrize("dims,g", [((2600, 2500), "0"), ((4096, 4096), "0"), ((4096, 4096), "32")])
 def test_column_pass_cooley_tukey_vs_stockham(tmp_path, dims, g):
     """Split-length column pass on the in-place Cooley-Tukey engine (DIF, spectrum product in
