@@ -56,6 +56,34 @@ __device__ __forceinline__ void philox4x64_10(uint64_t ctr0, uint64_t k0, uint64
   o[0] = c0; o[1] = c1; o[2] = c2; o[3] = c3;
 }
 
+// two Philox4x64-10 blocks of the same key in lockstep (counters ca, cb): the key schedule is
+// computed once per round for both, and the two blocks' products overlap
+__device__ __forceinline__ void philox4x64_10_x2(uint64_t ca, uint64_t cb, uint64_t k0, uint64_t k1, uint64_t oa[4],
+                                                 uint64_t ob[4]) {
+  uint64_t a0 = ca, a1 = 0, a2 = 0, a3 = 0, b0 = cb, b1 = 0, b2 = 0, b3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ULL;
+      k1 += 0xBB67AE8584CAA73BULL;
+    }
+    const uint64_t la0 = 0xD2E7470EE14C6C93ULL * a0, ha0 = __umul64hi(0xD2E7470EE14C6C93ULL, a0);
+    const uint64_t la1 = 0xCA5A826395121157ULL * a2, ha1 = __umul64hi(0xCA5A826395121157ULL, a2);
+    const uint64_t lb0 = 0xD2E7470EE14C6C93ULL * b0, hb0 = __umul64hi(0xD2E7470EE14C6C93ULL, b0);
+    const uint64_t lb1 = 0xCA5A826395121157ULL * b2, hb1 = __umul64hi(0xCA5A826395121157ULL, b2);
+    a0 = ha1 ^ a1 ^ k0;
+    a1 = la1;
+    a2 = ha0 ^ a3 ^ k1;
+    a3 = la0;
+    b0 = hb1 ^ b1 ^ k0;
+    b1 = lb1;
+    b2 = hb0 ^ b3 ^ k1;
+    b3 = lb0;
+  }
+  oa[0] = a0; oa[1] = a1; oa[2] = a2; oa[3] = a3;
+  ob[0] = b0; ob[1] = b1; ob[2] = b2; ob[3] = b3;
+}
+
 __device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t stream, uint64_t w) {
   uint64_t o[4];
   philox4x64_10(w / 4 + 1, seed, stream, o);
@@ -535,7 +563,11 @@ __device__ __forceinline__ void philox_words4(uint64_t w, uint64_t fs, uint64_t 
 // (e.g. cfg4's 2304-point rows): twiddles from L1 instead of smem and 128-entry tail queues, so
 // four CTAs fit an SM (56 registers) instead of three; CS 138.7 -> 135.4 us per realization.
 // RK_CS_GEN4=0 keeps the 3-per-SM kernel.
-template <bool TWS, int FM, int MAXT = (FM == 1 ? kFftWideThreads : FM == 2 ? kFftSplitThreads : 512), int MINB = 1>
+// AL (aligned): ps1 % 4 == 0, so every row starts on a Philox block for both the real and the
+// imaginary words (Ps = ps1 ps2 is then a multiple of 4 too) and every 4-point group lies inside
+// the row: one block per 4 words and no range checks (the doubled tori, e.g. cfg4's 2304).
+template <bool TWS, int FM, int MAXT = (FM == 1 ? kFftWideThreads : FM == 2 ? kFftSplitThreads : 512), int MINB = 1,
+          bool AL = false>
 __global__ void __launch_bounds__(MAXT, MINB) cs_rowgen_kernel(const CsGenArgs a) {
   constexpr int QCAP = MINB > 1 ? 128 : 256;   // tail-queue entries per warp
   extern __shared__ __align__(16) double2 smem[];
@@ -559,14 +591,22 @@ __global__ void __launch_bounds__(MAXT, MINB) cs_rowgen_kernel(const CsGenArgs a
       const int g = g0 + lane;
       const int x0 = 4 * g;
       uint64_t re[4], im[4];
-      philox_words4(wre + x0, fs, re);
-      philox_words4(wim + x0, fs, im);
+      if (AL) {
+        // the key is re-read per group (an opaque copy): hoisted out of the loop, its 10-round
+        // schedule stays live across the transform and spills at this kernel's 56 registers
+        uint64_t fk;
+        asm volatile("mov.b64 %0, %1;" : "=l"(fk) : "l"(fs));
+        philox4x64_10_x2(((wre + x0) >> 2) + 1, ((wim + x0) >> 2) + 1, fk, 0, re, im);
+      } else {
+        philox_words4(wre + x0, fs, re);
+        philox_words4(wim + x0, fs, im);
+      }
       double uu[8], z[8];
       unsigned tmask = 0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         uu[q] = word_uniform(q < 4 ? re[q] : im[q - 4]);
-        if (g < ng && x0 + (q & 3) < a.ps1 && ndtri_is_tail(uu[q])) tmask |= 1u << q;
+        if (g < ng && (AL || x0 + (q & 3) < a.ps1) && ndtri_is_tail(uu[q])) tmask |= 1u << q;
       }
       ndtri_central_n<8>(uu, z);
 #pragma unroll
@@ -603,7 +643,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cs_rowgen_kernel(const CsGenArgs a
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int x = x0 + q;
-          if (x < a.ps1) {
+          if (AL || x < a.ps1) {
             const double r = __ldg(&rq[min(x, a.ps1 - x)]);
             buf[x] = make_double2(r * z[q], r * z[4 + q]);
           }
@@ -631,6 +671,7 @@ __global__ void __launch_bounds__(MAXT, MINB) cs_rowgen_kernel(const CsGenArgs a
 // combined as y[n] = e[n] + w^-n o[n] for the kept n.
 constexpr int kSplitQcap = 128;   // tail-queue entries per warp
 
+template <bool AL = false>   // AL: ps1 % 4 == 0, as cs_rowgen_kernel
 __global__ void __launch_bounds__(kFftWideThreads, 1) cs_rowgen_split_kernel(const CsGenArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int H = a.pl.n;
@@ -655,14 +696,20 @@ __global__ void __launch_bounds__(kFftWideThreads, 1) cs_rowgen_split_kernel(con
     const int g = g0 + lane;
     const int x0 = 4 * g;
     uint64_t re[4], im[4];
-    philox_words4(wre + x0, fs, re);
-    philox_words4(wim + x0, fs, im);
+    if (AL) {
+      uint64_t fk;   // opaque per group (see cs_rowgen_kernel)
+      asm volatile("mov.b64 %0, %1;" : "=l"(fk) : "l"(fs));
+      philox4x64_10_x2(((wre + x0) >> 2) + 1, ((wim + x0) >> 2) + 1, fk, 0, re, im);
+    } else {
+      philox_words4(wre + x0, fs, re);
+      philox_words4(wim + x0, fs, im);
+    }
     double uu[8], z[8];
     unsigned tmask = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       uu[q] = word_uniform(q < 4 ? re[q] : im[q - 4]);
-      if (g < ng && x0 + (q & 3) < a.ps1 && ndtri_is_tail(uu[q])) tmask |= 1u << q;
+      if (g < ng && (AL || x0 + (q & 3) < a.ps1) && ndtri_is_tail(uu[q])) tmask |= 1u << q;
     }
     ndtri_central_n<8>(uu, z);
 #pragma unroll
@@ -785,8 +832,10 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     ga.sw.off = (int)((by + 15) / 16);
     by = (size_t)ga.sw.off * 16 + sizeof(double2) * (size_t)(128 + ga.sw.nhi);
     if (by <= 227 * 1024) {
-      RK_TRY(set_smem_attr((const void*)cs_rowgen_split_kernel, by));
-      cs_rowgen_split_kernel<<<dim3((unsigned)e.ps2, (unsigned)batch), threads, by, st>>>(ga);
+      static const bool al_env = !(getenv("RK_CS_ALIGNED") && atoi(getenv("RK_CS_ALIGNED")) == 0);
+      auto gkern = al_env && e.ps1 % 4 == 0 ? cs_rowgen_split_kernel<true> : cs_rowgen_split_kernel<false>;
+      RK_TRY(set_smem_attr((const void*)gkern, by));
+      gkern<<<dim3((unsigned)e.ps2, (unsigned)batch), threads, by, st>>>(ga);
       count_launch();
       RK_LAUNCH_CHECK();
       gen_done = true;
@@ -819,7 +868,9 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     const bool tws = !occ4 && smem <= 227 * 1024;
     if (!tws) smem = sizeof(double2) * (size_t)ga.tw_off;
     if (ga.pl.wide >= 2 && !tws && !occ4) return Status::err(RK_INTERNAL, "wide FFT plan without room for its twiddle table");
-    auto kern = occ4 ? cs_rowgen_kernel<false, 1, 288, 4>
+    static const bool al_env = !(getenv("RK_CS_ALIGNED") && atoi(getenv("RK_CS_ALIGNED")) == 0);
+    const bool al = al_env && e.ps1 % 4 == 0;
+    auto kern = occ4 ? (al ? cs_rowgen_kernel<false, 1, 288, 4, true> : cs_rowgen_kernel<false, 1, 288, 4>)
                 : ga.pl.wide == 2 ? cs_rowgen_kernel<true, 1> : ga.pl.wide == 3 ? cs_rowgen_kernel<true, 2>
                 : tws ? cs_rowgen_kernel<true, 0> : cs_rowgen_kernel<false, 0>;
     RK_TRY(set_smem_attr((const void*)kern, smem));
