@@ -29,6 +29,9 @@
 namespace rk {
 
 constexpr int FFT_MAX_STAGES = 16;
+#ifndef RK_TW_TREE
+#define RK_TW_TREE 0   // 1: balanced-tree twiddle powers (measured slower: more live registers, spills)
+#endif
 constexpr int kFftMagicSlots = FFT_MAX_STAGES / 4;   // double2 entries holding the stage divisors
 
 // n = 9^n9 * r3 * 8^n8 * r2.  Kept as counts (not a radix array) so the stage
@@ -284,12 +287,26 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
       for (int k = 0; k < R; ++k) a[q][k] = pre(j + k * nb, buf[j + k * nb]);
       if (jm != 0) {
         const double2 w1 = TWS ? tw[jm] : __ldg(&tw[jm]);
+#if RK_TW_TREE
+        // powers by a balanced tree: w^k = w^hb w^(k - hb), hb the largest power of two below k
+        // (dependency depth 3 for R = 9 instead of the running product's 7)
+        double2 pw[R];
+        pw[1] = w1;
+#pragma unroll
+        for (int k = 2; k < R; ++k) {
+          const int hb = k > 4 ? 4 : k > 2 ? 2 : 1;
+          pw[k] = cmul(pw[hb], pw[k - hb]);
+        }
+#pragma unroll
+        for (int k = 1; k < R; ++k) a[q][k] = INV ? cmulc(a[q][k], pw[k]) : cmul(a[q][k], pw[k]);
+#else
         double2 wk = w1;
 #pragma unroll
         for (int k = 1; k < R; ++k) {
           if (k > 1) wk = cmul(wk, w1);
           a[q][k] = INV ? cmulc(a[q][k], wk) : cmul(a[q][k], wk);
         }
+#endif
       }
       Dft<R, INV>::run(a[q]);
       outb[q] = (j - jm) * R + jm;
@@ -335,7 +352,14 @@ __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int 
       double2 wp[9];
       wp[1] = w1;
 #pragma unroll
-      for (int k = 2; k < 9; ++k) wp[k] = cmul(wp[k - 1], w1);
+      for (int k = 2; k < 9; ++k) {
+#if RK_TW_TREE
+        const int hb = k > 4 ? 4 : k > 2 ? 2 : 1;   // as fft_stage (bitwise the same powers)
+        wp[k] = cmul(wp[hb], wp[k - hb]);
+#else
+        wp[k] = cmul(wp[k - 1], w1);
+#endif
+      }
       const double2 wr = r == 1 ? wp[1] : wp[2];
       const double2 wr3 = r == 0 ? wp[3] : r == 1 ? wp[4] : wp[5];
       const double2 wr6 = r == 0 ? wp[6] : r == 1 ? wp[7] : wp[8];
