@@ -910,7 +910,9 @@ struct WMma {
   static constexpr size_t smem_bytes() { return sizeof(double) * (2 * FRAG + 2 * T * DLD + MP + 8 * MP * 8); }
 };
 
-template <int L>
+// HALF: half-integer nu (closed-form Matern only: a fraction of the code, which otherwise
+// overflows the instruction cache -- ncu: 14 % no-instruction stalls with the Bessel paths inlined)
+template <int L, bool HALF = false>
 __global__ void __launch_bounds__(256, 2) weights_kernel_mma(WArgs a) {
   using W = WMma<L>;
   constexpr int BS = W::BS, M = W::M, T = W::T, MP = W::MP;
@@ -989,7 +991,8 @@ __global__ void __launch_bounds__(256, 2) weights_kernel_mma(WArgs a) {
             const int r = m / BS, c = m % BS;
             const double nx = __dadd_rn(a.px0, __dmul_rn((double)(cx - (L - 1) + c), a.hx));
             const double ny = __dadd_rn(a.py0, __dmul_rn((double)(cy - (L - 1) + r), a.hy));
-            kv = matern_cov(a.P, hypot(__dsub_rn(nx, x), __dsub_rn(ny, y)), &bad);
+            const double dist = hypot(__dsub_rn(nx, x), __dsub_rn(ny, y));
+            kv = HALF ? a.P.sigma2 * matern_phi_half(a.P, a.P.alpha * dist) : matern_cov(a.P, dist, &bad);
           }
           kw[m * 8 + (lane & 7)] = kv;
         }
@@ -1518,9 +1521,10 @@ static Status launch_weights(const rk_setup* s, int32_t* base, double* weights, 
       return Status::ok();
     };
     if (use_mma) {
-      if (L == 2) RK_TRY(launch_mma(weights_kernel_mma<2>, WMma<2>::smem_bytes()));
-      else if (L == 3) RK_TRY(launch_mma(weights_kernel_mma<3>, WMma<3>::smem_bytes()));
-      else RK_TRY(launch_mma(weights_kernel_mma<4>, WMma<4>::smem_bytes()));
+      const bool half = s->mat.half_n >= 0;
+      if (L == 2) RK_TRY(launch_mma(half ? weights_kernel_mma<2, true> : weights_kernel_mma<2>, WMma<2>::smem_bytes()));
+      else if (L == 3) RK_TRY(launch_mma(half ? weights_kernel_mma<3, true> : weights_kernel_mma<3>, WMma<3>::smem_bytes()));
+      else RK_TRY(launch_mma(half ? weights_kernel_mma<4, true> : weights_kernel_mma<4>, WMma<4>::smem_bytes()));
     }
     else if (L == 1) RK_TRY(launch_l(weights_kernel_l<1>));
     else if (L == 2) RK_TRY(launch_l(weights_kernel_l<2>));

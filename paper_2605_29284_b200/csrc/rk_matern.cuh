@@ -164,6 +164,16 @@ __device__ inline double matern_phi(const MaternDev& P, double x, int* bad) {
   return fmin(fmax(phi, 0.0), 1.0);
 }
 
+// matern_phi for half-integer nu (P.half_n >= 0) only: the closed form alone, bitwise the same
+// value (kernels templated on it avoid inlining the Bessel paths' code)
+__device__ __forceinline__ double matern_phi_half(const MaternDev& P, double x) {
+  if (!(x > 1.0e-12)) return 1.0;
+  double acc = 0.0;
+  const double tx = 2.0 * x;
+  for (int i = 0; i < P.ncoef; ++i) acc = acc * tx + P.coef[i];
+  return fmin(fmax(P.pref * exp(-x) * acc, 0.0), 1.0);
+}
+
 // sigma2 * phi(alpha * dist)  (covariance.py:83-89)
 __device__ __forceinline__ double matern_cov(const MaternDev& P, double dist, int* bad) {
   return P.sigma2 * matern_phi(P, P.alpha * dist, bad);
