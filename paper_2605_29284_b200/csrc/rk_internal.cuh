@@ -94,6 +94,8 @@ struct Workspace {
   cudaStream_t aux = nullptr;
   cudaEvent_t fork = nullptr;
   cudaEvent_t xev[kMaxChunks] = {};
+  cudaEvent_t oev[kMaxChunks] = {};   // field row block k computed (its copy may start)
+  cudaEvent_t join = nullptr;         // the side stream's last field copy issued
   double* cb_h = nullptr;       // pinned staging of c and beta (beta at beta_in - c_in)
   std::map<GraphKey, cudaGraphExec_t> hgraphs;
   std::map<GraphKey, int> hseen;
@@ -106,6 +108,11 @@ struct HostIo {
   int chunks = 1;
   const cudaEvent_t* xev = nullptr;
   double* out_host = nullptr;
+  // with a copy stream: block k's device -> host copy runs there (after oev[k]) while block k + 1
+  // is computed; the launching stream waits on `join` after the last block
+  cudaStream_t copy = nullptr;
+  const cudaEvent_t* oev = nullptr;
+  cudaEvent_t join = nullptr;
 };
 int chunk_rows(int nrows, int chunks);   // rows per block (even)
 

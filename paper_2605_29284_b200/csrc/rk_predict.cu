@@ -1482,9 +1482,20 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
         RK_TRY(launch_row_inv_split(is, 1, st, &done));
       }
       if (!done) RK_TRY(launch_row_inv(ck, 1, st));
-      if (hio->out_host)
+      if (hio->out_host) {
+        cudaStream_t cq = st;
+        if (hio->copy) {   // overlap this block's copy with the next block's pass 3
+          RK_CUDA_TRY(cudaEventRecord(hio->oev[k], st));
+          RK_CUDA_TRY(cudaStreamWaitEvent(hio->copy, hio->oev[k], 0));
+          cq = hio->copy;
+        }
         RK_CUDA_TRY(cudaMemcpyAsync(hio->out_host + (int64_t)r0 * ia.ldo, ck.out,
-                                    sizeof(double) * (size_t)(r1 - r0) * ia.ldo, cudaMemcpyDeviceToHost, st));
+                                    sizeof(double) * (size_t)(r1 - r0) * ia.ldo, cudaMemcpyDeviceToHost, cq));
+      }
+    }
+    if (hio->out_host && hio->copy) {
+      RK_CUDA_TRY(cudaEventRecord(hio->join, hio->copy));
+      RK_CUDA_TRY(cudaStreamWaitEvent(st, hio->join, 0));
     }
   }
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[4], st));
@@ -1539,6 +1550,9 @@ static void free_ws(Workspace* w) {
   for (auto& g : w->hgraphs) cudaGraphExecDestroy(g.second);
   if (w->aux) cudaStreamDestroy(w->aux);
   if (w->fork) cudaEventDestroy(w->fork);
+  if (w->join) cudaEventDestroy(w->join);
+  for (auto& e : w->oev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : w->xev)
     if (e) cudaEventDestroy(e);
   cudaFreeHost(w->cb_h);
@@ -1586,6 +1600,8 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
   RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->aux, cudaStreamNonBlocking));
   RK_CUDA_TRY(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
   for (auto& e : w->xev) RK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : w->oev) RK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  RK_CUDA_TRY(cudaEventCreateWithFlags(&w->join, cudaEventDisableTiming));
   RK_CUDA_TRY(cudaMallocHost(&w->cb_h, sizeof(double) * (boff + 16)));
   *out = w.get();
   s->ws[st] = w.release();
@@ -1853,14 +1869,20 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
     // one block by default: on B200 (cfg2, 2.9 MB of X_g) the single side-stream upload
     // hidden behind the gather / FFT passes measured 114 us per call; 2 / 4 / 8 row blocks
     // 294 / 169 / 279 us (the interleaved small copies serialise on the copy engines)
-    static const int k_env = getenv("RK_HOST_CHUNKS") ? atoi(getenv("RK_HOST_CHUNKS")) : 1;
+    // Large fields (>= 16 MB) instead go through device memory, pass 3 in 4 row blocks, each
+    // block's device -> host copy on the side stream overlapping the next block (measured on
+    // cfg5's 134 MB field: 3.51 ms per call vs 3.61-4.04 ms zero-copy, whose kernel-issued PCIe
+    // writes vary from box to box; the DMA copies run at ~56 GB/s).
+    const bool big = (double)N * 8.0 >= 16.0e6;
+    static const int k_env = getenv("RK_HOST_CHUNKS") ? atoi(getenv("RK_HOST_CHUNKS")) : -1;
     static const int graph_env = getenv("RK_HOST_GRAPH") ? atoi(getenv("RK_HOST_GRAPH")) : 1;
-    const int K = std::max(1, std::min(k_env, Workspace::kMaxChunks));
-    // pass 3 writes the field straight into the pinned output through its device mapping:
-    // the device -> host traffic overlaps the last pass instead of following it
-    static const int zc_env = getenv("RK_HOST_ZEROCOPY") ? atoi(getenv("RK_HOST_ZEROCOPY")) : 1;
+    const int K = std::max(1, std::min(k_env >= 0 ? k_env : (big ? 4 : 1), Workspace::kMaxChunks));
+    // small fields: pass 3 writes the field straight into the pinned output through its device
+    // mapping, the device -> host traffic overlapping the last pass instead of following it
+    static const int zc_env = getenv("RK_HOST_ZEROCOPY") ? atoi(getenv("RK_HOST_ZEROCOPY")) : -1;
+    const bool zc = zc_env >= 0 ? zc_env != 0 : !big;
     double* out_map = nullptr;
-    if (zc_env && cudaHostGetDevicePointer((void**)&out_map, out, 0) != cudaSuccess) {
+    if (zc && cudaHostGetDevicePointer((void**)&out_map, out, 0) != cudaSuccess) {
       cudaGetLastError();
       out_map = nullptr;
     }
@@ -1869,6 +1891,11 @@ rk_status rk_predict_host(const rk_setup* s, const double* c, const double* beta
       HostIo hio;
       hio.chunks = K;
       hio.out_host = out_map ? nullptr : out;
+      if (!out_map && K > 1) {   // field copies on the side stream, overlapped with pass 3
+        hio.copy = w->aux;
+        hio.oev = w->oev;
+        hio.join = w->join;
+      }
       if (xg) {   // fork first: the X_g upload starts before anything else
         RK_CUDA_TRY(cudaEventRecord(w->fork, q));
         RK_CUDA_TRY(cudaStreamWaitEvent(w->aux, w->fork, 0));

@@ -186,3 +186,27 @@ def test_out_buffer_validation_and_many_streams():
             out = pk.predict_rapid(st, c, torch.tensor([1.0], dtype=torch.float64, device="cuda"))
         s.synchronize()
         assert torch.equal(out, ref), k
+
+
+def test_host_path_large_field_block_copies_bitwise():
+    """Host-buffer predict of a field >= 16 MB (device staging, pass 3 in 4 row blocks with their
+    device -> host copies on the side stream, captured into a graph from the second call) and of
+    a small one (zero-copy pass 3): bitwise equal to the device-resident path, and to pageable
+    buffers, on repeated calls (graph replay)."""
+    import torch
+    import paper_2605_29284_b200 as pk
+    rng = np.random.default_rng(5)
+    for dims, n in (((1600, 1500), 3000), ((120, 100), 400)):
+        obs = rng.uniform(0, 1, size=(n, 2))
+        model = pk.CovarianceModel(1.0, 10.0, 1.5, 0.01)
+        st = pk.build_setup(model, pk.build_padded_grid((0, 1, 0, 1), dims, 2, obs), 2, obs)
+        c = rng.normal(size=n)
+        beta = np.array([0.5])
+        ref = pk.predict_rapid(st, torch.as_tensor(c, device="cuda"), torch.as_tensor(beta, device="cuda")).cpu().numpy()
+        ch = torch.from_numpy(c).pin_memory().numpy()
+        out = torch.empty((dims[1], dims[0]), dtype=torch.float64).pin_memory().numpy()
+        for _ in range(3):   # direct, captured, replayed
+            out[:] = np.nan
+            pk.predict_rapid(st, ch, beta, out=out)
+            assert np.array_equal(out, ref), dims
+        assert np.array_equal(pk.predict_rapid(st, c, beta), ref), dims
