@@ -871,7 +871,8 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     static const bool al_env = !(getenv("RK_CS_ALIGNED") && atoi(getenv("RK_CS_ALIGNED")) == 0);
     const bool al = al_env && e.ps1 % 4 == 0;
     auto kern = occ4 ? (al ? cs_rowgen_kernel<false, 1, 288, 4, true> : cs_rowgen_kernel<false, 1, 288, 4>)
-                : ga.pl.wide == 2 ? cs_rowgen_kernel<true, 1> : ga.pl.wide == 3 ? cs_rowgen_kernel<true, 2>
+                : ga.pl.wide == 2 ? (al ? cs_rowgen_kernel<true, 1, kFftWideThreads, 1, true> : cs_rowgen_kernel<true, 1>)
+                : ga.pl.wide == 3 ? cs_rowgen_kernel<true, 2>
                 : tws ? cs_rowgen_kernel<true, 0> : cs_rowgen_kernel<false, 0>;
     RK_TRY(set_smem_attr((const void*)kern, smem));
     const dim3 grid((unsigned)ceil_div(e.ps2, ga.lpc), (unsigned)batch);
