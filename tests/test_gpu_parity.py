@@ -423,3 +423,26 @@ def test_concurrent_streams_share_one_setup(pk):
         torch.cuda.synchronize()
         for k in range(4):
             assert np.array_equal(outs[k].cpu().numpy(), want[k]), (rep, k)
+
+
+@pytest.mark.parametrize("nu,alpha", [(2.5, 0.3), (3.5, 1.0)])
+def test_kn_ridge_branch_against_oracle(pk, nu, alpha):
+    """K_N numerically singular (smooth, long-range Matern on a fine grid, L = 4): the setup adds
+    the documented ridge 1e-12 sigma2 (2L)^2 with a RuntimeWarning, exactly when the reference
+    does (rapid.py:120-135, restated by the oracle's kn_factor), and the field still matches the
+    oracle's ridged setup."""
+    rng = np.random.default_rng(21)
+    obs = rng.uniform(0, 1, size=(300, 2))
+    model = pk.CovarianceModel(1.0, alpha, nu)
+    om = ro.Model(1.0, alpha, nu)
+    og = ro.make_grid(UNIT, (100, 100), 4, obs)
+    _, ridged = ro.kn_factor(om, ro.kn_matrix(om, og, 4), 4)
+    assert ridged
+    grid = pk.build_padded_grid(UNIT, (100, 100), 4, obs)
+    with pytest.warns(RuntimeWarning, match="ridge"):
+        st = pk.build_setup(model, grid, 4, obs)
+    assert st.ridge_applied
+    ost = ro.rapid_setup(om, og, 4, obs)
+    c = rng.normal(size=300)
+    ref = ro.predict(ost, c, np.array([0.5]))
+    assert rel_err(pk.predict_rapid(st, c, np.array([0.5])), ref) < FIELD_TOL
