@@ -49,6 +49,13 @@ HEADLINE = dict(nu=2.5, L=4, m=4096)
 HEADLINE_NAME = "cfg5: predict (K1 + apply), n=50000 U[0,1]^2, 4096x4096, L=4, nu=2.5, range 0.05 (configs[4] largest cell)"
 
 
+def headline_config(world, embed, padded):
+    """The headline line's `config`, identical for both arms (`--impl reference` prints it too)."""
+    return {"workload": HEADLINE_NAME, "step": "K1 (weights kernel) + predict_rapid (T_predict, SURVEY 8(d))",
+            "embed": [int(v) for v in embed], "padded": [int(v) for v in padded],
+            "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}"}
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -721,7 +728,7 @@ def run_reference(args):
         "unit": "points/s", "n_gpus": world, "steps": len(step_s), "warmup": 1,
         "ms_per_step": round(1e3 * tot / len(step_s), 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE configs[4] shapes)",
-        "config": {"workload": HEADLINE_NAME},
+        "config": headline_config(world, st.embed_dims, og.total_dims),
         "cpu_baseline": {"value": round(value, 1), "unit": "points/s", "cores": procs, "kind": "port",
                          "sample": f"{len(step_s)} rounds x {procs} concurrent K1 + predict steps (one process per "
                                    f"core; numpy/pocketfft oracle port of rapid.py:200-261; steps capped at ~150 s "
@@ -787,11 +794,10 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; BASELINE configs[4] shapes: U[0,1]^2 obs, sinusoid-sum z)",
-        "config": {"workload": HEADLINE_NAME, "step": "K1 (weights kernel) + predict_rapid (T_predict, SURVEY 8(d))",
-                   "embed": list(st.embed_dims), "padded": list(st.grid.total_dims),
-                   "l2": "flushed (256 MB write) before every timed step", "parallelism": f"replicas x{world}",
-                   "setup_s": round(case["t_setup"], 3), "fit_s": round(case["t_fit"], 3),
-                   "broadcast_s": round(case["t_bcast"], 3)},
+        "config": headline_config(world, st.embed_dims, st.grid.total_dims),
+        "setup": {"setup_s": round(case["t_setup"], 3), "fit_s": round(case["t_fit"], 3),
+                  "broadcast_s": round(case["t_bcast"], 3), "what": "untimed: fit (rank 0), build_setup (rank 0), "
+                                                                   "NCCL broadcast to the other ranks"},
         "e2e": {"value": round(N * len(e2e_ms) * world / (e2e_tot * 1e-3), 1), "unit": "points/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": predict_roofline(case, pass_ms, pass_bytes, k1, tot_ms / args.steps, peaks, peaks_kind, "cfg5"),
