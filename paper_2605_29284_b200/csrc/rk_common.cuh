@@ -135,6 +135,28 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Exit protection of a 2-CTA cluster whose CTAs read each other's shared memory, lighter than a
+// second barrier.cluster (whose fence and L1 invalidation every thread pays): each CTA arrives
+// (release, cluster scope) on an mbarrier in its PARTNER's shared memory once all of its threads
+// have finished their remote reads, and before exiting waits (acquire, cluster scope) until its
+// own mbarrier has seen the partner's arrival.  The mbarrier (count 1) is initialised before the
+// cluster's first barrier.cluster, which publishes it.
+__device__ __forceinline__ void cluster_arrive_partner(uint64_t* bar, uint32_t partner) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(bar)), "r"(partner));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+__device__ __forceinline__ void cluster_wait_partner(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], 0;\n"
+      "@!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // make generic-proxy smem writes visible to the async (TMA) proxy before a bulk store
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

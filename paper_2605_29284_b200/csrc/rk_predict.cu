@@ -704,8 +704,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
   double2* buf = smem;
   double* S = (double*)(smem + H);                 // this half's spectrum (ldh)
   uint64_t* bar = (uint64_t*)(S + a.ldh);
+  uint64_t* xb = bar + 1;                          // exit protection (cluster_arrive_partner)
   const double2* Tb = a.T + (int64_t)b * a.T_bstride;
-  if (tl == 0) mbar_init(bar, 1);
+  if (tl == 0) {
+    mbar_init(bar, 1);
+    mbar_init(xb, 1);
+  }
   __syncthreads();
   const uint32_t colb = (uint32_t)a.nin * 16u, sb = (uint32_t)a.ldh * 8u;
   if (tl == 0) {
@@ -759,7 +763,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
       dst[0] = v[0];
       dst[1] = v[1];
     }
-    cl.sync();   // the partner's remote reads of this CTA's rows are done
+    __syncthreads();
+    if (tl == 0) cluster_arrive_partner(xb, (uint32_t)(half ^ 1));
+    cluster_wait_partner(xb);   // the partner has finished reading this CTA's shared memory
     return;
   }
   const int mid = a.row0 + ((a.nout + 1) >> 1);
@@ -770,13 +776,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
     buf[y] = cadd(e, cmulc(o, split_w(wt, y)));   // + w^-y (inverse half)
   }
   fence_async_smem();
-  cl.sync();   // the partner's remote reads of this CTA's rows are done
-  if (tl == 0 && y1 > y0) {
-    bulk_s2g(a.U + (int64_t)b * a.U_bstride + (int64_t)kx * a.ldU + (y0 - a.row0), buf + y0,
-             (uint32_t)(y1 - y0) * 16u);
-    bulk_commit();
-    bulk_wait_read0();
+  __syncthreads();   // this CTA's remote reads and its rows' combination are done
+  if (tl == 0) {
+    cluster_arrive_partner(xb, (uint32_t)(half ^ 1));
+    if (y1 > y0) {   // the store (own rows only) overlaps the wait for the partner
+      bulk_s2g(a.U + (int64_t)b * a.U_bstride + (int64_t)kx * a.ldU + (y0 - a.row0), buf + y0,
+               (uint32_t)(y1 - y0) * 16u);
+      bulk_commit();
+    }
   }
+  cluster_wait_partner(xb);   // the partner has finished reading this CTA's shared memory
+  if (tl == 0) bulk_wait_read0();
   __syncthreads();
 }
 
@@ -920,6 +930,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
   const int ya = 2 * (blockIdx.x >> 1);
   const double2* U = a.U + (int64_t)b * a.U_bstride;
   double2* buf = smem;
+  uint64_t* xb = (uint64_t*)(smem + a.ep_off);   // exit protection (cluster_arrive_partner)
+  if (tl == 0) mbar_init(xb, 1);                 // published by the first cl.sync below
   const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
   const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
   pdl_wait();
@@ -990,7 +1002,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
       out[(int64_t)y * a.ldo + x] = v;
     }
   }
-  cl.sync();   // the partner's remote reads are done before this CTA's shared memory goes away
+  __syncthreads();   // this CTA's remote reads are done
+  if (tl == 0) cluster_arrive_partner(xb, (uint32_t)(half ^ 1));
+  cluster_wait_partner(xb);   // ... and the partner's, before this CTA's shared memory goes away
 }
 
 // ----------------------------------------------------------------- launches
@@ -1212,6 +1226,8 @@ static Status launch_row_inv_split(const RowInvArgs& a0, int batch, cudaStream_t
   if (a.pl.nthr > kSplitThreads) return Status::ok();
   size_t smem = sizeof(double2) * (size_t)a.pl.n;
   smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
+  a.ep_off = tw_slot(smem);   // the exit-protection mbarrier
+  smem = (size_t)a.ep_off * 16 + 16;
   if (smem > kSmemMax) return Status::ok();
   RK_TRY(set_smem_attr((const void*)row_inv_split_kernel, smem));
   const dim3 grid((unsigned)(2 * ((a.nrows + 1) / 2)), (unsigned)batch);
