@@ -631,7 +631,7 @@ def _cpu_cs_leg(q, name, draws, procs):
 
 
 def start_cpu_legs(quick):
-    """CPU baselines in separate processes (they run while the GPU is measured)."""
+    """CPU baselines in separate processes (started after the GPU measurements)."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -765,8 +765,6 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = start_cpu_legs(args.quick)
     import paper_2605_29284_b200 as pk
     from paper_2605_29284_b200 import workloads
     peaks, peaks_kind = _peaks()
@@ -837,6 +835,11 @@ def main():
                            "roofline": predict_roofline(c2, pm2, pb2, k12, t2 / len(m2s), peaks, peaks_kind, w.name)}
             del c2
             torch.cuda.empty_cache()
+    # the CPU baselines run after every GPU measurement: concurrently, their numpy FFTs on all
+    # host cores compete with the e2e leg's host work and DMA for host memory bandwidth (measured:
+    # the cfg5 e2e step 3.5 -> 7.5 ms)
+    if rank == 0 and not args.no_cpu:
+        cpu = start_cpu_legs(args.quick)
     if cpu is not None:
         res = collect_cpu_legs(*cpu)
         cores = os.cpu_count() or 1

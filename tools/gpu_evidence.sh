@@ -6,7 +6,7 @@ TAG=${1:-b}
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"rk::|weights_kernel|split_kernel" -c 600 --csv \
+ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -k regex:"rk::|weights_kernel|split_kernel" -c 600 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 5 --warmup 3 --no-extra --no-cpu > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"row_fwd_split|col_split|row_inv_split|weights_kernel" -c 4 \
     -o gpurun_out/full_cfg5_$TAG -f python tools/profile_predict_cfg5.py 1 > /dev/null 2>&1

@@ -3,7 +3,7 @@
 # on the box (no bench line): bash tools/gpu_ncu_quick.sh <tag>
 TAG=${1:-q}
 mkdir -p gpurun_out/round2
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"rk::|weights_kernel|split_kernel" -c 600 --csv \
+ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -k regex:"rk::|weights_kernel|split_kernel" -c 600 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 5 --warmup 3 --no-extra --no-cpu > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"row_fwd_split|col_split|row_inv_split|weights_kernel" -c 4 \
     -o gpurun_out/full_cfg5_$TAG -f python tools/profile_predict_cfg5.py 1 > /dev/null 2>&1
