@@ -1349,13 +1349,16 @@ static Status build_sparse_gather(rk_setup* s) {
       s->max_pair_ent = std::max<int64_t>(s->max_pair_ent, no[a1] - no[a0]);
       s->max_half_ent = std::max<int64_t>(s->max_half_ent, std::max(no[am] - no[a0], no[a1] - no[am]));
     }
-    // per row pair p: {first node, first node of row 2p+1, first contribution}; entry
+    // per row pair p: {first node, first node of row 2p+1, first contribution, contributions
+    // of the first half of its nodes (where the split-length pass 1's second CTA starts)}; entry
     // npairs is the end sentinel, so a pair reads two adjacent records in one round trip
     const int npairs = (s->M2 + 1) / 2;
     std::vector<int4> pi(npairs + 1);
     for (int q = 0; q <= npairs; ++q) {
       const int y = std::min(2 * q, s->M2);
-      pi[q] = make_int4(rn[y], rn[std::min(y + 1, s->M2)], no[rn[y]], 0);
+      const int a0 = rn[y], a1 = rn[std::min(y + 2, s->M2)];
+      const int am = a0 + (a1 - a0 + 1) / 2;
+      pi[q] = make_int4(a0, rn[std::min(y + 1, s->M2)], no[a0], no[am] - no[a0]);
     }
     RK_CUDA_TRY(cudaMalloc(&s->pair_info, sizeof(int4) * pi.size()));
     RK_CUDA_TRY(cudaMemcpy(s->pair_info, pi.data(), sizeof(int4) * pi.size(), cudaMemcpyHostToDevice));

@@ -59,7 +59,8 @@ struct SparseSrc {
   const int32_t* ent_c;
   const double* wsort;
   const double* ent_wv;      // weight per contribution (pass 1: no wsort indirection)
-  const int4* pair_info;     // per row pair {node0, node of the odd row, contribution0, 0}
+  const int4* pair_info;     // per row pair {node0, node of the odd row, contribution0, contributions
+                             // of its first ceil(nodes / 2) nodes}
   const double* c;
   int64_t c_stride;
   int M1;
@@ -618,10 +619,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
   }
   const int n0 = P0.x, n1 = P0.y, e0 = P0.z;
   const int nn = P1.x - n0;
-  // this CTA's nodes [kA, kB) and their contributions [eA, eB) (relative to e0)
+  // this CTA's nodes [kA, kB) and their contributions [eA, eB) (relative to e0); the split
+  // point's contribution offset comes with the pair record (no dependent node_off round trip)
   const int kA = half ? (nn + 1) / 2 : 0, kB = half ? nn : (nn + 1) / 2;
-  const int eA = kA < nn ? (kA ? __ldg(&g.node_off[n0 + kA]) - e0 : 0) : (P1.z - e0);
-  const int eB = kB ? __ldg(&g.node_off[n0 + kB]) - e0 : 0;
+  const int eA = half ? P0.w : 0;
+  const int eB = half ? P1.z - e0 : P0.w;
   const int cnt = max(eB - eA, 0), nk = kB - kA;
   const int rowq = ya * g.M1;
   constexpr int U = 4;
