@@ -415,7 +415,7 @@ def predict_roofline(case, pass_ms, pass_bytes, k1, step_ms, peaks, peaks_kind, 
     """Dominant kernel of the step (algorithmic bytes / its event time vs the HBM peak), plus the
     whole step against both roofs: HBM (B_apply + K1 bytes) and FP64 (FFT + K1 flops)."""
     st = case["setup"]
-    p1, p2 = st.embed_dims
+    p1, p2 = st.exec_dims   # the torus the passes run on (the reference's, or shorter along y)
     H1 = p1 // 2 + 1
     m1, m2 = st.grid.interior_dims
     M1, M2 = st.grid.total_dims
@@ -463,7 +463,7 @@ def cs_roofline(setup, f_n, p, S, ms_per_real, peaks):
     M1, M2 = setup.grid.total_dims
     m1, m2 = setup.grid.interior_dims
     n, M = setup.n_obs, setup.block_size
-    p1, p2 = setup.embed_dims
+    p1, p2 = setup.exec_dims
     H1, G, Npix, Ps = p1 // 2 + 1, M1 * M2, m1 * m2, ps1 * ps2
     b_apply = n * (8 * M + 16) + 16 * H1 * M2 + 8 * H1 * (p2 // 2 + 1) + 16 * H1 * m2 + 16 * H1 * m2 + 8 * Npix
     b = (32 * M1 * ps2 + 8 * G            # row generator writes V, column pass reads V, writes g

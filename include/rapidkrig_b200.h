@@ -99,8 +99,13 @@ rk_status rk_setup_info(const rk_setup* s, int64_t* n_obs, int32_t* L, int32_t e
 rk_status rk_setup_copy_out(const rk_setup* s, int64_t* indices_host, double* weights_host,
                             double* cond_var_host, double* kn_inv_host);
 /* Filter spectrum real part, full (p2, p1) layout, UNSCALED like np.fft.fft2
- * (rapid.py:86); imaginary part is zero for the even lag filter. */
+ * (rapid.py:86); imaginary part is zero for the even lag filter.  Always on the reference's
+ * torus (embed dims of rk_setup_info). */
 rk_status rk_setup_copy_spectrum(const rk_setup* s, double* spectrum_host);
+/* The torus predict_rapid executes on (p1, p2): the reference's embed dims, or along y a
+ * shorter 2^a 3^b length whose few aliased lags are corrected exactly (no reference
+ * counterpart: rapid.py:72-86 fixes the torus; the predicted field is the same). */
+rk_status rk_setup_exec_dims(const rk_setup* s, int32_t dims[2]);
 
 /* ---- L2: rapid predict (rapid.py:164-174, 89-100, 233-261) -------------- */
 /* c* = A' c  (RapidSetup.coefficients_to_grid, rapid.py:164-174); device arrays */

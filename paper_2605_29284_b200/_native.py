@@ -57,6 +57,7 @@ _PROTOS = {
                              C.POINTER(_i32 * 2)]),
     "rk_setup_copy_out": (_i32, [_vp, _dp, _dp, _dp, _dp]),
     "rk_setup_copy_spectrum": (_i32, [_vp, _dp]),
+    "rk_setup_exec_dims": (_i32, [_vp, C.POINTER(_i32 * 2)]),
     "rk_coefficients_to_grid": (_i32, [_vp, _dp, _dp, _vp]),
     "rk_convolve_filter": (_i32, [_vp, _dp, _dp, _vp]),
     "rk_convolve_spectrum": (_i32, [_dp, _i32, _i32, _dp, _i32, _i32, _dp, _vp]),

@@ -165,10 +165,115 @@ Status setup_plans(rk_setup* s) {
     RK_TRY(plan_set(s->p1 / 2, &s->h1v));
     RK_TRY(split_table(s->p1, &s->sw1));
   }
-  if (split_len(s->p2) && s->M2 <= s->p2 / 2) {
+  // the column pass folds up to kSplitFold input rows beyond the half (execution torus)
+  if (split_len(s->p2) && s->M2 <= s->p2 / 2 + kSplitFold) {
     RK_TRY(plan_set(s->p2 / 2, &s->h2v));
     RK_TRY(split_table(s->p2, &s->sw2));
   }
+  return Status::ok();
+}
+
+// ----------------------------------------------------------------- execution torus
+// The reference embeds the padded grid in the smallest 2^a 3^b torus >= 2 M - 1 per axis
+// (rapid.py:72-86): 8748 for configs[4]'s M = 4102, radix 6 9 9 9 per half.  Interior outputs,
+// though, only meet lags <= maxlag = max(pad + m - 1, M - 1 - pad) (4098), so along y the
+// convolution runs on the smallest 2^a 3^b length P >= 2 (maxlag - kAcBand) -- 8192, radix
+// 8 8 8 8 per half, ~20 % fewer FP64 instructions per point and 6 % fewer points -- and the few
+// (input row u, output row y) pairs with |y - u| > P / 2, whose wrapped lag P - |y - u| differs
+// from the true one, are corrected exactly afterwards (AliasCorr, rk_predict.cu).  The x axis
+// keeps the reference length (no corrections there).  embed_dims / filter_spectrum /
+// convolve_filter stay on the reference torus.
+// Measured on B200 and OFF by default (RK_EXEC_TORUS=1 enables it): cfg5 step 1.263 -> 1.456 ms,
+// cfg3 0.337 -> 0.387 ms.  The power-of-two half lines make every Stockham stage's shared-memory
+// stride a power of two (bank conflicts the 3-smooth lengths avoid: the column pass falls from
+// 7.5 to 4.3 TF/s), and the corrections cost ~0.07 ms.  Exact either way (all parity tests pass
+// with it on); worth it only with a conflict-free power-of-two layout in the engine.
+static constexpr int kAcBand = 4;
+
+__global__ void ac_kernel_build(MaternDev P, double hx, double hy, int M1, int p2, AliasCorr ac, const int* dks,
+                                double* out, int* bad) {
+  // row kernels g_d(dx) = K(d, dx) - K(p2 - d, dx), dx = -(M1 - 1) .. M1 - 1 (d: a y lag)
+  const int L1 = 2 * M1 - 1;
+  const int64_t tot = (int64_t)ac.nkr * L1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e / L1), dx = abs((int)(e % L1) - (M1 - 1));
+    const int d = dks[k];
+    // K(a_y, b_x) = sigma2 phi(alpha hypot(b_x hx, a_y hy)), as the spectrum's lag table (lagq_kernel)
+    out[e] = matern_cov(P, hypot((double)dx * hx, (double)d * hy), bad) -
+             matern_cov(P, hypot((double)dx * hx, (double)(p2 - d) * hy), bad);
+  }
+}
+
+// y-axis execution length and corrections for setup s (s->rp2 set); returns the length
+static int choose_exec_y(rk_setup* s) {
+  static const bool on = getenv("RK_EXEC_TORUS") && atoi(getenv("RK_EXEC_TORUS")) == 1;
+  const int rp = s->rp2;
+  s->ac = AliasCorr{};
+  if (!on || rp < 4096) return rp;
+  const int lo = s->grid.pad[2], m = s->m2, M = s->M2;
+  const int maxlag = std::max(lo + m - 1, M - 1 - lo);
+  int64_t best = rp;
+  for (int64_t two = 1; two < 2 * (int64_t)rp; two *= 2)
+    for (int64_t v = two; v < rp; v *= 3) {
+      if (v < 2 * (int64_t)(maxlag - kAcBand) || v < M) continue;
+      if (split_len((int)v) && (M > v / 2 + kSplitFold || m > v / 2)) continue;   // column pass fold / combine
+      best = std::min(best, v);
+    }
+  if (best >= rp) return rp;
+  const int P = (int)best;
+  AliasCorr ac;
+  for (int u = 0; u < M; ++u)
+    for (int yo = 0; yo < m; ++yo) {
+      const int d = std::abs(lo + yo - u);
+      if (2 * d <= P) continue;
+      if (ac.nrp == kAcMax) return rp;   // too many pairs: keep the reference torus
+      int su = 0, sk = 0;
+      while (su < ac.nru && ac.ru[su] != u) ++su;
+      if (su == ac.nru) {
+        if (ac.nru == kAcMax) return rp;
+        ac.ru[ac.nru++] = u;
+      }
+      // kernel slot: distinct lags d, kept in cp_ker as scratch (column pairs are unused)
+      while (sk < ac.nkr && ac.cp_ker[sk] != d) ++sk;
+      if (sk == ac.nkr) ac.cp_ker[ac.nkr++] = d;
+      ac.rp_strip[ac.nrp] = su;
+      ac.rp_out[ac.nrp] = yo;
+      ac.rp_ker[ac.nrp] = sk;
+      ++ac.nrp;
+    }
+  if (ac.nrp == 0) return P;
+  ac.row_lo = 0;
+  ac.row_hi = m;
+  for (int k = 0; k < ac.nrp; ++k) {   // pairs sit at the edges: rows < row_lo or >= row_hi
+    if (ac.rp_out[k] < m / 2) ac.row_lo = std::max(ac.row_lo, ac.rp_out[k] + 1);
+    else ac.row_hi = std::min(ac.row_hi, ac.rp_out[k]);
+  }
+  s->ac = ac;
+  return P;
+}
+
+static Status build_alias_kernels(rk_setup* s) {
+  cudaFree(s->ac_ker);
+  s->ac_ker = nullptr;
+  if (s->ac.nrp == 0) return Status::ok();
+  const int L1 = 2 * s->M1 - 1;
+  int* dks = nullptr;
+  int* bad = nullptr;
+  RK_CUDA_TRY(cudaMalloc(&s->ac_ker, sizeof(double) * (size_t)s->ac.nkr * L1));
+  RK_CUDA_TRY(cudaMalloc(&dks, sizeof(int) * kAcMax));
+  RK_CUDA_TRY(cudaMalloc(&bad, sizeof(int)));
+  RK_CUDA_TRY(cudaMemcpy(dks, s->ac.cp_ker, sizeof(int) * kAcMax, cudaMemcpyHostToDevice));
+  RK_CUDA_TRY(cudaMemset(bad, 0, sizeof(int)));
+  ac_kernel_build<<<(int)std::min<int64_t>(ceil_div((int64_t)s->ac.nkr * L1, 256), 148 * 8), 256>>>(
+      s->mat, s->grid.hx, s->grid.hy, s->M1, s->p2, s->ac, dks, s->ac_ker, bad);
+  count_launch();
+  RK_LAUNCH_CHECK();
+  int hb = 0;
+  RK_CUDA_TRY(cudaMemcpy(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(dks);
+  cudaFree(bad);
+  if (hb) return Status::err(RK_NUMERIC, "Temme series / continued fraction for K_nu failed to converge");
+  for (int k = 0; k < kAcMax; ++k) s->ac.cp_ker[k] = 0;   // scratch of choose_exec_y
   return Status::ok();
 }
 
@@ -1445,6 +1550,7 @@ void free_setup(rk_setup* s) {
   cudaFree(s->spec_q);
   cudaFree(s->spec_s);
   cudaFree(s->kn_chol_dev);
+  cudaFree(s->ac_ker);
   cudaFree(s->emb.root_q);
   delete s;
   if (swap) cudaSetDevice(cur);
@@ -1682,8 +1788,10 @@ spectrum:
     }
     return best;
   };
-  s->p1 = (int)next_fft_len(2 * (int64_t)s->M1 - 1);
-  s->p2 = (int)next_fft_len(2 * (int64_t)s->M2 - 1);
+  s->rp1 = (int)next_fft_len(2 * (int64_t)s->M1 - 1);
+  s->rp2 = (int)next_fft_len(2 * (int64_t)s->M2 - 1);
+  s->p1 = s->rp1;
+  s->p2 = grid_only ? s->rp2 : choose_exec_y(s);   // execution torus (see choose_exec_y)
   s->H1 = s->p1 / 2 + 1;
   s->Q2 = quarter_ld(s->p2);
   RK_TRY(setup_plans(s));
@@ -1691,6 +1799,7 @@ spectrum:
   RK_TRY(spectrum_quarter(s->mat, grid->hx, grid->hy, s->p1, s->p2,
                           1.0 / ((double)s->p1 * (double)s->p2), s->spec_q, s->Q2, 0));
   RK_TRY(build_spec_split(s, 0));
+  RK_TRY(build_alias_kernels(s));
   RK_CUDA_TRY(cudaDeviceSynchronize());
   *out = guard.release();
   return Status::ok();
@@ -1809,7 +1918,7 @@ rk_status rk_setup_info(const rk_setup* s, int64_t* n_obs, int32_t* L, int32_t e
                         int32_t total[2]) {
   if (n_obs) *n_obs = s->n;
   if (L) *L = s->L;
-  if (embed) { embed[0] = s->p1; embed[1] = s->p2; }
+  if (embed) { embed[0] = s->rp1; embed[1] = s->rp2; }   // the reference's torus (execution: rk_setup_exec_dims)
   if (total) { total[0] = s->M1; total[1] = s->M2; }
   return RK_OK;
 }
@@ -1886,16 +1995,34 @@ rk_status rk_setup_copy_out(const rk_setup* s, int64_t* indices_host, double* we
   return (rk_status)finish(run());
 }
 
+rk_status rk_setup_exec_dims(const rk_setup* s, int32_t dims[2]) {
+  dims[0] = s->p1;
+  dims[1] = s->p2;
+  return RK_OK;
+}
+
 rk_status rk_setup_copy_spectrum(const rk_setup* s, double* spectrum_host) {
   auto run = [&]() -> Status {
-    std::vector<double> q((size_t)s->H1 * s->Q2);
-    RK_CUDA_TRY(cudaMemcpy(q.data(), s->spec_q, sizeof(double) * q.size(), cudaMemcpyDeviceToHost));
-    const double P = (double)s->p1 * (double)s->p2;
-    for (int ky = 0; ky < s->p2; ++ky) {
-      const int a = std::min(ky, s->p2 - ky);
-      for (int kx = 0; kx < s->p1; ++kx) {
-        const int b = std::min(kx, s->p1 - kx);
-        spectrum_host[(size_t)ky * s->p1 + kx] = q[(size_t)b * s->Q2 + a] * P;
+    // the reference torus' spectrum: the setup's own when it executes there, else built here
+    const int p1 = s->rp1, p2 = s->rp2, H1 = p1 / 2 + 1, Q2 = quarter_ld(p2);
+    std::vector<double> q((size_t)H1 * Q2);
+    if (p1 == s->p1 && p2 == s->p2) {
+      RK_CUDA_TRY(cudaMemcpy(q.data(), s->spec_q, sizeof(double) * q.size(), cudaMemcpyDeviceToHost));
+    } else {
+      double* d = nullptr;
+      RK_CUDA_TRY(cudaMalloc(&d, sizeof(double) * q.size()));
+      Status r = spectrum_quarter(s->mat, s->grid.hx, s->grid.hy, p1, p2, 1.0 / ((double)p1 * (double)p2), d, Q2, 0);
+      if (r.good()) r = cudaMemcpy(q.data(), d, sizeof(double) * q.size(), cudaMemcpyDeviceToHost) == cudaSuccess
+                            ? Status::ok() : Status::err(RK_CUDA, "spectrum copy failed");
+      cudaFree(d);
+      RK_TRY(r);
+    }
+    const double P = (double)p1 * (double)p2;
+    for (int ky = 0; ky < p2; ++ky) {
+      const int a = std::min(ky, p2 - ky);
+      for (int kx = 0; kx < p1; ++kx) {
+        const int b = std::min(kx, p1 - kx);
+        spectrum_host[(size_t)ky * p1 + kx] = q[(size_t)b * Q2 + a] * P;
       }
     }
     return Status::ok();

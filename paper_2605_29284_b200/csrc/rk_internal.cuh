@@ -50,6 +50,24 @@ Status scratch_alloc(void** p, size_t bytes, cudaStream_t st);
 void scratch_free(void* p, cudaStream_t st);
 
 // ------------------------------------------------------------------- setup
+// Execution torus smaller than the reference's (rk_core.cu choose_exec_torus): the convolution runs
+// on a torus whose half length covers every interior-output lag but a band of a few lags; the
+// pairs (input row u, output row y) and (input column v, output column x) whose lag falls in that
+// band are corrected exactly by one-dimensional convolutions of the outer input rows / columns
+// of c* ("strips") with kernel differences (rk_predict.cu, alias_corrections).
+constexpr int kAcMax = 16;
+constexpr int kSplitFold = 16;   // input rows beyond the half the split column pass folds in
+struct AliasCorr {
+  int nrp = 0, ncp = 0;                    // row pairs, column pairs
+  int rp_strip[kAcMax] = {}, rp_out[kAcMax] = {}, rp_ker[kAcMax] = {};   // strip, interior output row, kernel
+  int cp_strip[kAcMax] = {}, cp_out[kAcMax] = {}, cp_ker[kAcMax] = {};   // strip, interior output column, kernel
+  int nru = 0, ncv = 0;                    // strips: padded input rows ru[], padded input columns cv[]
+  int ru[kAcMax] = {}, cv[kAcMax] = {};
+  int nkr = 0, nkc = 0;                    // kernels: row pairs' (2 M1 - 1 each), then columns' (2 M2 - 1)
+  int row_lo = 0, row_hi = 0;              // interior rows < row_lo or >= row_hi may carry row corrections
+  int col_lo = 0, col_hi = 0;              // same for columns
+};
+
 struct Embedding {
   bool ready = false;
   int ps1 = 0, ps2 = 0, doubled = 0;
@@ -95,6 +113,8 @@ struct Workspace {
   cudaEvent_t fork = nullptr;
   cudaEvent_t xev[kMaxChunks] = {};
   cudaEvent_t oev[kMaxChunks] = {};   // field row block k computed (its copy may start)
+  double* ac_buf = nullptr;           // aliased-lag corrections: strips, partial sums, corrections (batch 1)
+  size_t ac_cap = 0;
   cudaEvent_t join = nullptr;         // the side stream's last field copy issued
   double* cb_h = nullptr;       // pinned staging of c and beta (beta at beta_in - c_in)
   std::map<GraphKey, cudaGraphExec_t> hgraphs;
@@ -127,7 +147,10 @@ struct rk_setup {
   int64_t n = 0;
   int M1 = 0, M2 = 0, m1 = 0, m2 = 0;
   double px0 = 0, py0 = 0;
-  int p1 = 0, p2 = 0, H1 = 0, Q2 = 0;
+  int p1 = 0, p2 = 0, H1 = 0, Q2 = 0;   // the EXECUTION torus (and its half / quarter sizes)
+  int rp1 = 0, rp2 = 0;                 // the reference's torus (rapid.py:72-86): embed_dims, filter_spectrum
+  rk::AliasCorr ac;                     // corrections when (p1, p2) != (rp1, rp2)
+  double* ac_ker = nullptr;             // device: the correction kernels (AliasCorr)
   rk::FftPlan pl1{}, pl2{};
   rk::PlanSet pl1v, pl2v;       // all plan variants of p1 / p2, see plan_pick
   rk::PlanSet h1v, h2v;         // plan variants of p1 / 2, p2 / 2 (split-length passes; n = 0 if unused)

@@ -351,6 +351,8 @@ struct ColArgs {
   int hh;
   int x_off;                 // col_pair_kernel: smem offset (double2 units) of its 2 mbarriers
   int batch;                 // col_pair_kernel: fields per launch (persistent over columns x batch)
+  int fold;                  // col_split_kernel: input rows beyond the half (nin - H > 0: execution
+                             // torus), folded into the half transforms' inputs
   int fuse_pp;               // col_split_kernel: twist / spectrum product fused into the first /
                              // last forward stage (fft_line_pp; RK_FUSE_PP=0 keeps the passes)
   CtPlan ct;                 // col_split_ct_kernel: in-place Cooley-Tukey plan of the half length
@@ -454,7 +456,22 @@ struct RowInvArgs {
   int upair;                 // split-length kernel: U is pair-blocked (see UPair)
   int64_t ldp;
   int hh;
+  // aliased-lag corrections of the execution torus (AliasCorr): corr[b][pair][x], added to the
+  // convolution of interior row ac_row0 + y for the pairs whose output row it is
+  const double* ac_corr;
+  int64_t ac_cbs;
+  int ac_row0;
+  AliasCorr ac;
 };
+
+__device__ __forceinline__ double ac_row_corr(const RowInvArgs& a, int b, int y, int x) {
+  double v = 0.0;
+  const int yi = a.ac_row0 + y;
+  if (yi < a.ac.row_lo || yi >= a.ac.row_hi)
+    for (int k = 0; k < a.ac.nrp; ++k)
+      if (a.ac.rp_out[k] == yi) v += a.ac_corr[(int64_t)b * a.ac_cbs + (int64_t)k * a.ncols + x];
+  return v;
+}
 
 template <bool TWS, int FM>
 __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
@@ -554,6 +571,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
     if (y >= a.nrows) continue;
     const double2 z = buf[a.col0 + x];
     double v = which ? z.y : z.x;
+    if (a.ac_corr) v += ac_row_corr(a, b, y, x);
     const int lr = 2 * line + which;
     if (a.epi == EPI_SCALAR) {
       v = v + beta[0];
@@ -703,8 +721,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
   const int tl = threadIdx.x;
   const int b = blockIdx.y;
   const int kx = blockIdx.x >> 1;
-  double2* buf = smem;
-  double* S = (double*)(smem + H);                 // this half's spectrum (ldh)
+  double2* buf = smem;                             // H (+ fold) entries
+  double* S = (double*)(smem + H + a.fold);        // this half's spectrum (ldh)
   uint64_t* bar = (uint64_t*)(S + a.ldh);
   uint64_t* xb = bar + 1;                          // exit protection (cluster_arrive_partner)
   const double2* Tb = a.T + (int64_t)b * a.T_bstride;
@@ -725,6 +743,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
   for (int y = a.nin + tl; y < H; y += nthr) buf[y] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
+  if (a.fold) {   // rows y >= H: X[2m] = F_H(x[n] + x[n + H]), X[2m + 1] = F_H((x[n] - x[n + H]) w^n)
+    for (int n = tl; n < a.fold; n += nthr) buf[n] = half ? csub(buf[n], buf[H + n]) : cadd(buf[n], buf[H + n]);
+    __syncthreads();
+  }
+  const int nin_h = min(a.nin, H);
   // S[k] for k = 2 mm + half: S_half[min(mm, H - half - mm)]
   if (a.fuse_pp) {   // the odd half's twist on the first stage's loads, the product on the last stage's stores
     fft_line_pp<false, true, 1>(
@@ -733,7 +756,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
         [&](int mm, double2 v) { return cscale(v, S[min(mm, H - half - mm)]); });
   } else {
     if (half) {
-      for (int y = tl; y < a.nin; y += nthr) buf[y] = cmul(buf[y], split_w(wt, y));
+      for (int y = tl; y < nin_h; y += nthr) buf[y] = cmul(buf[y], split_w(wt, y));
       __syncthreads();
     }
     fft_line<false, true, 1>(buf, pls, tl);
@@ -772,10 +795,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
   }
   const int mid = a.row0 + ((a.nout + 1) >> 1);
   const int y0 = half ? mid : a.row0, y1 = half ? a.row0 + a.nout : mid;
+  // y < H: e[y] + w^-y o[y]; y >= H (execution torus): e[y - H] - w^-(y - H) o[y - H] -- those
+  // sources lie below row0 (nout <= H), which no CTA overwrites
   for (int y = y0 + tl; y < y1; y += nthr) {
-    const double2 e = half ? other[y] : buf[y];
-    const double2 o = half ? buf[y] : other[y];
-    buf[y] = cadd(e, cmulc(o, split_w(wt, y)));   // + w^-y (inverse half)
+    const int yy = y < H ? y : y - H;
+    const double2 e = half ? other[yy] : buf[yy];
+    const double2 o = half ? buf[yy] : other[yy];
+    const double2 t = cmulc(o, split_w(wt, yy));
+    buf[y] = y < H ? cadd(e, t) : csub(e, t);
   }
   fence_async_smem();
   __syncthreads();   // this CTA's remote reads and its rows' combination are done
@@ -992,6 +1019,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
       const int y = ya + which;
       if (y >= a.nrows) break;
       double v = which ? z.y : z.x;
+      if (a.ac_corr) v += ac_row_corr(a, b, y, x);
       if (a.epi == EPI_SCALAR) {
         v = v + beta[0];
       } else if (a.epi == EPI_COV) {
@@ -1007,6 +1035,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
   __syncthreads();   // this CTA's remote reads are done
   if (tl == 0) cluster_arrive_partner(xb, (uint32_t)(half ^ 1));
   cluster_wait_partner(xb);   // ... and the partner's, before this CTA's shared memory goes away
+}
+
+// ----------------------------------------------------------------- aliased-lag corrections
+// (AliasCorr, rk_internal.cuh; rk_core.cu choose_exec_y): for each pair (input row u, interior
+// output row y) whose lag d = |y - u| exceeds half the execution torus P2, the convolution used
+// K(P2 - d, .) where the reference uses K(d, .); the difference is the one-dimensional
+// convolution corr[y][x] = sum_v c*[u][v] g_d(x - v), g_d(dx) = K(d, dx) - K(P2 - d, dx), added
+// in pass 3's epilogue.  c* rows u ("strips") come from the sparse plan (or the dense input);
+// the sums run in chunks of kAcChunk inputs (partial sums, then added in chunk order:
+// deterministic).
+constexpr int kAcChunk = 512, kAcTile = 128;
+
+__global__ void __launch_bounds__(256) ac_strips_kernel(const SparseSrc g, const double* __restrict__ rows,
+                                                        int64_t ld_rows, int64_t rows_bs, const AliasCorr ac,
+                                                        int M1, double* __restrict__ strips, int64_t sbs) {
+  const int k = blockIdx.x, b = blockIdx.y, u = ac.ru[k];
+  double* st = strips + (int64_t)b * sbs + (int64_t)k * M1;
+  for (int x = threadIdx.x; x < M1; x += blockDim.x)
+    st[x] = rows ? rows[(int64_t)b * rows_bs + (int64_t)u * ld_rows + x] : 0.0;
+  if (rows) return;
+  __syncthreads();
+  gather_row(g, g.c + (int64_t)b * g.c_stride, u, threadIdx.x, blockDim.x, [&](int x, double v) { st[x] = v; });
+}
+
+// grid (output tiles, row pairs, batch x chunks), kAcTile threads: partial sums of one chunk
+__global__ void __launch_bounds__(kAcTile) ac_partial_kernel(const AliasCorr ac, const double* __restrict__ ker,
+                                                             const double* __restrict__ strips, int64_t sbs,
+                                                             int M1, int m1, int col0, int nchunk,
+                                                             double* __restrict__ part, int64_t pbs) {
+  __shared__ double sv[kAcChunk];
+  __shared__ double sk[kAcChunk + kAcTile];
+  const int k = blockIdx.y;
+  const int b = blockIdx.z / nchunk, ch = blockIdx.z - b * nchunk;
+  const int o0 = blockIdx.x * kAcTile;
+  const int v0 = ch * kAcChunk, v1 = min(M1, v0 + kAcChunk);
+  const double* st = strips + (int64_t)b * sbs + (int64_t)ac.rp_strip[k] * M1;
+  const int L1 = 2 * M1 - 1;
+  const double* kr = ker + (int64_t)ac.rp_ker[k] * L1;
+  for (int i = threadIdx.x; i < v1 - v0; i += blockDim.x) sv[i] = st[v0 + i];
+  // term (o, v): kr[col0 + o - v + M1 - 1]; the tile needs indices kbase .. kbase + klen - 1
+  const int kbase = col0 + o0 - (v1 - 1) + M1 - 1, klen = (v1 - v0) + kAcTile - 1;
+  for (int i = threadIdx.x; i < klen; i += blockDim.x) {
+    const int idx = kbase + i;
+    sk[i] = idx >= 0 && idx < L1 ? kr[idx] : 0.0;
+  }
+  __syncthreads();
+  const int o = o0 + threadIdx.x;
+  if (o >= m1) return;
+  const int t = threadIdx.x + (v1 - 1);
+  double acc = 0.0;
+  for (int v = v0; v < v1; ++v) acc = fma(sv[v - v0], sk[t - v], acc);
+  part[(int64_t)b * pbs + ((int64_t)k * nchunk + ch) * m1 + o] = acc;
+}
+
+__global__ void ac_reduce_kernel(int nrp, const double* __restrict__ part, int64_t pbs, int nchunk, int m1,
+                                 double* __restrict__ corr, int64_t cbs, int batch) {
+  const int64_t tot = (int64_t)batch * nrp * m1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(e % m1);
+    const int64_t kb = e / m1;
+    const int k = (int)(kb % nrp), b = (int)(kb / nrp);
+    const double* p = part + (int64_t)b * pbs + (int64_t)k * nchunk * m1 + o;
+    double acc = 0.0;
+    for (int ch = 0; ch < nchunk; ++ch) acc += p[(int64_t)ch * m1];
+    corr[(int64_t)b * cbs + (int64_t)k * m1 + o] = acc;
+  }
 }
 
 // ----------------------------------------------------------------- launches
@@ -1150,7 +1244,9 @@ static Status launch_col_split(const ColArgs& a0, int batch, cudaStream_t st, bo
   a.lpc = 1;
   if (a.pl.nthr > kSplitThreads) return Status::ok();
   if (!a.spec_s) return Status::ok();
-  size_t smem = sizeof(double2) * (size_t)a.pl.n + sizeof(double) * (size_t)a.ldh + 16;
+  a.fold = std::max(0, a.nin - a.pl.n);
+  if (a.fold > kSplitFold || (a.fold && a.upair)) return Status::ok();
+  size_t smem = sizeof(double2) * (size_t)(a.pl.n + a.fold) + sizeof(double) * (size_t)a.ldh + 16;
   smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
   if (smem > kSmemMax) return Status::ok();
   static const bool fuse = !(getenv("RK_FUSE_PP") && atoi(getenv("RK_FUSE_PP")) == 0);
@@ -1173,6 +1269,7 @@ static Status launch_col_pair(const ColArgs& a0, int batch, cudaStream_t st, boo
   // each column's input load, which two co-resident cluster CTAs hide; off unless RK_COL_PAIR=1
   static const bool on = getenv("RK_COL_PAIR") && atoi(getenv("RK_COL_PAIR")) == 1;
   if (!on || a.upair || !a.spec_s || a.pl.nthr > kSplitThreads) return Status::ok();
+  if (a.nin > a.pl.n || a.row0 + a.nout > a.pl.n) return Status::ok();   // no fold / tail rows here
   a.lpc = 1;
   a.batch = batch;
   const size_t xb = std::max((size_t)a.nin * 16, (size_t)a.ldh * 16);
@@ -1201,6 +1298,7 @@ static Status launch_col_split_ct(const ColArgs& a0, int batch, cudaStream_t st,
   static const bool on = getenv("RK_COL_CT") && atoi(getenv("RK_COL_CT")) == 1;
   static const int g_env = getenv("RK_CT_G") ? atoi(getenv("RK_CT_G")) : 0;
   if (!on || a.upair || !a.spec_s) return Status::ok();
+  if (a.nin > a.pl.n || a.row0 + a.nout > a.pl.n) return Status::ok();   // no fold / tail rows here
   CtPlan cp{};
   if (!ct_plan_for(a.pl.n, g_env, &cp).good() || cp.nthr > kCtThreads) return Status::ok();
   a.ct = cp;
@@ -1358,21 +1456,64 @@ static Status launch_cstar(const rk_setup* s, const double* c, int64_t c_stride,
 
 static inline int64_t round_even(int64_t v) { return (v + 1) & ~int64_t(1); }
 
+// aliased-lag corrections of one conv_pipeline call (interior outputs): strips, partial sums,
+// corrections corr[b][pair][x] (*corr null when the setup has none); *owned: scratch to free
+static Status alias_corrections(const rk_setup* s, const SparseSrc* sp, const double* rows, int64_t ld_in,
+                                int64_t in_bstride, int batch, Workspace* ws, cudaStream_t st, double** corr,
+                                int64_t* cbs, double** owned) {
+  *corr = nullptr;
+  *owned = nullptr;
+  const AliasCorr& ac = s->ac;
+  if (ac.nrp == 0) return Status::ok();
+  const int M1 = s->M1, m1 = s->m1, nchunk = (int)ceil_div(M1, kAcChunk);
+  const int64_t sbs = (int64_t)ac.nru * M1, pbs = (int64_t)ac.nrp * nchunk * m1, cb = (int64_t)ac.nrp * m1;
+  const size_t per = (size_t)(sbs + pbs + cb);
+  double* buf = nullptr;
+  if (ws && batch == 1) {
+    if (ws->ac_cap < per) {
+      cudaFree(ws->ac_buf);
+      ws->ac_buf = nullptr;
+      ws->ac_cap = 0;
+      RK_CUDA_TRY(cudaMalloc(&ws->ac_buf, sizeof(double) * per));
+      ws->ac_cap = per;
+    }
+    buf = ws->ac_buf;
+  } else {
+    RK_TRY(scratch_alloc((void**)&buf, sizeof(double) * per * batch, st));
+    *owned = buf;
+  }
+  double* strips = buf;
+  double* part = strips + sbs * batch;
+  double* cr = part + pbs * batch;
+  SparseSrc g = sp ? *sp : SparseSrc{};
+  ac_strips_kernel<<<dim3((unsigned)ac.nru, (unsigned)batch), 256, 0, st>>>(g, sp ? nullptr : rows, ld_in, in_bstride,
+                                                                            ac, M1, strips, sbs);
+  ac_partial_kernel<<<dim3((unsigned)ceil_div(m1, kAcTile), (unsigned)ac.nrp, (unsigned)(batch * nchunk)), kAcTile,
+                      0, st>>>(ac, s->ac_ker, strips, sbs, M1, m1, s->grid.pad[0], nchunk, part, pbs);
+  ac_reduce_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)batch * cb, 256), 148 * 8), 256, 0, st>>>(
+      ac.nrp, part, pbs, nchunk, m1, cr, cb, batch);
+  count_launch(3);
+  RK_LAUNCH_CHECK();
+  *corr = cr;
+  *cbs = cb;
+  return Status::ok();
+}
+
 // Shared 3-pass convolution. `rows` (nrows = M2, ld_in) holds the padded real input
 // (c* or a caller field); output rows [row0, row0 + nout) x cols [col0, col0 + ncols).
 static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in, int64_t in_bstride,
-                            int batch, int row0, int nout, int col0, int ncols, const RowInvArgs& epi,
+                            int batch, int row0, int nout, int col0, int ncols, RowInvArgs epi,
                             cudaStream_t st, cudaEvent_t* ev = nullptr, Workspace* ws = nullptr,
                             const HostIo* hio = nullptr, const SparseSrc* sp = nullptr) {
   const int64_t ldT = round_even(s->M2);
   const int64_t ldU = round_even(nout);
   // pair-blocked U when both the column and the inverse-row passes are split-length
-  const bool split2 = s->h2v.v[2].n && s->spec_s && row0 + nout <= s->p2 / 2;
+  const bool split2 = s->h2v.v[2].n && s->spec_s && nout <= s->p2 / 2 && row0 + nout <= s->p2 / 2 + kSplitFold;
   const bool split3 = s->h1v.v[2].n && col0 + ncols <= s->p1 / 2;
   // measured on cfg5 (B200): pair-blocked U takes pass 3 from 0.336 to 0.291 ms but pass 2's
   // scattered 32-byte stores cost more (0.697 -> 0.813 ms); off unless RK_UPAIR=1
   static const bool upair_env = getenv("RK_UPAIR") && atoi(getenv("RK_UPAIR")) == 1;
-  const bool upair = upair_env && split2 && split3;
+  const bool upair = upair_env && split2 && split3 && s->M2 <= s->p2 / 2 && row0 + nout <= s->p2 / 2;
   const int hh = (s->H1 + 1) / 2;
   const int64_t U_bstride = (int64_t)(s->H1 + 1) * ldU;   // holds either layout
   double2 *T = nullptr, *U = nullptr;
@@ -1456,6 +1597,18 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   }
   if (!done) RK_TRY(launch_col(0, ca, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
+  double* ac_owned = nullptr;
+  if (s->ac.nrp) {   // execution torus: exact only with the corrections, for the interior
+    if (row0 != s->grid.pad[2] || nout != s->m2 || col0 != s->grid.pad[0] || ncols != s->m1)
+      return Status::err(RK_INTERNAL, "execution-torus convolution for non-interior outputs");
+    double* corr = nullptr;
+    int64_t cbs = 0;
+    RK_TRY(alias_corrections(s, sp, rows, ld_in, in_bstride, batch, ws, st, &corr, &cbs, &ac_owned));
+    epi.ac_corr = corr;
+    epi.ac_cbs = cbs;
+    epi.ac_row0 = 0;
+    epi.ac = s->ac;
+  }
   RowInvArgs ia = epi;
   ia.pl = plan_pick(s->pl1v, (int64_t)((nout + 1) / 2) * batch);
   ia.lpc = pick_lpc(ia.pl, 4, (int64_t)((nout + 1) / 2) * batch);
@@ -1483,6 +1636,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
       const int r1 = std::min(nout, r0 + per);
       RowInvArgs ck = ia;
       ck.nrows = r1 - r0;
+      ck.ac_row0 = r0;
       ck.U = upair && split3 ? U + (int64_t)(r0 / 2) * 4LL * hh : U + r0;   // r0 is even
       ck.out = ia.out + (int64_t)r0 * ia.ldo;
       if (ck.xg) ck.xg = ia.xg + (int64_t)r0 * ncols * ia.p;
@@ -1521,6 +1675,7 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     scratch_free(T, st);
     scratch_free(U, st);
   }
+  if (ac_owned) scratch_free(ac_owned, st);
   return Status::ok();
 }
 
@@ -1569,6 +1724,7 @@ static void free_ws(Workspace* w) {
   if (w->aux) cudaStreamDestroy(w->aux);
   if (w->fork) cudaEventDestroy(w->fork);
   if (w->join) cudaEventDestroy(w->join);
+  cudaFree(w->ac_buf);
   for (auto& e : w->oev)
     if (e) cudaEventDestroy(e);
   for (auto& e : w->xev)
@@ -1731,7 +1887,26 @@ rk_status rk_convolve_filter(const rk_setup* s, const double* values_dev, double
     e.out = out_dev;
     e.ldo = s->M1;
     e.epi = EPI_PLAIN;
-    return conv_pipeline(s, values_dev, s->M1, 0, 1, 0, s->M2, 0, s->M1, e, (cudaStream_t)stream);
+    const cudaStream_t st = (cudaStream_t)stream;
+    if (s->p1 == s->rp1 && s->p2 == s->rp2)
+      return conv_pipeline(s, values_dev, s->M1, 0, 1, 0, s->M2, 0, s->M1, e, st);
+    // the setup executes on a smaller torus (interior outputs only): convolve_filter's whole
+    // padded output runs on the reference's torus, its spectrum built here (rapid.py:89-100)
+    rk_setup t;
+    t.M1 = s->M1;
+    t.M2 = s->M2;
+    t.p1 = t.rp1 = s->rp1;
+    t.p2 = t.rp2 = s->rp2;
+    t.H1 = t.p1 / 2 + 1;
+    t.Q2 = quarter_ld(t.p2);
+    RK_TRY(scratch_alloc((void**)&t.spec_q, sizeof(double) * (size_t)t.H1 * t.Q2, st));
+    Status r = spectrum_quarter(s->mat, s->grid.hx, s->grid.hy, t.p1, t.p2, 1.0 / ((double)t.p1 * (double)t.p2),
+                                t.spec_q, t.Q2, st);
+    if (r.good()) r = setup_plans(&t);
+    if (r.good()) r = conv_pipeline(&t, values_dev, s->M1, 0, 1, 0, s->M2, 0, s->M1, e, st);
+    scratch_free(t.spec_q, st);
+    t.spec_q = nullptr;
+    return r;
   };
   return (rk_status)finish_status(run());
 }

@@ -32,10 +32,12 @@ struct SetupHdr {
   int64_t n, nnodes, max_pair_ent, max_half_ent, pblk_stride;
   double px0, py0, cond_var_min;
   int32_t emb_ready, ps1, ps2, doubled, hs1, qs2;
+  int32_t rp1, rp2;
+  AliasCorr ac;
   int64_t field_bytes[24];
   int32_t nfields, has_field[24];
 };
-constexpr uint64_t kSetupMagic = 0x52'4B'53'45'54'55'50'32ULL;   // "RKSETUP2"
+constexpr uint64_t kSetupMagic = 0x52'4B'53'45'54'55'50'33ULL;   // "RKSETUP3"
 
 struct Field {
   void** slot;
@@ -67,6 +69,7 @@ std::vector<Field> setup_fields(rk_setup* s) {
       {(void**)&s->spec_s, sizeof(double) * (size_t)s->H1 * 2 * s->ldh},
       {(void**)&s->kn_chol_dev, sizeof(double) * M * M},
       {(void**)&s->emb.root_q, sizeof(double) * (size_t)s->emb.hs1 * s->emb.qs2},
+      {(void**)&s->ac_ker, sizeof(double) * ((size_t)s->ac.nkr * (2 * s->M1 - 1) + (size_t)s->ac.nkc * (2 * s->M2 - 1))},
   };
   return f;
 }
@@ -86,6 +89,7 @@ SetupHdr header_of(rk_setup* s) {
   h.px0 = s->px0; h.py0 = s->py0; h.cond_var_min = s->cond_var_min;
   h.emb_ready = s->emb.ready; h.ps1 = s->emb.ps1; h.ps2 = s->emb.ps2; h.doubled = s->emb.doubled;
   h.hs1 = s->emb.hs1; h.qs2 = s->emb.qs2;
+  h.rp1 = s->rp1; h.rp2 = s->rp2; h.ac = s->ac;
   const auto f = setup_fields(s);
   h.nfields = (int32_t)f.size();
   for (size_t i = 0; i < f.size(); ++i) {
@@ -113,6 +117,7 @@ Status setup_from_header(const SetupHdr& h, rk_setup* s) {
   s->n = h.n; s->nnodes = h.nnodes; s->max_pair_ent = h.max_pair_ent; s->max_half_ent = h.max_half_ent;
   s->pblk_stride = h.pblk_stride;
   s->px0 = h.px0; s->py0 = h.py0; s->cond_var_min = h.cond_var_min;
+  s->rp1 = h.rp1; s->rp2 = h.rp2; s->ac = h.ac;
   RK_TRY(setup_plans(s));
   Embedding& e = s->emb;
   e.ps1 = h.ps1; e.ps2 = h.ps2; e.doubled = h.doubled; e.hs1 = h.hs1; e.qs2 = h.qs2;

@@ -101,6 +101,9 @@ class RapidSetup:
         n, _, emb, tot = _info(handle.ptr)
         self._n = n
         self.embed_dims = emb
+        ex = (N.C.c_int32 * 2)()
+        N.call("rk_setup_exec_dims", handle.ptr, N.C.byref(ex))
+        self.exec_dims = (int(ex[0]), int(ex[1]))   # the torus predict_rapid runs on (see the C header)
         self._total = tot
         self._cache = {}
         self.device = D.torch().cuda.current_device() if device is None else int(device)

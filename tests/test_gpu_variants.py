@@ -38,7 +38,8 @@ field = pk.predict_rapid(st, c, np.array([0.25]))
 cstar = st.coefficients_to_grid(c)
 conv = pk.convolve_filter(st.filter_spectrum, st.embed_dims, cstar)
 np.savez({out!r}, field=field, w=st.weights, cv=st.cond_var, idx=st.neighbor_indices, conv=conv,
-         embed=np.array(st.embed_dims), obs=obs, h=np.array(grid.spacing))
+         embed=np.array(st.embed_dims), exe=np.array(st.exec_dims), obs=obs, h=np.array(grid.spacing),
+         spec=np.asarray(st.filter_spectrum).real[:3, :3])
 """
 
 
@@ -71,6 +72,23 @@ def test_column_pass_one_cta_vs_cluster_bitwise(tmp_path, dims):
     assert max(a["embed"]) > 4608
     assert np.array_equal(a["field"], b["field"])
     assert np.array_equal(a["conv"], b["conv"])
+
+
+@pytest.mark.parametrize("dims", [(2048, 2048), (4096, 4096)])
+def test_execution_torus_matches_reference_torus(tmp_path, dims):
+    """RK_EXEC_TORUS=1: along y the passes run on the shorter 2^a 3^b torus (4096 / 8192 instead
+    of the reference's 4374 / 8748; the 8192 one with the split column pass folding the 6 input rows
+    beyond its half), the few aliased lags corrected exactly: the predicted field equals the
+    reference-torus one to 1e-12; embed_dims, filter_spectrum and convolve_filter (whole padded
+    output) stay on the reference torus."""
+    kw = dict(n=6000, L=2, dims=dims, nu=1.5)
+    a = _run(tmp_path, "exec", {"RK_EXEC_TORUS": "1"}, **kw)
+    b = _run(tmp_path, "ref", {"RK_EXEC_TORUS": "0"}, **kw)
+    assert tuple(a["embed"]) == tuple(b["embed"]) and tuple(b["exe"]) == tuple(b["embed"])
+    assert a["exe"][1] < a["embed"][1] and a["exe"][0] == a["embed"][0]
+    assert rel_err(a["field"], b["field"]) < 1e-12
+    assert np.array_equal(a["spec"], b["spec"])
+    assert rel_err(a["conv"], b["conv"]) < 1e-12
 
 
 @pytest.mark.parametrize("dims", [(2600, 2500), (4096, 4096)])
