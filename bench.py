@@ -764,6 +764,8 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        print(f"[bench] rank {rank}/{world}: backend {dist.get_backend()}, cuda:{local} "
+              f"({torch.cuda.get_device_name(local)}), NCCL {torch.cuda.nccl.version()}", file=sys.stderr, flush=True)
     cpu = None
     import paper_2605_29284_b200 as pk
     from paper_2605_29284_b200 import workloads
