@@ -26,6 +26,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-ffp-contract=off", "-I" + os.path.join(ROOT, "include")]
 if os.environ.get("RK_PHASE_TIMING") == "1":   # diagnostics build (tools/phase_probe.py); use force=True
     FLAGS.append("-DRK_PHASE_TIMING")
+FLAGS += os.environ.get("RK_DEFS", "").split()   # extra -D switches for measured alternatives (use force=True)
 SOURCES = ["rk_core.cu", "rk_predict.cu", "rk_sim.cu", "rk_exact.cu", "rk_refit.cu", "rk_replicate.cu"]
 
 

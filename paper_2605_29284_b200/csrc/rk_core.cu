@@ -1618,7 +1618,9 @@ static Status launch_weights(const rk_setup* s, int32_t* base, double* weights, 
     // default: L >= 3 with enough observations to fill the GPU with 8-observation tasks (measured:
     // cfg5 L = 4 0.204 -> 0.077 ms, cfg3 0.096 -> 0.050, cfg4 0.023 -> 0.014; cfg2's 1368
     // observations are 171 tasks, latency-bound: 0.016 ms one observation per warp vs 0.037)
-    const bool use_mma = mma_env >= 0 ? (mma_env != 0 && L >= 2) : (L >= 3 && n >= 2048);
+    // (tools/k1_l2_probe.py, us per launch, substitution vs tensor-core: L = 2 n = 4096 7.3 vs 8.3,
+    // n = 8192 12.4 vs 8.3, n = 50000 36.7 vs 20.6; L = 3 n = 2048 12.3 vs 14.4, n = 4096 22.6 vs 14.4)
+    const bool use_mma = mma_env >= 0 ? (mma_env != 0 && L >= 2) : (L >= 3 ? n >= 3072 : L == 2 && n >= 6144);
     auto launch_mma = [&](auto kern, size_t smem) -> Status {
       RK_TRY(set_smem_attr((const void*)kern, smem));
       int per_sm = 0;

@@ -263,10 +263,19 @@ struct FftNoOp {
   __device__ __forceinline__ double2 operator()(int, double2 v) const { return v; }
 };
 
-template <int R, bool INV, bool TWS = false, bool WIDE = false, class Pre = FftNoOp, class Post = FftNoOp>
+// SWZ (power-of-two lines, radix 8 only): the Ns = 1 stage of a 2^a line stores butterfly j's
+// outputs at 8 j + k -- a 128-byte lane stride, all eight lanes of a quarter warp on the same four
+// banks (8-way conflicts on every store; measured: the 8192^2 torus ran slower than 8748^2).
+// SWZ = 1 stores them at 8 j + (k ^ (j & 7)) instead (conflict-free), and SWZ = 2 is the next
+// stage loading element i from i ^ ((i >> 3) & 7) -- within an aligned group of eight lanes the
+// XOR is a permutation, so those loads stay conflict-free.  Only the two stages' physical
+// addresses change: same arithmetic, bitwise the same line.
+template <int R, bool INV, bool TWS = false, bool WIDE = false, class Pre = FftNoOp, class Post = FftNoOp,
+          int SWZ = 0>
 __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
                                           const double2* __restrict__ tw, uint32_t nsm, int bid = 0,
                                           const Pre& pre = Pre(), const Post& post = Post()) {
+  static_assert(SWZ == 0 || R == 8, "swizzled stages are radix 8");
   constexpr int K = WIDE ? fft_kmax_wide(R) : fft_kmax(R);
   const int nb = n / R;
   double2 a[K][R];
@@ -284,7 +293,10 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
     }
     if (j < nb) {
 #pragma unroll
-      for (int k = 0; k < R; ++k) a[q][k] = pre(j + k * nb, buf[j + k * nb]);
+      for (int k = 0; k < R; ++k) {
+        const int i = j + k * nb;   // SWZ == 2: nb % 8 == 0, so (i >> 3) & 7 = ((j >> 3) + k (nb >> 3)) & 7
+        a[q][k] = pre(i, buf[SWZ == 2 ? i ^ (((j >> 3) + k * (nb >> 3)) & 7) : i]);
+      }
       if (jm != 0) {
         const double2 w1 = TWS ? tw[jm] : __ldg(&tw[jm]);
 #if RK_TW_TREE
@@ -317,7 +329,10 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
   for (int q = 0; q < K; ++q) {
     if (outb[q] >= 0) {
 #pragma unroll
-      for (int k = 0; k < R; ++k) buf[outb[q] + k * Ns] = post(outb[q] + k * Ns, a[q][k]);
+      for (int k = 0; k < R; ++k) {
+        const int i = outb[q] + k * Ns;   // SWZ == 1: Ns = 1, outb = 8 j, so (i >> 3) & 7 = j & 7
+        buf[SWZ == 1 ? outb[q] + (k ^ ((outb[q] >> 3) & 7)) : i] = post(i, a[q][k]);
+      }
     }
   }
   group_sync(bid, nthr);
@@ -407,7 +422,8 @@ __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int 
 // Full transform of the line at `buf` by thread t (0 <= t < pl.nthr or idle beyond).
 // Must be called by every thread of the CTA (contains barriers).  FM (FFT mode): 0 normal /
 // spread plans, 1 WIDE (64-register kernels), 2 split radix-9 stages.
-template <bool INV, bool TWS = false, int FM = 0, bool MAG = true>   // MAG: magic-divisor modulo
+// PSW: swizzle between the first two radix-8 stages of a power-of-two line (fft_stage SWZ).
+template <bool INV, bool TWS = false, int FM = 0, bool MAG = true, bool PSW = false>   // MAG: magic-divisor modulo
 __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t, int bid = 0) {
   constexpr bool WIDE = FM >= 1;   // split plans also keep the small register footprint elsewhere
   const int n = pl.n, nthr = pl.nthr;
@@ -433,8 +449,18 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
     Ns *= 9;
     ++si;
   }
+  int s8 = 0;
+  if (PSW && Ns == 1 && pl.n8 >= 2 && FM != 2) {   // power-of-two line: swizzled first pair of stages
+    fft_stage<8, INV, TWS, WIDE, FftNoOp, FftNoOp, 1>(buf, n, 1, t, nthr, tw, 0u, bid);
+    ++si;
+    fft_stage<8, INV, TWS, WIDE, FftNoOp, FftNoOp, 2>(buf, n, 8, t, nthr, tw, MAG ? mg[si] : 0u, bid);
+    tw += 8;
+    Ns = 64;
+    ++si;
+    s8 = 2;
+  }
 #pragma unroll 1
-  for (int s = 0; s < pl.n8; ++s) {
+  for (int s = s8; s < pl.n8; ++s) {
     fft_stage<8, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     if (Ns > 1) tw += Ns;
     Ns *= 8;
