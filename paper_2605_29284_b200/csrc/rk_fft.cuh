@@ -270,12 +270,18 @@ struct FftNoOp {
 // stage loading element i from i ^ ((i >> 3) & 7) -- within an aligned group of eight lanes the
 // XOR is a permutation, so those loads stay conflict-free.  Only the two stages' physical
 // addresses change: same arithmetic, bitwise the same line.
+// SWZ = 3 / 4, the same for lines that start with the radix-6 stage (6 9^a ..., e.g. 4374): butterfly
+// j's outputs go to 6 j + k, so lanes j and j + 4 of a quarter warp share banks (2-way conflicts on
+// every store of that stage; ncu counted them as ~9 % of the column pass's shared-memory
+// wavefronts).  Element i lives at i ^ ((i >> 3) & 1) between the two stages: conflict-free for the
+// stores and, the next stage's n / R being even, for its loads (checked exhaustively on the host).
 template <int R, bool INV, bool TWS = false, bool WIDE = false, class Pre = FftNoOp, class Post = FftNoOp,
           int SWZ = 0>
 __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int Ns, int t, int nthr,
                                           const double2* __restrict__ tw, uint32_t nsm, int bid = 0,
                                           const Pre& pre = Pre(), const Post& post = Post()) {
-  static_assert(SWZ == 0 || R == 8, "swizzled stages are radix 8");
+  static_assert(SWZ == 0 || (SWZ <= 2 && R == 8) || (SWZ == 3 && R == 6) || (SWZ == 4 && (R == 9 || R == 8)),
+                "swizzled stages: radix 8 pairs, or radix 6 followed by radix 9 / 8");
   constexpr int K = WIDE ? fft_kmax_wide(R) : fft_kmax(R);
   const int nb = n / R;
   double2 a[K][R];
@@ -295,7 +301,7 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const int i = j + k * nb;   // SWZ == 2: nb % 8 == 0, so (i >> 3) & 7 = ((j >> 3) + k (nb >> 3)) & 7
-        a[q][k] = pre(i, buf[SWZ == 2 ? i ^ (((j >> 3) + k * (nb >> 3)) & 7) : i]);
+        a[q][k] = pre(i, buf[SWZ == 2 ? i ^ (((j >> 3) + k * (nb >> 3)) & 7) : SWZ == 4 ? i ^ ((i >> 3) & 1) : i]);
       }
       if (jm != 0) {
         const double2 w1 = TWS ? tw[jm] : __ldg(&tw[jm]);
@@ -331,7 +337,7 @@ __device__ __forceinline__ void fft_stage(double2* __restrict__ buf, int n, int 
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         const int i = outb[q] + k * Ns;   // SWZ == 1: Ns = 1, outb = 8 j, so (i >> 3) & 7 = j & 7
-        buf[SWZ == 1 ? outb[q] + (k ^ ((outb[q] >> 3) & 7)) : i] = post(i, a[q][k]);
+        buf[SWZ == 1 ? outb[q] + (k ^ ((outb[q] >> 3) & 7)) : SWZ == 3 ? i ^ ((i >> 3) & 1) : i] = post(i, a[q][k]);
       }
     }
   }
@@ -422,8 +428,9 @@ __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int 
 // Full transform of the line at `buf` by thread t (0 <= t < pl.nthr or idle beyond).
 // Must be called by every thread of the CTA (contains barriers).  FM (FFT mode): 0 normal /
 // spread plans, 1 WIDE (64-register kernels), 2 split radix-9 stages.
-// PSW: swizzle between the first two radix-8 stages of a power-of-two line (fft_stage SWZ).
-template <bool INV, bool TWS = false, int FM = 0, bool MAG = true, bool PSW = false>   // MAG: magic-divisor modulo
+// PSW: swizzled first pair of stages (fft_stage SWZ), a mask: 1 = power-of-two lines (8 8 ...),
+// 2 = lines starting 6 9 ... (each costs one more stage body in the kernel).
+template <bool INV, bool TWS = false, int FM = 0, bool MAG = true, int PSW = 0>   // MAG: magic-divisor modulo
 __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t, int bid = 0) {
   constexpr bool WIDE = FM >= 1;   // split plans also keep the small register footprint elsewhere
   const int n = pl.n, nthr = pl.nthr;
@@ -432,17 +439,28 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
   int Ns = 1, si = 0;   // si: stage index (magic divisors)
   // the radix-6 / 3 stage first: as the Ns = 1 stage it needs no twiddles, which keeps the WIDE
   // kernels' two-butterfly radix-6 stage inside 64 registers
+  int s9 = 0;
   if (pl.r3 == 6) {
-    fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
-    Ns *= 6;
-    ++si;
+    if ((PSW & 2) && FM != 2 && pl.n9 >= 1) {   // swizzled radix-6 / first radix-9 pair (fft_stage SWZ 3 / 4)
+      fft_stage<6, INV, TWS, WIDE, FftNoOp, FftNoOp, 3>(buf, n, 1, t, nthr, tw, 0u, bid);
+      ++si;
+      fft_stage<9, INV, TWS, WIDE, FftNoOp, FftNoOp, 4>(buf, n, 6, t, nthr, tw, MAG ? mg[si] : 0u, bid);
+      tw += 6;
+      Ns = 54;
+      ++si;
+      s9 = 1;
+    } else {
+      fft_stage<6, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
+      Ns *= 6;
+      ++si;
+    }
   } else if (pl.r3 == 3) {
     fft_stage<3, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     Ns *= 3;
     ++si;
   }
 #pragma unroll 1
-  for (int s = 0; s < pl.n9; ++s) {
+  for (int s = s9; s < pl.n9; ++s) {
     if (FM == 2) fft_stage9_split<INV, TWS>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     else fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, MAG ? mg[si] : 0u, bid);
     if (Ns > 1) tw += Ns;
@@ -450,7 +468,7 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
     ++si;
   }
   int s8 = 0;
-  if (PSW && Ns == 1 && pl.n8 >= 2 && FM != 2) {   // power-of-two line: swizzled first pair of stages
+  if ((PSW & 1) && Ns == 1 && pl.n8 >= 2 && FM != 2) {   // power-of-two line: swizzled first pair of stages
     fft_stage<8, INV, TWS, WIDE, FftNoOp, FftNoOp, 1>(buf, n, 1, t, nthr, tw, 0u, bid);
     ++si;
     fft_stage<8, INV, TWS, WIDE, FftNoOp, FftNoOp, 2>(buf, n, 8, t, nthr, tw, MAG ? mg[si] : 0u, bid);
@@ -484,24 +502,32 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
 // and the spectrum product after it).  Schedules {3 or 6} 9^n9 only (fft_line_pp_ok); the stage
 // arithmetic is fft_line's, so the transform is bitwise the same as hooks applied in passes.
 inline bool fft_line_pp_ok(const FftPlan& pl) { return pl.r3 > 1 && pl.n9 >= 1 && pl.n8 == 0 && pl.r2 == 1; }
-template <bool INV, bool TWS, int FM, class Pre, class Post>
+template <bool INV, bool TWS, int FM, class Pre, class Post, bool PSW = false>
 __device__ __forceinline__ void fft_line_pp(double2* __restrict__ buf, const FftPlan& pl, int t, int bid,
                                             const Pre& pre, const Post& post) {
   constexpr bool WIDE = FM >= 1;
   const int n = pl.n, nthr = pl.nthr;
   const double2* tw = pl.tw;
   const uint32_t* mg = reinterpret_cast<const uint32_t*>(pl.tw + pl.ntw - kFftMagicSlots);
-  int Ns;
+  int Ns, si = 1, s9 = 0;
   if (pl.r3 == 6) {
-    fft_stage<6, INV, TWS, WIDE, Pre, FftNoOp>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
-    Ns = 6;
+    if (PSW && pl.n9 >= 2) {   // swizzled radix-6 / first radix-9 pair, as fft_line
+      fft_stage<6, INV, TWS, WIDE, Pre, FftNoOp, 3>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
+      fft_stage<9, INV, TWS, WIDE, FftNoOp, FftNoOp, 4>(buf, n, 6, t, nthr, tw, mg[1], bid);
+      tw += 6;
+      Ns = 54;
+      si = 2;
+      s9 = 1;
+    } else {
+      fft_stage<6, INV, TWS, WIDE, Pre, FftNoOp>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
+      Ns = 6;
+    }
   } else {
     fft_stage<3, INV, TWS, WIDE, Pre, FftNoOp>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
     Ns = 3;
   }
-  int si = 1;
 #pragma unroll 1
-  for (int s = 0; s < pl.n9 - 1; ++s) {
+  for (int s = s9; s < pl.n9 - 1; ++s) {
     fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, mg[si], bid);
     tw += Ns;
     Ns *= 9;

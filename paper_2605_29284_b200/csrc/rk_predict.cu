@@ -303,7 +303,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
   const FftPlan pls = TWS ? twiddles_commit(a.pl, twp, smem + a.tw_off) : a.pl;
   __syncthreads();
   RK_PHASE(0, 2);
-  fft_line<false, TWS, FM, true, FM == 1>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+  fft_line<false, TWS, FM, true, FM == 1 ? 3 : 0>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
   if (a.lpc > 1) __syncthreads();   // the split below reads every line
   RK_PHASE(0, 3);
   pdl_trigger();   // the column pass may start staging while the split rows are stored
@@ -401,13 +401,13 @@ __global__ void RK_FFT_BOUNDS(FM) col_kernel(const ColArgs a) {
   mbar_wait(bar, 0);
   __syncthreads();
   RK_PHASE(1, 1);
-  fft_line<false, TWS, FM, true, FM == 1>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+  fft_line<false, TWS, FM, true, FM == 1 ? 3 : 0>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
   RK_PHASE(1, 2);
   if (MODE == 0) {
     const double* S = specs + (size_t)line * a.ldq;
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     group_sync(a.lpc > 1 ? 1 + line : 0, nthr);
-    fft_line<true, TWS, FM, true, FM == 1>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+    fft_line<true, TWS, FM, true, FM == 1 ? 3 : 0>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
     RK_PHASE(1, 3);
     pdl_trigger();
     // TMA bulk store of the kept rows
@@ -558,7 +558,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
   __syncthreads();
   RK_PHASE(2, 2);
   double2* buf = smem + (size_t)line * n;
-  fft_line<true, TWS, FM, true, FM == 1>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+  fft_line<true, TWS, FM, true, FM == 1 ? 1 : 0>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
   if (xwait) mbar_wait(bar, 0);   // init is ordered by the barrier above
   RK_PHASE(2, 3);
   const int ya = 2 * (blockIdx.x * a.lpc + line);
@@ -685,7 +685,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
     for (int x = tl; x < a.ncols; x += nthr) buf[x] = cmul(buf[x], split_w(wt, x));
     __syncthreads();
   }
-  fft_line<false, true, 1, true, true>(buf, pls, tl);
+  fft_line<false, true, 1, true, 3>(buf, pls, tl);
   pdl_trigger();
   // Z[kx], kx = 2 mm + half, is buf[mm]; conj Z[P - kx] comes from the same half
   const int Hf = H + 1;
@@ -750,20 +750,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
   const int nin_h = min(a.nin, H);
   // S[k] for k = 2 mm + half: S_half[min(mm, H - half - mm)]
   if (a.fuse_pp) {   // the odd half's twist on the first stage's loads, the product on the last stage's stores
-    fft_line_pp<false, true, 1>(
-        buf, pls, tl, 0,
-        [&](int y, double2 v) { return half ? cmul(v, split_w(wt, y)) : v; },
-        [&](int mm, double2 v) { return cscale(v, S[min(mm, H - half - mm)]); });
+    auto pre_tw = [&](int y, double2 v) { return half ? cmul(v, split_w(wt, y)) : v; };
+    auto post_sp = [&](int mm, double2 v) { return cscale(v, S[min(mm, H - half - mm)]); };
+    fft_line_pp<false, true, 1, decltype(pre_tw), decltype(post_sp), true>(buf, pls, tl, 0, pre_tw, post_sp);
   } else {
     if (half) {
       for (int y = tl; y < nin_h; y += nthr) buf[y] = cmul(buf[y], split_w(wt, y));
       __syncthreads();
     }
-    fft_line<false, true, 1, true, true>(buf, pls, tl);
+    fft_line<false, true, 1, true, 3>(buf, pls, tl);
     for (int mm = tl; mm < H; mm += nthr) buf[mm] = cscale(buf[mm], S[min(mm, H - half - mm)]);
     __syncthreads();
   }
-  fft_line<true, true, 1, true, true>(buf, pls, tl);
+  fft_line<true, true, 1, true, 3>(buf, pls, tl);
   pdl_trigger();
   cl.sync();   // both halves transformed
   const double2* other = cl.map_shared_rank(buf, half ^ 1);
@@ -861,7 +860,7 @@ __global__ void __launch_bounds__(2 * kSplitThreads, 1) col_pair_kernel(const Co
     mbar_expect_tx(bar + 1, (uint32_t)a.ldh * 16u);
     bulk_g2s(smem + 2 * H, a.spec_s + (int64_t)kx * 2 * a.ldh, (uint32_t)a.ldh * 16u, bar + 1);
   }
-  fft_line<false, true, 1, true, true>(mine, pls, tl, 1 + grp);
+  fft_line<false, true, 1, true, 3>(mine, pls, tl, 1 + grp);
   mbar_wait(bar + 1, 0);
   {
     const int half = grp ^ 1;
@@ -869,7 +868,7 @@ __global__ void __launch_bounds__(2 * kSplitThreads, 1) col_pair_kernel(const Co
     for (int mm = tl; mm < H; mm += G) mine[mm] = cscale(mine[mm], S[min(mm, H - half - mm)]);
   }
   group_sync(1 + grp, G);
-  fft_line<true, true, 1, true, true>(mine, pls, tl, 1 + grp);
+  fft_line<true, true, 1, true, 3>(mine, pls, tl, 1 + grp);
   __syncthreads();   // both halves transformed
   for (int y = a.row0 + (int)threadIdx.x; y < a.row0 + a.nout; y += 2 * G)
     B[y] = cadd(B[y], cmulc(A[y], split_w(wt, y)));   // even + w^-y odd
@@ -998,7 +997,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
     }
   }
   __syncthreads();
-  fft_line<true, true, 1, true, true>(buf, pls, tl);
+  fft_line<true, true, 1, true, 3>(buf, pls, tl);
   cl.sync();   // both halves transformed
   const double2* other = cl.map_shared_rank(buf, half ^ 1);
   const double* beta = a.beta ? a.beta + (int64_t)b * a.p : nullptr;

@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(kFftWideThreads, 1) cs_rowgen_split_kernel(con
     }
   }
   __syncthreads();
-  fft_line<true, true, 1>(half ? bo : be, pls, tl, 1 + half);
+  fft_line<true, true, 1, true, 2>(half ? bo : be, pls, tl, 1 + half);
   __syncthreads();   // both halves
   double2* V = a.V + (int64_t)b * a.V_bstride;
   for (int ix = threadIdx.x; ix < a.keep; ix += blockDim.x)
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(kFftWideThreads, 1) cs_col_split_kernel(const 
         make_double2(0.5 * ((A.x + Am.x) - (B.y - Bm.y)), 0.5 * ((A.y - Am.y) + (B.x + Bm.x)));
   }
   __syncthreads();
-  fft_line<true, true, 1>(half ? bo : be, pls, tl, 1 + half);
+  fft_line<true, true, 1, true, 2>(half ? bo : be, pls, tl, 1 + half);
   __syncthreads();   // both halves
   double* g = a.g + (int64_t)b * a.g_bstride;
   for (int y = threadIdx.x; y < a.keep; y += blockDim.x) {
