@@ -157,6 +157,19 @@ __device__ __forceinline__ void cluster_wait_partner(uint64_t* bar) {
       : "memory");
 }
 
+// 256-bit global accesses (sm_100: LDG.256 / STG.256), 32-byte aligned: two adjacent double2 in one
+// request -- the transposed row-pair pieces of T and U are 32 bytes per (column, row pair), and
+// the strided gathers / scatters of passes 1 and 3 are bound by the number of L1 requests
+__device__ __forceinline__ void ldg256(const double2* p, double2& a, double2& b) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void stg256(double2* p, double2 a, double2 b) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y) : "memory");
+}
+__device__ __forceinline__ bool aligned32(const void* p, int64_t ld_elems16) {
+  return ((uintptr_t)p & 31) == 0 && (ld_elems16 & 1) == 0;
+}
+
 // make generic-proxy smem writes visible to the async (TMA) proxy before a bulk store
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

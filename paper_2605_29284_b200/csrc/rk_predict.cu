@@ -311,18 +311,34 @@ __global__ void RK_FFT_BOUNDS(FM) row_fwd_kernel(const RowFwdArgs a) {
   const int nr = 2 * a.lpc;
   const int H = n / 2 + 1;
   double2* T = a.T + (int64_t)b * a.T_bstride;
-  for (int idx = threadIdx.x; idx < H * nr; idx += blockDim.x) {
-    const int r = idx % nr, kx = idx / nr;
-    const int l = r >> 1;
-    const int row = 2 * (blockIdx.x * a.lpc + l) + (r & 1);
-    if (row >= a.nrows) continue;
-    const double2* bl = smem + (size_t)l * n;
-    const double2 z = bl[kx];
-    const double2 zc = bl[kx == 0 ? 0 : n - kx];
-    double2 o;
-    if ((r & 1) == 0) o = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
-    else o = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
-    T[(int64_t)kx * a.ldT + row] = o;
+  if (aligned32(T, a.ldT)) {   // both rows of a pair in one 32-byte store (one thread per (kx, pair))
+    for (int idx = threadIdx.x; idx < H * a.lpc; idx += blockDim.x) {
+      const int l = idx % a.lpc, kx = idx / a.lpc;
+      const int row = 2 * (blockIdx.x * a.lpc + l);
+      if (row >= a.nrows) continue;
+      const double2* bl = smem + (size_t)l * n;
+      const double2 z = bl[kx];
+      const double2 zc = bl[kx == 0 ? 0 : n - kx];
+      const double2 o0 = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+      const double2 o1 = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+      double2* dst = T + (int64_t)kx * a.ldT + row;
+      if (row + 1 < a.nrows) stg256(dst, o0, o1);
+      else dst[0] = o0;
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < H * nr; idx += blockDim.x) {
+      const int r = idx % nr, kx = idx / nr;
+      const int l = r >> 1;
+      const int row = 2 * (blockIdx.x * a.lpc + l) + (r & 1);
+      if (row >= a.nrows) continue;
+      const double2* bl = smem + (size_t)l * n;
+      const double2 z = bl[kx];
+      const double2 zc = bl[kx == 0 ? 0 : n - kx];
+      double2 o;
+      if ((r & 1) == 0) o = make_double2(0.5 * (z.x + zc.x), 0.5 * (z.y - zc.y));
+      else o = make_double2(0.5 * (z.y + zc.y), -0.5 * (z.x - zc.x));
+      T[(int64_t)kx * a.ldT + row] = o;
+    }
   }
   RK_PHASE(0, 4);
 }
@@ -527,6 +543,7 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
   // line's 2188 entries in one round trip; 8 deep spilled the 64-register kernels)
   const int tot = a.lpc * H;
   constexpr int D = 5;
+  const bool al32 = aligned32(U, a.ldU);   // row pairs start at even rows
   for (int base = threadIdx.x; base < tot; base += D * blockDim.x) {
     double2 A[D], B[D];
 #pragma unroll
@@ -537,8 +554,12 @@ __global__ void RK_FFT_BOUNDS(FM) row_inv_kernel(const RowInvArgs a) {
         const int l = idx % a.lpc, k = idx / a.lpc;
         const int ya = 2 * (blockIdx.x * a.lpc + l);
         const double2* u = U + (int64_t)k * a.ldU + ya;
-        if (ya < a.nrows) A[d] = u[0];
-        if (ya + 1 < a.nrows) B[d] = u[1];
+        if (ya + 1 < a.nrows && al32) {
+          ldg256(u, A[d], B[d]);   // both rows' entries in one 32-byte request
+        } else {
+          if (ya < a.nrows) A[d] = u[0];
+          if (ya + 1 < a.nrows) B[d] = u[1];
+        }
       }
     }
 #pragma unroll
@@ -968,6 +989,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
   const int nk = (Hf - half + 1) / 2;
   const bool vA = ya < a.nrows, vB = ya + 1 < a.nrows;
   constexpr int D = 5;   // 5 x 512 threads cover a half line's <= 2305 entries in one round trip
+  // (one 256-bit load per row pair, as row_inv_kernel does, measured slower here: the aligned
+  // 8-register groups make the 64-register kernel spill; cfg5 pass 3 0.250 -> 0.258 ms)
   for (int base = tl; base < nk; base += D * nthr) {
     double2 A[D], B[D];
 #pragma unroll
