@@ -92,7 +92,9 @@ __device__ __forceinline__ FftPlan twiddles_commit(const FftPlan& pl, const TwPr
 // WIDE kernels (__launch_bounds__(1024): 64 registers) hold one radix-8/9 butterfly or two
 // smaller ones per thread, so a line spreads over up to 1024 threads and an SM keeps 32
 // FFT warps resident instead of 16
-__host__ __device__ constexpr int fft_kmax_wide(int r) { return r >= 8 ? 1 : 2; }
+// (radix 3: three, the registers of one radix-9 butterfly -- an odd line 3 9^a, e.g. 2187, then
+// needs n / 9 threads instead of n / 6, so its radix-9 stages keep every thread busy)
+__host__ __device__ constexpr int fft_kmax_wide(int r) { return r >= 8 ? 1 : r == 3 ? 3 : 2; }
 // threads per SM (and at most per line) of the WIDE kernels' launch bound
 constexpr int kFftWideThreads = 1024;
 // resident threads per SM of the split-radix-9 kernels (launch bound 576: <= 113 registers,
