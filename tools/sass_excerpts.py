@@ -11,7 +11,8 @@ LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 KERNELS = ["row_fwd_split_kernel", "col_split_kernel", "row_inv_split_kernel", "weights_kernel_mma<4, true>",
            "col_kernel<0, true, 1>", "row_fwd_kernel<3, true, 1>", "row_inv_kernel<true, 1>",
            "cs_rowgen_kernel<false, 1, 288, 4, true>", "cs_rowgen_split_kernel<true>", "trmm_panel_kernel<false, 1>"]
-KEYS = ["UBLKCP", "UTMALDG", "UTMASTG", "SYNCS", "UCGABAR", "BAR.SYNC", "DMMA", "DFMA", "SHFL", "STL", "LDL"]
+KEYS = ["UBLKCP", "UTMALDG", "UTMASTG", "SYNCS", "UCGABAR", "BAR.SYNC", "DMMA", "DFMA", "SHFL", "LDG.E.ENL2.256", "STG.E.ENL2.256",
+        "STL", "LDL"]
 
 txt = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s+Function : ", txt)
