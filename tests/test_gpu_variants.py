@@ -228,3 +228,22 @@ def test_host_path_large_field_block_copies_bitwise():
             pk.predict_rapid(st, ch, beta, out=out)
             assert np.array_equal(out, ref), dims
         assert np.array_equal(pk.predict_rapid(st, c, beta), ref), dims
+
+
+@pytest.mark.parametrize("dims,L", [((115, 118), 2),    # torus 243 = 3 9^2: radix-3 stage, three butterflies per thread
+                                    ((124, 120), 2),    # 256 / 243
+                                    ((124, 126), 1),    # 256 = 8 8 4: swizzled radix-8 pair
+                                    ((250, 254), 1),    # 512 = 8^3
+                                    ((200, 230), 2),    # 432 = 6 9 8 and 486 = 6 9 9: swizzled radix-6 / radix-9 pair
+                                    ((180, 100), 3),    # 384 = 6 8 8 and 216 = 6 9 4
+                                    ((1000, 990), 1)])  # 2048 = 8 8 8 4
+def test_wide_plans_match_normal_plans(tmp_path, dims, L):
+    """The WIDE FFT plans (64-register kernels: swizzled first stage pairs, fft_kmax_wide
+    butterflies per thread) forced on tori of every first-stage family (RK_WIDE=3) against the
+    normal plans (RK_WIDE=0): the same stage arithmetic in a different thread mapping and a
+    different shared-memory layout between the first two stages -- bitwise identical fields."""
+    kw = dict(n=300, L=L, dims=dims, nu=1.5)
+    a = _run(tmp_path, "wide", {"RK_WIDE": "3"}, **kw)
+    b = _run(tmp_path, "normal", {"RK_WIDE": "0"}, **kw)
+    assert np.array_equal(a["field"], b["field"])
+    assert np.array_equal(a["conv"], b["conv"])
