@@ -12,6 +12,7 @@
 //   refit_coefficients/_gls   exact.py:59-68,108-113 -> gls_batch (rk_exact.cu)
 //   conditional_draw / generate_ensemble simulate.py:146-192 -> rk_ensemble_accumulate
 //   fit / _cholesky_with_ridge exact.py:25-37,71-105 -> rk_fit_create (rk_exact.cu)
+#include <cooperative_groups.h>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -23,6 +24,8 @@
 
 #include "rk_internal.cuh"
 #include "rk_ndtri.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rk {
 
@@ -761,6 +764,118 @@ __global__ void __launch_bounds__(kFftWideThreads, 1) cs_rowgen_split_kernel(con
     V[(int64_t)ix * a.ldV + iy] = cadd(be[ix], cmulc(bo[ix], split_w(wt, ix)));
 }
 
+// The same row pass with ONE half line per CTA of a 2-CTA cluster (two CTAs, i.e. two rows' worth of
+// half lines, per SM, where cs_rowgen_split_kernel's single 140 KB CTA per SM cannot overlap its
+// generation, transform and store phases).  A measured alternative (RK_CS_PAIR=1): no faster.  The row's Philox
+// groups are dealt to the two CTAs warp by warp; each group's four elements alternate between
+// the even and the odd half line, so every CTA stores two of them locally and two into its
+// partner's line over DSMEM.  After the transforms the halves are combined as in the predict
+// passes, each CTA finishing half the kept columns.  Same arithmetic per element as
+// cs_rowgen_split_kernel: bitwise the same field.
+constexpr int kCsPairThreads = 512;
+
+template <bool AL = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCsPairThreads, 2) cs_rowgen_pair_kernel(const CsGenArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int half = (int)cl.block_rank();
+  const int H = a.pl.n;
+  const int tl = threadIdx.x;
+  const int nthr = blockDim.x;   // == a.pl.nthr
+  const int lane = tl & 31, warp = tl >> 5, nwarps = nthr >> 5;
+  const int b = blockIdx.y;
+  const int iy = blockIdx.x >> 1;
+  double2* buf = smem;                                        // this CTA's half line (x % 2 == half)
+  double2* remote = cl.map_shared_rank(buf, half ^ 1);
+  double* wq = (double*)(smem + a.q_off) + (size_t)warp * kSplitQcap;
+  uint64_t* xb = (uint64_t*)(smem + a.sw.off + 128 + a.sw.nhi);   // exit protection
+  if (tl == 0) mbar_init(xb, 1);
+  const FftPlan pls = fft_twiddles_to_smem(a.pl, smem + a.tw_off);
+  const double2* wt = stage_split_tw(a.sw, smem + a.sw.off);
+  const uint64_t fs = a.direct ? a.seed : draw_seed(draw_seed(a.seed, (uint64_t)(a.j0 + b)), 101);
+  const uint64_t Ps = (uint64_t)a.ps1 * (uint64_t)a.ps2;
+  const uint64_t wre = (uint64_t)iy * a.ps1, wim = Ps + wre;   // simulate.py:114-115
+  const double* rq = a.root_q + (int64_t)min(iy, a.ps2 - iy) * a.rq_ld;
+  const int ng = (a.ps1 + 3) / 4;
+  cl.sync();   // the partner runs (remote stores may follow); publishes xb
+  for (int c = 2 * warp + half; 32 * c < ng; c += 2 * nwarps) {   // warp-uniform: 32 groups per turn
+    const int g = 32 * c + lane;
+    const int x0 = 4 * g;
+    uint64_t re[4], im[4];
+    if (AL) {
+      uint64_t fk;   // opaque per group (see cs_rowgen_kernel)
+      asm volatile("mov.b64 %0, %1;" : "=l"(fk) : "l"(fs));
+      philox4x64_10_x2(((wre + x0) >> 2) + 1, ((wim + x0) >> 2) + 1, fk, 0, re, im);
+    } else {
+      philox_words4(wre + x0, fs, re);
+      philox_words4(wim + x0, fs, im);
+    }
+    double uu[8], z[8];
+    unsigned tmask = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uu[q] = word_uniform(q < 4 ? re[q] : im[q - 4]);
+      if (g < ng && (AL || x0 + (q & 3) < a.ps1) && ndtri_is_tail(uu[q])) tmask |= 1u << q;
+    }
+    ndtri_central_n<8>(uu, z);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (tmask >> q & 1) z[q] = uu[q];
+    const int cnt = __popc(tmask);
+    int off = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;
+    if (total > min(kSplitQcap, a.qcap)) {   // queue overflow (rare): each lane evaluates its own
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) z[q] = ndtri_tail(uu[q]);
+    } else if (total) {
+      int o = off;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) wq[o++] = z[q];
+      __syncwarp();
+      for (int k = lane; k < total; k += 32) wq[k] = ndtri_tail(wq[k]);
+      __syncwarp();
+      o = off;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (tmask >> q & 1) z[q] = wq[o++];
+      __syncwarp();
+    }
+    if (g < ng) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int x = x0 + q;
+        if (x < a.ps1) {
+          const double r = __ldg(&rq[min(x, a.ps1 - x)]);
+          ((q & 1) == half ? buf : remote)[x >> 1] = make_double2(r * z[q], r * z[4 + q]);   // x0 is even
+        }
+      }
+    }
+  }
+  cl.sync();   // both CTAs' elements are in both half lines
+  fft_line<true, true, 1, true, 2>(buf, pls, tl);
+  cl.sync();   // both halves transformed
+  const double2* other = cl.map_shared_rank(buf, half ^ 1);
+  double2* V = a.V + (int64_t)b * a.V_bstride;
+  const int km = (a.keep + 1) >> 1;
+  const int i0 = half ? km : 0, i1 = half ? a.keep : km;
+  for (int ix = i0 + tl; ix < i1; ix += nthr) {
+    const double2 e = half ? other[ix] : buf[ix];
+    const double2 o = half ? buf[ix] : other[ix];
+    V[(int64_t)ix * a.ldV + iy] = cadd(e, cmulc(o, split_w(wt, ix)));
+  }
+  __syncthreads();   // this CTA's remote reads are done
+  if (tl == 0) cluster_arrive_partner(xb, (uint32_t)(half ^ 1));
+  cluster_wait_partner(xb);   // ... and the partner's, before this CTA's shared memory goes away
+}
+
 __global__ void __launch_bounds__(kFftWideThreads, 1) cs_col_split_kernel(const CsColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int H = a.pl.n, P = 2 * H;
@@ -831,7 +946,30 @@ static Status uncond_fields(rk_setup* s, uint64_t seed, int64_t j0, int direct, 
     by = (size_t)ga.tw_off * 16 + sizeof(double2) * (size_t)ga.pl.ntw;
     ga.sw.off = (int)((by + 15) / 16);
     by = (size_t)ga.sw.off * 16 + sizeof(double2) * (size_t)(128 + ga.sw.nhi);
-    if (by <= 227 * 1024) {
+    // RK_CS_PAIR=1: one half line per CTA of a 2-CTA cluster (two CTAs per SM) where it fits.
+    // Bitwise the same field (test_gpu_variants) and measured no faster than the one-CTA kernel
+    // (configs[4] CS 3.95 vs 3.94 ms per realization), so off by default.
+    static const bool pair_env = getenv("RK_CS_PAIR") && atoi(getenv("RK_CS_PAIR")) != 0;
+    if (pair_env && ga.pl.nthr <= kCsPairThreads) {
+      CsGenArgs pa = ga;
+      size_t pb = sizeof(double2) * (size_t)pa.pl.n;
+      pa.q_off = (int)((pb + 15) / 16);
+      pb = (size_t)pa.q_off * 16 + sizeof(double) * (size_t)(pa.pl.nthr / 32) * kSplitQcap;
+      pa.tw_off = (int)((pb + 15) / 16);
+      pb = (size_t)pa.tw_off * 16 + sizeof(double2) * (size_t)pa.pl.ntw;
+      pa.sw.off = (int)((pb + 15) / 16);
+      pb = (size_t)pa.sw.off * 16 + sizeof(double2) * (size_t)(128 + pa.sw.nhi) + 16;   // + the exit mbarrier
+      if (pb <= 113 * 1024) {
+        static const bool al_env = !(getenv("RK_CS_ALIGNED") && atoi(getenv("RK_CS_ALIGNED")) == 0);
+        auto pkern = al_env && e.ps1 % 4 == 0 ? cs_rowgen_pair_kernel<true> : cs_rowgen_pair_kernel<false>;
+        RK_TRY(set_smem_attr((const void*)pkern, pb));
+        pkern<<<dim3((unsigned)(2 * e.ps2), (unsigned)batch), pa.pl.nthr, pb, st>>>(pa);
+        count_launch();
+        RK_LAUNCH_CHECK();
+        gen_done = true;
+      }
+    }
+    if (!gen_done && by <= 227 * 1024) {
       static const bool al_env = !(getenv("RK_CS_ALIGNED") && atoi(getenv("RK_CS_ALIGNED")) == 0);
       auto gkern = al_env && e.ps1 % 4 == 0 ? cs_rowgen_split_kernel<true> : cs_rowgen_split_kernel<false>;
       RK_TRY(set_smem_attr((const void*)gkern, by));

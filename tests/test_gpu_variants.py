@@ -247,3 +247,37 @@ def test_wide_plans_match_normal_plans(tmp_path, dims, L):
     b = _run(tmp_path, "normal", {"RK_WIDE": "0"}, **kw)
     assert np.array_equal(a["field"], b["field"])
     assert np.array_equal(a["conv"], b["conv"])
+
+
+CS_CODE = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2605_29284_b200 as pk
+from paper_2605_29284_b200.simulate import embedding_dims
+rng = np.random.default_rng(5)
+obs = rng.uniform(0, 1, size=(50, 2))
+model = pk.CovarianceModel(1.0, {alpha}, {nu}, 0.01)
+grid = pk.build_padded_grid((0, 1, 0, 1), {dims}, {L}, obs)
+fields = [pk.sim_unconditional_grid(model, grid, seed) for seed in (3, 2 ** 63 + 5)]
+np.savez({out!r}, f0=fields[0], f1=fields[1], emb=np.array(embedding_dims(model, grid)[:2]))
+"""
+
+
+@pytest.mark.parametrize("dims,L,nu,alpha", [((2400, 40), 1, 1.5, 40.0),     # row torus 5184 = 2 x 2592
+                                             ((4096, 24), 2, 0.5, 60.0)])    # 8748 = 2 x 4374 (configs[4])
+def test_cs_row_generator_cluster_pair_bitwise(tmp_path, dims, L, nu, alpha):
+    """Split-length CS row pass with one half line per CTA of a 2-CTA cluster (RK_CS_PAIR=1, the
+    Philox groups dealt to both CTAs, the other parity's elements sent over DSMEM) against the
+    one-CTA kernel (RK_CS_PAIR=0): bitwise identical unconditional fields."""
+    outs = []
+    for v in ("1", "0"):
+        out = str(tmp_path / f"cs{v}.npz")
+        code = CS_CODE.format(root=ROOT, out=out, dims=dims, L=L, nu=nu, alpha=alpha)
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RK_CS_PAIR=v), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs.append(dict(np.load(out)))
+    assert outs[0]["emb"][0] > 4608, outs[0]["emb"]
+    assert np.array_equal(outs[0]["f0"], outs[1]["f0"])
+    assert np.array_equal(outs[0]["f1"], outs[1]["f1"])
+    assert np.all(np.isfinite(outs[0]["f0"])) and np.abs(outs[0]["f0"]).max() > 0
