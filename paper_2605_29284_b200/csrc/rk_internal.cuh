@@ -115,6 +115,8 @@ struct Workspace {
   cudaEvent_t oev[kMaxChunks] = {};   // field row block k computed (its copy may start)
   double* ac_buf = nullptr;           // aliased-lag corrections: strips, partial sums, corrections (batch 1)
   size_t ac_cap = 0;
+  cudaStream_t aux2 = nullptr;        // the corrections run here, beside passes 1 and 2 (they only read c)
+  cudaEvent_t ac_fork = nullptr, ac_join = nullptr;
   cudaEvent_t join = nullptr;         // the side stream's last field copy issued
   double* cb_h = nullptr;       // pinned staging of c and beta (beta at beta_in - c_in)
   std::map<GraphKey, cudaGraphExec_t> hgraphs;

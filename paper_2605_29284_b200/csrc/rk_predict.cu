@@ -1547,6 +1547,24 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
     T = ws->T;
     U = ws->U;
   }
+  // execution torus: the aliased-lag corrections only read the input, so with a workspace they run
+  // on its second side stream beside passes 1 and 2 and are joined before pass 3
+  double* ac_owned = nullptr;
+  double* corr = nullptr;
+  int64_t cbs = 0;
+  bool ac_forked = false;
+  if (s->ac.nrp) {
+    if (row0 != s->grid.pad[2] || nout != s->m2 || col0 != s->grid.pad[0] || ncols != s->m1)
+      return Status::err(RK_INTERNAL, "execution-torus convolution for non-interior outputs");
+    static const bool ac_async = !(getenv("RK_AC_ASYNC") && atoi(getenv("RK_AC_ASYNC")) == 0);
+    if (ac_async && ws && batch == 1 && !ev) {
+      RK_CUDA_TRY(cudaEventRecord(ws->ac_fork, st));
+      RK_CUDA_TRY(cudaStreamWaitEvent(ws->aux2, ws->ac_fork, 0));
+      RK_TRY(alias_corrections(s, sp, rows, ld_in, in_bstride, batch, ws, ws->aux2, &corr, &cbs, &ac_owned));
+      RK_CUDA_TRY(cudaEventRecord(ws->ac_join, ws->aux2));
+      ac_forked = true;
+    }
+  }
   RowFwdArgs ra{};
   ra.pl = plan_pick(s->pl1v, (int64_t)((s->M2 + 1) / 2) * batch);
   ra.lpc = pick_lpc(ra.pl, 4, (int64_t)((s->M2 + 1) / 2) * batch);
@@ -1619,13 +1637,9 @@ static Status conv_pipeline(const rk_setup* s, const double* rows, int64_t ld_in
   }
   if (!done) RK_TRY(launch_col(0, ca, batch, st));
   if (ev) RK_CUDA_TRY(cudaEventRecord(ev[3], st));
-  double* ac_owned = nullptr;
   if (s->ac.nrp) {   // execution torus: exact only with the corrections, for the interior
-    if (row0 != s->grid.pad[2] || nout != s->m2 || col0 != s->grid.pad[0] || ncols != s->m1)
-      return Status::err(RK_INTERNAL, "execution-torus convolution for non-interior outputs");
-    double* corr = nullptr;
-    int64_t cbs = 0;
-    RK_TRY(alias_corrections(s, sp, rows, ld_in, in_bstride, batch, ws, st, &corr, &cbs, &ac_owned));
+    if (ac_forked) RK_CUDA_TRY(cudaStreamWaitEvent(st, ws->ac_join, 0));
+    else RK_TRY(alias_corrections(s, sp, rows, ld_in, in_bstride, batch, ws, st, &corr, &cbs, &ac_owned));
     epi.ac_corr = corr;
     epi.ac_cbs = cbs;
     epi.ac_row0 = 0;
@@ -1744,6 +1758,9 @@ static void free_ws(Workspace* w) {
   for (auto& g : w->graphs) cudaGraphExecDestroy(g.second);
   for (auto& g : w->hgraphs) cudaGraphExecDestroy(g.second);
   if (w->aux) cudaStreamDestroy(w->aux);
+  if (w->aux2) cudaStreamDestroy(w->aux2);
+  if (w->ac_fork) cudaEventDestroy(w->ac_fork);
+  if (w->ac_join) cudaEventDestroy(w->ac_join);
   if (w->fork) cudaEventDestroy(w->fork);
   if (w->join) cudaEventDestroy(w->join);
   cudaFree(w->ac_buf);
@@ -1794,6 +1811,9 @@ static Status get_ws(rk_setup* s, cudaStream_t st, Workspace** out) {
   RK_CUDA_TRY(cudaMalloc(&w->out, sizeof(double) * (size_t)s->m1 * s->m2));
   RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->cap, cudaStreamNonBlocking));
   RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->aux, cudaStreamNonBlocking));
+  RK_CUDA_TRY(cudaStreamCreateWithFlags(&w->aux2, cudaStreamNonBlocking));
+  RK_CUDA_TRY(cudaEventCreateWithFlags(&w->ac_fork, cudaEventDisableTiming));
+  RK_CUDA_TRY(cudaEventCreateWithFlags(&w->ac_join, cudaEventDisableTiming));
   RK_CUDA_TRY(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
   for (auto& e : w->xev) RK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : w->oev) RK_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
