@@ -432,13 +432,32 @@ __device__ __forceinline__ void fft_stage9_split(double2* __restrict__ buf, int 
 // spread plans, 1 WIDE (64-register kernels), 2 split radix-9 stages.
 // PSW: swizzled first pair of stages (fft_stage SWZ), a mask: 1 = power-of-two lines (8 8 ...),
 // 2 = lines starting 6 9 ... (each costs one more stage body in the kernel).
-template <bool INV, bool TWS = false, int FM = 0, bool MAG = true, int PSW = 0>   // MAG: magic-divisor modulo
+// FAM 1: the caller guarantees a line 6 9^a, a >= 2 (fft_family69) and PSW & 2: only those two stage
+// bodies are compiled in (the hot kernels are sensitive to their code size).
+inline bool fft_family69(const FftPlan& pl) { return pl.r3 == 6 && pl.n9 >= 2 && pl.n8 == 0 && pl.r2 == 1; }
+template <bool INV, bool TWS = false, int FM = 0, bool MAG = true, int PSW = 0, int FAM = 0>   // MAG: magic-divisor modulo
 __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPlan& pl, int t, int bid = 0) {
   constexpr bool WIDE = FM >= 1;   // split plans also keep the small register footprint elsewhere
   const int n = pl.n, nthr = pl.nthr;
   const double2* tw = pl.tw;   // stage 1 (Ns = 1) needs no twiddles and has no block
   const uint32_t* mg = reinterpret_cast<const uint32_t*>(pl.tw + pl.ntw - kFftMagicSlots);
   int Ns = 1, si = 0;   // si: stage index (magic divisors)
+  if (FAM == 1) {
+    static_assert(FAM != 1 || ((PSW & 2) && FM == 1 && MAG), "family kernels: WIDE, swizzled, magic divisors");
+    fft_stage<6, INV, TWS, WIDE, FftNoOp, FftNoOp, 3>(buf, n, 1, t, nthr, tw, 0u, bid);
+    fft_stage<9, INV, TWS, WIDE, FftNoOp, FftNoOp, 4>(buf, n, 6, t, nthr, tw, mg[1], bid);
+    tw += 6;
+    Ns = 54;
+    si = 2;
+#pragma unroll 1
+    for (int s = 1; s < pl.n9; ++s) {
+      fft_stage<9, INV, TWS, WIDE>(buf, n, Ns, t, nthr, tw, mg[si], bid);
+      tw += Ns;
+      Ns *= 9;
+      ++si;
+    }
+    return;
+  }
   // the radix-6 / 3 stage first: as the Ns = 1 stage it needs no twiddles, which keeps the WIDE
   // kernels' two-butterfly radix-6 stage inside 64 registers
   int s9 = 0;
@@ -504,7 +523,7 @@ __device__ __forceinline__ void fft_line(double2* __restrict__ buf, const FftPla
 // and the spectrum product after it).  Schedules {3 or 6} 9^n9 only (fft_line_pp_ok); the stage
 // arithmetic is fft_line's, so the transform is bitwise the same as hooks applied in passes.
 inline bool fft_line_pp_ok(const FftPlan& pl) { return pl.r3 > 1 && pl.n9 >= 1 && pl.n8 == 0 && pl.r2 == 1; }
-template <bool INV, bool TWS, int FM, class Pre, class Post, bool PSW = false>
+template <bool INV, bool TWS, int FM, class Pre, class Post, bool PSW = false, int FAM = 0>
 __device__ __forceinline__ void fft_line_pp(double2* __restrict__ buf, const FftPlan& pl, int t, int bid,
                                             const Pre& pre, const Post& post) {
   constexpr bool WIDE = FM >= 1;
@@ -512,19 +531,19 @@ __device__ __forceinline__ void fft_line_pp(double2* __restrict__ buf, const Fft
   const double2* tw = pl.tw;
   const uint32_t* mg = reinterpret_cast<const uint32_t*>(pl.tw + pl.ntw - kFftMagicSlots);
   int Ns, si = 1, s9 = 0;
-  if (pl.r3 == 6) {
-    if (PSW && pl.n9 >= 2) {   // swizzled radix-6 / first radix-9 pair, as fft_line
+  if (FAM == 1 || pl.r3 == 6) {
+    if (FAM == 1 || (PSW && pl.n9 >= 2)) {   // swizzled radix-6 / first radix-9 pair, as fft_line
       fft_stage<6, INV, TWS, WIDE, Pre, FftNoOp, 3>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
       fft_stage<9, INV, TWS, WIDE, FftNoOp, FftNoOp, 4>(buf, n, 6, t, nthr, tw, mg[1], bid);
       tw += 6;
       Ns = 54;
       si = 2;
       s9 = 1;
-    } else {
+    } else if (FAM != 1) {
       fft_stage<6, INV, TWS, WIDE, Pre, FftNoOp>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
       Ns = 6;
     }
-  } else {
+  } else if (FAM != 1) {
     fft_stage<3, INV, TWS, WIDE, Pre, FftNoOp>(buf, n, 1, t, nthr, tw, mg[0], bid, pre, FftNoOp());
     Ns = 3;
   }

@@ -630,6 +630,7 @@ constexpr int kSplitThreads = 512;   // the WIDE plan's threads per half line (n
 // The pair's two CTAs (a 2-CTA cluster) split the gather by nodes: each forms the sums of half
 // the pair's active nodes and writes them into both half lines (its own and, over DSMEM, its
 // partner's); the odd half then twists its copy by w_P^x.
+template <bool LEAN>   // LEAN: a line 6 9^a with the other stage bodies compiled out (fft_line FAM)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) row_fwd_split_kernel(const RowFwdArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   cg::cluster_group cl = cg::this_cluster();
@@ -706,7 +707,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
     for (int x = tl; x < a.ncols; x += nthr) buf[x] = cmul(buf[x], split_w(wt, x));
     __syncthreads();
   }
-  fft_line<false, true, 1, true, 3>(buf, pls, tl);
+  fft_line<false, true, 1, true, 3, LEAN ? 1 : 0>(buf, pls, tl);
   pdl_trigger();
   // Z[kx], kx = 2 mm + half, is buf[mm]; conj Z[P - kx] comes from the same half
   const int Hf = H + 1;
@@ -733,6 +734,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
 
 // pass 2: column kx, this CTA's half (cluster rank) -> x real-even spectrum -> inverse half;
 // the cluster's two halves are combined over DSMEM, each CTA finishing half the kept rows
+// LEAN: the default configuration on a line 6 9^a (fused hooks, standard U, no fold) with everything
+// else compiled out
+template <bool LEAN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) col_split_kernel(const ColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   cg::cluster_group cl = cg::this_cluster();
@@ -764,16 +768,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
   for (int y = a.nin + tl; y < H; y += nthr) buf[y] = make_double2(0.0, 0.0);
   mbar_wait(bar, 0);
   __syncthreads();
-  if (a.fold) {   // rows y >= H: X[2m] = F_H(x[n] + x[n + H]), X[2m + 1] = F_H((x[n] - x[n + H]) w^n)
+  if (!LEAN && a.fold) {   // rows y >= H: X[2m] = F_H(x[n] + x[n + H]), X[2m + 1] = F_H((x[n] - x[n + H]) w^n)
     for (int n = tl; n < a.fold; n += nthr) buf[n] = half ? csub(buf[n], buf[H + n]) : cadd(buf[n], buf[H + n]);
     __syncthreads();
   }
   const int nin_h = min(a.nin, H);
   // S[k] for k = 2 mm + half: S_half[min(mm, H - half - mm)]
-  if (a.fuse_pp) {   // the odd half's twist on the first stage's loads, the product on the last stage's stores
+  if (LEAN || a.fuse_pp) {   // the odd half's twist on the first stage's loads, the product on the last stage's stores
     auto pre_tw = [&](int y, double2 v) { return half ? cmul(v, split_w(wt, y)) : v; };
     auto post_sp = [&](int mm, double2 v) { return cscale(v, S[min(mm, H - half - mm)]); };
-    fft_line_pp<false, true, 1, decltype(pre_tw), decltype(post_sp), true>(buf, pls, tl, 0, pre_tw, post_sp);
+    fft_line_pp<false, true, 1, decltype(pre_tw), decltype(post_sp), true, LEAN ? 1 : 0>(buf, pls, tl, 0, pre_tw,
+                                                                                        post_sp);
   } else {
     if (half) {
       for (int y = tl; y < nin_h; y += nthr) buf[y] = cmul(buf[y], split_w(wt, y));
@@ -783,11 +788,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) co
     for (int mm = tl; mm < H; mm += nthr) buf[mm] = cscale(buf[mm], S[min(mm, H - half - mm)]);
     __syncthreads();
   }
-  fft_line<true, true, 1, true, 3>(buf, pls, tl);
+  fft_line<true, true, 1, true, 3, LEAN ? 1 : 0>(buf, pls, tl);
   pdl_trigger();
   cl.sync();   // both halves transformed
   const double2* other = cl.map_shared_rank(buf, half ^ 1);
-  if (a.upair) {   // pair-blocked U: each thread finishes one U row pair (32 contiguous bytes)
+  if (!LEAN && a.upair) {   // pair-blocked U: each thread finishes one U row pair (32 contiguous bytes)
     const int nq = (a.nout + 1) >> 1, qm = (nq + 1) >> 1;
     const int q0 = half ? qm : 0, q1 = half ? nq : qm;
     double2* Ub = a.U + (int64_t)b * a.U_bstride + (int64_t)(kx & 1) * 2 * a.hh + 2 * (kx >> 1);
@@ -967,6 +972,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MAXT, 2) col_split_c
 // pass 3: Hermitian pair of interior rows -> this CTA's half spectrum (Z[k], k % 2 == half) ->
 // inverse half; the cluster combines the halves over DSMEM, each CTA finishing half the
 // kept columns (fixed-part / draw epilogue)
+template <bool LEAN>   // LEAN: a line 6 9^a, standard U, the other code compiled out
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) row_inv_split_kernel(const RowInvArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   cg::cluster_group cl = cg::this_cluster();
@@ -998,7 +1004,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
       const int mm = base + d * nthr;
       A[d] = B[d] = make_double2(0.0, 0.0);
       if (mm < nk) {
-        if (a.upair) {   // the pair's parity run: contiguous 32-byte records
+        if (!LEAN && a.upair) {   // the pair's parity run: contiguous 32-byte records
           const double2* u = U + (int64_t)(ya >> 1) * a.ldp + (int64_t)half * 2 * a.hh + 2 * mm;
           A[d] = u[0];
           B[d] = u[1];
@@ -1020,7 +1026,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSplitThreads, 2) ro
     }
   }
   __syncthreads();
-  fft_line<true, true, 1, true, 3>(buf, pls, tl);
+  fft_line<true, true, 1, true, 3, LEAN ? 1 : 0>(buf, pls, tl);
   cl.sync();   // both halves transformed
   const double2* other = cl.map_shared_rank(buf, half ^ 1);
   const double* beta = a.beta ? a.beta + (int64_t)b * a.p : nullptr;
@@ -1234,6 +1240,13 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
 }
 
 // split-length launches (see row_fwd_split_kernel); *done = false when the layout does not fit
+// the split-length kernels' LEAN instantiations: lines 6 9^a (4374: the halves of the 8748 torus),
+// every other stage body and option compiled out (RK_LEAN=0: the general kernels)
+static bool lean_family(const FftPlan& pl) {
+  static const bool lean_env = !(getenv("RK_LEAN") && atoi(getenv("RK_LEAN")) == 0);
+  return lean_env && fft_family69(pl);
+}
+
 static inline size_t split_tail(size_t bytes, const FftPlan& pl, SplitTw* sw, int* tw_off) {
   *tw_off = tw_slot(bytes);
   bytes = (size_t)*tw_off * 16 + (size_t)pl.ntw * 16;
@@ -1251,9 +1264,14 @@ static Status launch_row_fwd_split(const RowFwdArgs& a0, int batch, cudaStream_t
   smem = (size_t)a.prod_off * 16 + sizeof(double) * 2 * (size_t)a.prod_cap;
   smem = split_tail(smem, a.pl, &a.sw, &a.tw_off);
   if (smem > kSmemMax) return Status::ok();
-  RK_TRY(set_smem_attr((const void*)row_fwd_split_kernel, smem));
   const dim3 grid((unsigned)(2 * ((a.nrows + 1) / 2)), (unsigned)batch);
-  row_fwd_split_kernel<<<grid, a.pl.nthr, smem, st>>>(a);
+  if (lean_family(a.pl)) {
+    RK_TRY(set_smem_attr((const void*)row_fwd_split_kernel<true>, smem));
+    row_fwd_split_kernel<true><<<grid, a.pl.nthr, smem, st>>>(a);
+  } else {
+    RK_TRY(set_smem_attr((const void*)row_fwd_split_kernel<false>, smem));
+    row_fwd_split_kernel<false><<<grid, a.pl.nthr, smem, st>>>(a);
+  }
   count_launch();
   RK_LAUNCH_CHECK();
   *done = true;
@@ -1273,9 +1291,14 @@ static Status launch_col_split(const ColArgs& a0, int batch, cudaStream_t st, bo
   if (smem > kSmemMax) return Status::ok();
   static const bool fuse = !(getenv("RK_FUSE_PP") && atoi(getenv("RK_FUSE_PP")) == 0);
   a.fuse_pp = fuse && fft_line_pp_ok(a.pl);
-  RK_TRY(set_smem_attr((const void*)col_split_kernel, smem));
   const dim3 grid((unsigned)(2 * a.ncols), (unsigned)batch);
-  col_split_kernel<<<grid, a.pl.nthr, smem, st>>>(a);
+  if (lean_family(a.pl) && a.fuse_pp && !a.upair && a.fold == 0) {
+    RK_TRY(set_smem_attr((const void*)col_split_kernel<true>, smem));
+    col_split_kernel<true><<<grid, a.pl.nthr, smem, st>>>(a);
+  } else {
+    RK_TRY(set_smem_attr((const void*)col_split_kernel<false>, smem));
+    col_split_kernel<false><<<grid, a.pl.nthr, smem, st>>>(a);
+  }
   count_launch();
   RK_LAUNCH_CHECK();
   *done = true;
@@ -1351,9 +1374,14 @@ static Status launch_row_inv_split(const RowInvArgs& a0, int batch, cudaStream_t
   a.ep_off = tw_slot(smem);   // the exit-protection mbarrier
   smem = (size_t)a.ep_off * 16 + 16;
   if (smem > kSmemMax) return Status::ok();
-  RK_TRY(set_smem_attr((const void*)row_inv_split_kernel, smem));
   const dim3 grid((unsigned)(2 * ((a.nrows + 1) / 2)), (unsigned)batch);
-  row_inv_split_kernel<<<grid, a.pl.nthr, smem, st>>>(a);
+  if (lean_family(a.pl) && !a.upair) {
+    RK_TRY(set_smem_attr((const void*)row_inv_split_kernel<true>, smem));
+    row_inv_split_kernel<true><<<grid, a.pl.nthr, smem, st>>>(a);
+  } else {
+    RK_TRY(set_smem_attr((const void*)row_inv_split_kernel<false>, smem));
+    row_inv_split_kernel<false><<<grid, a.pl.nthr, smem, st>>>(a);
+  }
   count_launch();
   RK_LAUNCH_CHECK();
   *done = true;

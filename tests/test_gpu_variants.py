@@ -281,3 +281,14 @@ def test_cs_row_generator_cluster_pair_bitwise(tmp_path, dims, L, nu, alpha):
     assert np.array_equal(outs[0]["f0"], outs[1]["f0"])
     assert np.array_equal(outs[0]["f1"], outs[1]["f1"])
     assert np.all(np.isfinite(outs[0]["f0"])) and np.abs(outs[0]["f0"]).max() > 0
+
+
+def test_lean_split_kernels_bitwise(tmp_path):
+    """The 6 9^a-only instantiations of the split-length passes (default on the 8748 torus) against
+    the general kernels (RK_LEAN=0): the same stage bodies, bitwise identical."""
+    kw = dict(n=6000, L=2, dims=(4096, 4096), nu=1.5)
+    a = _run(tmp_path, "lean", {"RK_LEAN": "1"}, **kw)
+    b = _run(tmp_path, "general", {"RK_LEAN": "0"}, **kw)
+    assert tuple(a["embed"]) == (8748, 8748)
+    assert np.array_equal(a["field"], b["field"])
+    assert np.array_equal(a["conv"], b["conv"])
