@@ -375,7 +375,8 @@ struct ColArgs {
   int ct_off;                // smem offset (double2 units) where its twiddles are staged
 };
 
-template <int MODE, bool TWS, int FM>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
+// FAM 1 (WIDE filter mode only): lines 6 9^a with the other stage bodies compiled out (fft_line FAM)
+template <int MODE, bool TWS, int FM, int FAM = 0>  // MODE 0 = filter (fwd, x spectrum, inv, crop), 1 = spectrum (fwd, real part)
 __global__ void RK_FFT_BOUNDS(FM) col_kernel(const ColArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   const int n = a.pl.n;
@@ -417,13 +418,13 @@ __global__ void RK_FFT_BOUNDS(FM) col_kernel(const ColArgs a) {
   mbar_wait(bar, 0);
   __syncthreads();
   RK_PHASE(1, 1);
-  fft_line<false, TWS, FM, true, FM == 1 ? 3 : 0>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+  fft_line<false, TWS, FM, true, FM == 1 ? 3 : 0, FAM>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
   RK_PHASE(1, 2);
   if (MODE == 0) {
     const double* S = specs + (size_t)line * a.ldq;
     for (int ky = tl; ky < n; ky += nthr) buf[ky] = cscale(buf[ky], valid ? S[min(ky, n - ky)] : 0.0);
     group_sync(a.lpc > 1 ? 1 + line : 0, nthr);
-    fft_line<true, TWS, FM, true, FM == 1 ? 3 : 0>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
+    fft_line<true, TWS, FM, true, FM == 1 ? 3 : 0, FAM>(buf, pls, tl, a.lpc > 1 ? 1 + line : 0);
     RK_PHASE(1, 3);
     pdl_trigger();
     // TMA bulk store of the kept rows
@@ -1147,6 +1148,13 @@ static inline Status wide_needs_tws(const FftPlan& pl, bool tws) {
   return Status::ok();
 }
 
+// LEAN instantiations of the split-length kernels and the WIDE column pass: lines 6 9^a (4374: the halves of the 8748 torus),
+// every other stage body and option compiled out (RK_LEAN=0: the general kernels)
+static bool lean_family(const FftPlan& pl) {
+  static const bool lean_env = !(getenv("RK_LEAN") && atoi(getenv("RK_LEAN")) == 0);
+  return lean_env && fft_family69(pl);
+}
+
 static Status launch_row_fwd(int src, const RowFwdArgs& a0, int batch, cudaStream_t st) {
   RowFwdArgs a = a0;
   const int pairs = (a.nrows + 1) / 2;
@@ -1201,7 +1209,8 @@ static Status launch_col(int mode, const ColArgs& a0, int batch, cudaStream_t st
   const bool tws = tw_fits(smem, a.pl);
   if (tws) smem = with_tw(smem, a.pl);
   RK_TRY(wide_needs_tws(a.pl, tws));
-  auto kern = a.pl.wide == 2 ? (mode == 0 ? col_kernel<0, true, 1> : col_kernel<1, true, 1>)
+  auto kern = a.pl.wide == 2 ? (mode == 0 ? (lean_family(a.pl) ? col_kernel<0, true, 1, 1> : col_kernel<0, true, 1>)
+                                          : col_kernel<1, true, 1>)
               : a.pl.wide == 3 ? (mode == 0 ? col_kernel<0, true, 2> : col_kernel<1, true, 2>)
               : mode == 0 ? (tws ? col_kernel<0, true, 0> : col_kernel<0, false, 0>)
                           : (tws ? col_kernel<1, true, 0> : col_kernel<1, false, 0>);
@@ -1240,13 +1249,6 @@ static Status launch_row_inv(const RowInvArgs& a0, int batch, cudaStream_t st) {
 }
 
 // split-length launches (see row_fwd_split_kernel); *done = false when the layout does not fit
-// the split-length kernels' LEAN instantiations: lines 6 9^a (4374: the halves of the 8748 torus),
-// every other stage body and option compiled out (RK_LEAN=0: the general kernels)
-static bool lean_family(const FftPlan& pl) {
-  static const bool lean_env = !(getenv("RK_LEAN") && atoi(getenv("RK_LEAN")) == 0);
-  return lean_env && fft_family69(pl);
-}
-
 static inline size_t split_tail(size_t bytes, const FftPlan& pl, SplitTw* sw, int* tw_off) {
   *tw_off = tw_slot(bytes);
   bytes = (size_t)*tw_off * 16 + (size_t)pl.ntw * 16;
