@@ -9,7 +9,7 @@ import subprocess
 LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2605_29284_b200",
                    "librapidkrig_b200.so")
 KERNELS = ["row_fwd_split_kernel", "col_split_kernel", "row_inv_split_kernel", "weights_kernel_mma<4, true>",
-           "col_kernel<0, true, 1>", "row_fwd_kernel<3, true, 1>", "row_inv_kernel<true, 1>",
+           "col_kernel<0, true, 1, 1>", "row_fwd_kernel<3, true, 1>", "row_inv_kernel<true, 1>",
            "cs_rowgen_kernel<false, 1, 288, 4, true>", "cs_rowgen_split_kernel<true>", "trmm_panel_kernel<false, 1>"]
 KEYS = ["UBLKCP", "UTMALDG", "UTMASTG", "SYNCS", "UCGABAR", "BAR.SYNC", "DMMA", "DFMA", "SHFL", "LDG.E.ENL2.256", "STG.E.ENL2.256",
         "STL", "LDL"]
